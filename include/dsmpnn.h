@@ -1,0 +1,234 @@
+/*
+ * dsmpnn.h - C ABI of libdsmpnn.so, the B200 (sm_100a) hot path of DS-MPNN
+ * (arXiv 2402.15106): the edge-conditioned message-passing layer on
+ * ball-radius graphs over Nystrom-sampled nodes of overlapping sub-domains.
+ *
+ * Citations are PAPER.md:<line> of the paper's LaTeX source; "R<n>" are the
+ * readings listed in DESIGN.md §2.
+ *
+ * Conventions (all calls):
+ *  - Every call returns dsmpnn_status; DSMPNN_OK == 0.  On error, a text is
+ *    available from dsmpnn_last_error() (thread-local).  No call aborts.
+ *  - Pointers are DEVICE pointers unless the argument says "host".  The caller
+ *    owns every buffer (it allocates them, e.g. with PyTorch); the library never
+ *    frees or retains them past the enqueued work.
+ *  - `stream` is a cudaStream_t passed as void*; NULL is the legacy default
+ *    stream.  Calls are stream-ordered and asynchronous, except where a
+ *    "host" output is requested (then the call synchronises `stream`).
+ *  - Layouts are row-major and contiguous.  Index types: int64 row_ptr and
+ *    global ids, int32 local column indices.
+ *  - Workspace: calls that need scratch take (ws, ws_bytes) sized by the
+ *    matching *_workspace_size query; DSMPNN_ERR_CAPACITY is returned if it
+ *    is too small.
+ *  - Determinism: equal inputs give bit-equal outputs on every run (no
+ *    floating-point atomics on any result).
+ */
+#ifndef DSMPNN_H
+#define DSMPNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DSMPNN_OK = 0,
+  DSMPNN_ERR_INVALID_ARG = -1, /* r<=0, s<1, n_e<1, P not 2^m or P>n, dim not 2/3, ... */
+  DSMPNN_ERR_SHAPE = -2,       /* width mismatch, ROOT_IDENTITY with d_in!=d_out, misalignment */
+  DSMPNN_ERR_INDEX = -3,       /* index out of range */
+  DSMPNN_ERR_CAPACITY = -4,    /* output or workspace buffer too small */
+  DSMPNN_ERR_CUDA = -5,        /* a CUDA runtime error (text in dsmpnn_last_error) */
+  DSMPNN_ERR_UNSUPPORTED = -8, /* shape/dtype combination not implemented */
+  DSMPNN_ERR_DEGENERATE = -9   /* RCB split leaves an empty side (R12) */
+} dsmpnn_status;
+
+typedef enum { DSMPNN_F32 = 0, DSMPNN_BF16 = 1 } dsmpnn_dtype;
+typedef enum { DSMPNN_ROOT_NONE = 0, DSMPNN_ROOT_IDENTITY = 1, DSMPNN_ROOT_DENSE = 2 } dsmpnn_root;
+typedef enum { DSMPNN_ACT_IDENTITY = 0, DSMPNN_ACT_RELU = 1 } dsmpnn_act;
+typedef enum { DSMPNN_EDGE_DIFF = 0, DSMPNN_EDGE_CONCAT = 1 } dsmpnn_edge_mode;
+
+/* Layer description.  kappa_phi (R5) = Linear(d_e,k) -> ReLU -> Linear(k,k)
+ * -> ReLU -> Linear(k, d_in*d_out); K[c][o] = kappa_out[c*d_out+o] (R4). */
+typedef struct {
+  int32_t d_e, d_in, d_out, k;
+  int32_t dtype; /* dsmpnn_dtype: F32 = fp32 SIMT arithmetic; BF16 = tcgen05 bf16 MMA, fp32 accumulate */
+  int32_t root;  /* dsmpnn_root (R2) */
+  int32_t act;   /* dsmpnn_act (R1) */
+  int32_t reserved;
+} dsmpnn_layer_desc;
+
+/* fp32 master weights in PyTorch Linear layout [out, in] (device). */
+typedef struct {
+  const float *W1, *b1;         /* [k x d_e], [k] */
+  const float *W2, *b2;         /* [k x k], [k] */
+  const float *W3, *b3;         /* [d_in*d_out x k], [d_in*d_out] */
+  const float *W_root, *b;      /* [d_out x d_in] (ROOT_DENSE only, else may be NULL), [d_out] */
+  const void *packed;           /* BF16 mode: buffer filled by dsmpnn_pack_weights (required) */
+} dsmpnn_weights;
+
+/* fp32 weight gradients, ACCUMULATED (+=) by dsmpnn_layer_bwd. Any may be NULL. */
+typedef struct {
+  float *W1, *b1, *W2, *b2, *W3, *b3, *W_root, *b;
+} dsmpnn_grads;
+
+const char *dsmpnn_last_error(void);
+int32_t dsmpnn_version(void);
+
+/* ------------------------------------------------------------------ a1 --- */
+/* Nystrom node sampling ("randomly sampling nodes, |V_s| = s";
+ * Alg. 1 :391).  R9: the min(s,N) ids g in [0,N) with the smallest
+ * (key_node(seed,g), g), key_node = smx(smx(seed) ^ g), written ascending.
+ * ids: int32[min(s,N)].  Errors: s < 1 or N < 0 -> INVALID_ARG. */
+dsmpnn_status dsmpnn_sample_workspace_size(int64_t n_points, size_t *bytes /*host*/);
+dsmpnn_status dsmpnn_sample(int64_t n_points, int64_t s, uint64_t seed, int32_t *ids,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ a2 --- */
+/* Radius graph kernel + random edge cap (Alg. 1 :395-396).
+ * For each destination row i < n_dst: candidates C_i = {j < n_loc, j != i :
+ * pred_fp32(x_i, x_j, r)} (R7, inclusive, no FMA); if |C_i| > n_e keep the n_e
+ * smallest (key_edge(seed, gid_i, gid_j), gid_j) (R10); the row is ordered by
+ * gid_j ascending (R11).  Cell-list search over cells of edge r(1+2^-8).
+ *   coords   float32[n_loc x dim] (dim 2 or 3), local order
+ *   gid      int64[n_loc] global ids (unique)
+ *   row_ptr  int64[n_dst+1] (out), col_idx int32[col_capacity] (out, local ids)
+ *   n_edges  host int64 out (may be NULL: then the call stays asynchronous and
+ *            row_ptr[n_dst] holds the count); if col_capacity < E the call
+ *            returns CAPACITY and *n_edges holds E (requires n_edges != NULL).
+ * Errors: r <= 0, n_e < 1, dim not in {2,3}, n_dst > n_loc -> INVALID_ARG. */
+dsmpnn_status dsmpnn_radius_graph_workspace_size(int64_t n_loc, int64_t n_dst, int dim, size_t *bytes);
+dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64_t n_loc, int64_t n_dst,
+                                  int dim, float r, int32_t n_e, uint64_t seed, int64_t *row_ptr,
+                                  int32_t *col_idx, int64_t col_capacity, int64_t *n_edges /*host*/,
+                                  void *ws, size_t ws_bytes, void *stream);
+
+/* Candidate counts |C_i| (pre-cap) per destination row; same search as above.
+ * counts int32[n_dst].  Used for diagnostics and tests. */
+dsmpnn_status dsmpnn_radius_counts(const float *coords, int64_t n_loc, int64_t n_dst, int dim, float r,
+                                   int32_t *counts, void *ws, size_t ws_bytes, void *stream);
+
+/* CSC view of a CSR graph for deterministic scatters (backward a7):
+ * csc_perm int32[E] = edge ids sorted by (col_idx, edge id); csc_ptr int64[n_loc+1]. */
+dsmpnn_status dsmpnn_csc_workspace_size(int64_t n_edges, int64_t n_loc, size_t *bytes);
+dsmpnn_status dsmpnn_csc(const int32_t *col_idx, int64_t n_edges, int64_t n_loc, int32_t *csc_perm,
+                         int64_t *csc_ptr, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ a3 --- */
+/* Domain decomposition with overlap l ("extended overlap of
+ * length l", :70 "equally partitioned based on their coordinates"; Alg. 1
+ * :392, :403).  R12 median RCB on the longest axis, ties to the lower rank;
+ * R13 closed L-inf box extension by l; R23 near/deep split at
+ * t = fl(max(l,r)(1+2^-10)) from internal faces.  Computes the plan of `rank`:
+ *   owner      int32[n]            owner rank of every sampled point
+ *   boxes      float32[P x 2 x dim] lo/hi per rank
+ *   internal   uint8[P x 2 x dim]   1 if that face was created by a split
+ *   local_rows int64[n] (capacity)  indices into the n points, local order
+ *                                   deep (gid asc) | near (gid asc) | halo (owner asc, gid asc)
+ *   counts     int64[4 + 2(P+1)]    n_deep, n_near, n_halo, n_send_total,
+ *                                   halo_ptr[P+1] (absolute local rows, halo_ptr[0] = n_own),
+ *                                   send_ptr[P+1] (offsets into send_idx)
+ *   send_idx   int32[n*(P-1)] (capacity; n if P == 1): local rows sent to each q,
+ *                                   q ascending, gid ascending within q
+ *   counts_host host int64[4 + 2(P+1)] copy of counts (may be NULL: asynchronous)
+ * Errors: P not a power of two or P > n, l < 0, r <= 0 -> INVALID_ARG;
+ * DEGENERATE if a split leaves an empty side (only detected when
+ * counts_host != NULL, which synchronises). */
+dsmpnn_status dsmpnn_partition_workspace_size(int64_t n, int dim, int nparts, size_t *bytes);
+dsmpnn_status dsmpnn_partition(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
+                               float overlap_l, float radius, int rank, int32_t *owner, float *boxes,
+                               uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
+                               int64_t *counts_host, void *ws, size_t ws_bytes, void *stream);
+
+/* Gather rows (local order) of a float32 array: out[k] = in[rows[k]].  Used to
+ * form local coordinates / attributes / global ids from a plan. elem_bytes 4 or 8. */
+dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
+                                 int32_t elem_bytes, void *out, void *stream);
+
+/* Edge attributes ("relative difference between node coordinates
+ * and attributes"; Alg. 1 :397; R21).  For edge p of row i with source j:
+ *   DIFF:   e_p = (x_i - x_j, a_i - a_j)            d_e = dim + n_attr
+ *   CONCAT: e_p = (x_i, x_j, a_i, a_j)              d_e = 2(dim + n_attr)
+ * Each value is one fp32 operation or a copy.  Writes e32 float32[E x d_e]
+ * and/or e16 bf16[E x 16] (zero-padded to 16 columns; d_e <= 16), either may be NULL. */
+dsmpnn_status dsmpnn_edge_features(int32_t mode, const float *coords, int dim, const float *attr, int n_attr,
+                                   const int64_t *row_ptr, const int32_t *col_idx, int64_t n_dst,
+                                   int64_t n_edges, float *e32, void *e16, void *stream);
+
+/* -------------------------------------------------------------- a4 + a5 --- */
+/* Bytes of the bf16 packed-weight buffer, and packing (BF16 mode). */
+dsmpnn_status dsmpnn_packed_weights_size(const dsmpnn_layer_desc *desc, size_t *bytes);
+dsmpnn_status dsmpnn_pack_weights(const dsmpnn_layer_desc *desc, const dsmpnn_weights *w, void *packed,
+                                  size_t bytes, void *stream);
+
+/* Layer forward, Eq. (1) / eq. (ii) (:40) with Alg. 1's residual
+ * (:407-409) and the north_star root/sigma (R1-R5):
+ *   out_i = sigma( [deg_i>0] (1/deg_i) sum_{p in row i} K_p^T v_{j(p)} + root(v_i) + b )
+ * for destination rows [row_begin, row_end).  K_p is never materialised: the
+ * row sum is contracted as vec(sum_p h~_p (x) v_j) . Theta~.
+ *   v        [n_loc x d_in]  fp32 (F32) or bf16 (BF16); rows 0..n_dst-1 are the destinations
+ *   e        [E x d_e] fp32 (F32) or [E x 16] bf16 zero-padded (BF16)
+ *   row_ptr  int64[n_dst+1] device; row_ptr_host: host copy (may be NULL: then the
+ *            call reads row_ptr[row_begin], row_ptr[row_end] synchronously)
+ *   col_idx  int32[E]
+ *   out      float32[n_dst x d_out] (rows row_begin.. written)
+ *   out_lowp bf16[n_dst x d_out] copy of out, or NULL
+ *   ws       saved activations for dsmpnn_layer_bwd, sized by
+ *            dsmpnn_layer_workspace_size(desc, n_dst, E); pass the same ws to bwd.
+ * Errors: SHAPE for ROOT_IDENTITY with d_in != d_out or BF16 with d_e > 16;
+ * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64}, k in {64,128,256}. */
+dsmpnn_status dsmpnn_layer_workspace_size(const dsmpnn_layer_desc *desc, int64_t n_dst, int64_t n_edges,
+                                          size_t *bytes);
+dsmpnn_status dsmpnn_layer_fwd(const dsmpnn_layer_desc *desc, const dsmpnn_weights *w, const void *v,
+                               const void *e, const int64_t *row_ptr, const int64_t *row_ptr_host,
+                               const int32_t *col_idx, int64_t n_dst, int64_t row_begin, int64_t row_end,
+                               float *out, void *out_lowp, void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ a7 --- */
+/* Layer backward (Alg. 1 :417 "Backprop", local gradients; R16 detach).
+ * Given grad_out = dL/dout (fp32 [n_dst x d_out], rows [row_begin,row_end)
+ * used), accumulates:
+ *   grad_v [n_loc x d_in] fp32  +=  dL/dv (root term on destination rows and
+ *                                   messages on source rows, incl. halo rows)
+ *   grad_e [E x d_e] fp32       =   dL/de for edges of the rows (NULL: skipped)
+ *   grads                       +=  weight gradients (fp32)
+ * csc_perm/csc_ptr from dsmpnn_csc (deterministic scatter to source rows).
+ * ws: the workspace passed to the matching dsmpnn_layer_fwd (unmodified);
+ * bwd_ws: scratch sized by dsmpnn_layer_bwd_workspace_size. */
+dsmpnn_status dsmpnn_layer_bwd_workspace_size(const dsmpnn_layer_desc *desc, int64_t n_dst, int64_t n_loc,
+                                              int64_t n_edges, size_t *bytes);
+dsmpnn_status dsmpnn_layer_bwd(const dsmpnn_layer_desc *desc, const dsmpnn_weights *w, const void *v,
+                               const void *e, const int64_t *row_ptr, const int64_t *row_ptr_host,
+                               const int32_t *col_idx, const int32_t *csc_perm, const int64_t *csc_ptr,
+                               int64_t n_dst, int64_t n_loc, int64_t row_begin, int64_t row_end,
+                               const float *grad_out, float *grad_v, float *grad_e, const dsmpnn_grads *grads,
+                               const void *ws, void *bwd_ws, size_t bwd_ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ a6 --- */
+/* Halo exchange building blocks ("the overlap area of a given
+ * domain is updated from the neighboring domains' interiors"; Alg. 1 :411).
+ * The plan makes every receive slice contiguous, so a FORWARD exchange is:
+ * gather the send rows into a contiguous buffer, transfer (NCCL send/recv via
+ * torch.distributed, or a device copy between virtual ranks), done.  The
+ * REVERSE_ADD direction gathers the contiguous halo slice, transfers it, and
+ * scatter-adds it into the owner's send rows in ascending peer order.
+ * width elements of dtype (F32 or BF16) per row. */
+dsmpnn_status dsmpnn_halo_gather(const void *values, const int32_t *rows, int64_t n_rows, int32_t width,
+                                 int32_t dtype, void *out, void *stream);
+dsmpnn_status dsmpnn_halo_scatter_add(const float *in, const int32_t *rows, int64_t n_rows, int32_t width,
+                                      float *values, void *stream);
+
+/* Loopback exchange among P virtual ranks resident on ONE device (no NCCL):
+ * for every ordered pair (p -> q), values[q][halo_ptr_q[p] .. halo_ptr_q[p+1])
+ * <- values[p][send_idx_p[send_ptr_p[q] .. send_ptr_p[q+1])].
+ * values, send_idx: host arrays of P device pointers; halo_ptr, send_ptr:
+ * host arrays of P host pointers to int64[P+1]. */
+dsmpnn_status dsmpnn_halo_exchange_loopback(int32_t nparts, void *const *values, const int64_t *const *halo_ptr,
+                                            const int64_t *const *send_ptr, const int32_t *const *send_idx,
+                                            int32_t width, int32_t dtype, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSMPNN_H */

@@ -1,0 +1,266 @@
+"""ctypes binding of libdsmpnn.so (include/dsmpnn.h).  Argument marshalling only.
+
+Every function here has the name of the C entry point without the ``dsmpnn_``
+prefix and takes torch tensors (device memory) plus plain Python scalars.  A
+non-OK status raises ``DsmpnnError`` with the library's error text.  If the
+shared library is missing, importing this module raises: there is no fallback.
+"""
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdsmpnn.so")
+
+F32, BF16 = 0, 1
+ROOT_NONE, ROOT_IDENTITY, ROOT_DENSE = 0, 1, 2
+ACT_IDENTITY, ACT_RELU = 0, 1
+EDGE_DIFF, EDGE_CONCAT = 0, 1
+
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "SHAPE", -3: "INDEX", -4: "CAPACITY", -5: "CUDA",
+          -8: "UNSUPPORTED", -9: "DEGENERATE"}
+
+
+class DsmpnnError(RuntimeError):
+    def __init__(self, status, where, text):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {text}")
+        self.status = status
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libdsmpnn.so not found at {LIB_PATH}; run `python -m paper_2402_15106_b200.build` "
+                      "(no CPU fallback exists)")
+_lib = C.CDLL(LIB_PATH)
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+U64 = C.c_uint64
+F = C.c_float
+SZ = C.c_size_t
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("d_e", I32), ("d_in", I32), ("d_out", I32), ("k", I32), ("dtype", I32), ("root", I32),
+                ("act", I32), ("reserved", I32)]
+
+
+class Weights(C.Structure):
+    _fields_ = [("W1", P), ("b1", P), ("W2", P), ("b2", P), ("W3", P), ("b3", P), ("W_root", P), ("b", P),
+                ("packed", P)]
+
+
+class Grads(C.Structure):
+    _fields_ = [("W1", P), ("b1", P), ("W2", P), ("b2", P), ("W3", P), ("b3", P), ("W_root", P), ("b", P)]
+
+
+def _sig(name, *args):
+    f = getattr(_lib, "dsmpnn_" + name)
+    f.restype = C.c_int
+    f.argtypes = list(args)
+    return f
+
+
+_lib.dsmpnn_last_error.restype = C.c_char_p
+_lib.dsmpnn_version.restype = C.c_int32
+
+_f = {
+    "sample_workspace_size": _sig("sample_workspace_size", I64, C.POINTER(SZ)),
+    "sample": _sig("sample", I64, I64, U64, P, P, SZ, P),
+    "radius_graph_workspace_size": _sig("radius_graph_workspace_size", I64, I64, C.c_int, C.POINTER(SZ)),
+    "radius_graph": _sig("radius_graph", P, P, I64, I64, C.c_int, F, I32, U64, P, P, I64, C.POINTER(I64), P, SZ, P),
+    "radius_counts": _sig("radius_counts", P, I64, I64, C.c_int, F, P, P, SZ, P),
+    "csc_workspace_size": _sig("csc_workspace_size", I64, I64, C.POINTER(SZ)),
+    "csc": _sig("csc", P, I64, I64, P, P, P, SZ, P),
+    "partition_workspace_size": _sig("partition_workspace_size", I64, C.c_int, C.c_int, C.POINTER(SZ)),
+    "partition": _sig("partition", P, P, I64, C.c_int, C.c_int, F, F, C.c_int, P, P, P, P, P, P, P, P, SZ, P),
+    "gather_rows": _sig("gather_rows", P, P, I64, I64, I32, P, P),
+    "edge_features": _sig("edge_features", I32, P, C.c_int, P, C.c_int, P, P, I64, I64, P, P, P),
+    "packed_weights_size": _sig("packed_weights_size", C.POINTER(LayerDesc), C.POINTER(SZ)),
+    "pack_weights": _sig("pack_weights", C.POINTER(LayerDesc), C.POINTER(Weights), P, SZ, P),
+    "layer_workspace_size": _sig("layer_workspace_size", C.POINTER(LayerDesc), I64, I64, C.POINTER(SZ)),
+    "layer_fwd": _sig("layer_fwd", C.POINTER(LayerDesc), C.POINTER(Weights), P, P, P, P, P, I64, I64, I64, P, P, P,
+                      SZ, P),
+    "layer_bwd_workspace_size": _sig("layer_bwd_workspace_size", C.POINTER(LayerDesc), I64, I64, I64, C.POINTER(SZ)),
+    "layer_bwd": _sig("layer_bwd", C.POINTER(LayerDesc), C.POINTER(Weights), P, P, P, P, P, P, P, I64, I64, I64, I64,
+                      P, P, P, C.POINTER(Grads), P, P, SZ, P),
+    "halo_gather": _sig("halo_gather", P, P, I64, I32, I32, P, P),
+    "halo_scatter_add": _sig("halo_scatter_add", P, P, I64, I32, P, P),
+    "halo_exchange_loopback": _sig("halo_exchange_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
+                                   C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, P),
+}
+
+EXPORTED = sorted(["dsmpnn_" + k for k in _f] + ["dsmpnn_last_error", "dsmpnn_version"])
+
+
+def _call(name, *args):
+    st = _f[name](*args)
+    if st != 0:
+        raise DsmpnnError(st, name, _lib.dsmpnn_last_error().decode())
+
+
+def version():
+    return int(_lib.dsmpnn_version())
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ws(nbytes, device):
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------- a1 -----
+def sample(n_points, s, seed, ids, ws=None, stream=None):
+    sz = SZ()
+    _call("sample_workspace_size", n_points, C.byref(sz))
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, ids.device)
+    _call("sample", n_points, s, seed, _p(ids), _p(ws), ws.numel(), _stream(stream))
+    return ids
+
+
+# ---------------------------------------------------------------- a2 -----
+def radius_graph_workspace_size(n_loc, n_dst, dim):
+    sz = SZ()
+    _call("radius_graph_workspace_size", n_loc, n_dst, dim, C.byref(sz))
+    return sz.value
+
+
+def radius_graph(coords, gid, n_dst, r, n_e, seed, row_ptr, col_idx, want_count=True, ws=None, stream=None):
+    n_loc, dim = coords.shape
+    need = radius_graph_workspace_size(n_loc, n_dst, dim)
+    ws = ws if ws is not None and ws.numel() >= need else _ws(need, coords.device)
+    ne = I64(0)
+    _call("radius_graph", _p(coords), _p(gid), n_loc, n_dst, dim, float(r), n_e, seed, _p(row_ptr), _p(col_idx),
+          col_idx.numel(), C.byref(ne) if want_count else None, _p(ws), ws.numel(), _stream(stream))
+    return int(ne.value) if want_count else None
+
+
+def radius_counts(coords, n_dst, r, counts, stream=None):
+    n_loc, dim = coords.shape
+    ws = _ws(radius_graph_workspace_size(n_loc, n_dst, dim), coords.device)
+    _call("radius_counts", _p(coords), n_loc, n_dst, dim, float(r), _p(counts), _p(ws), ws.numel(), _stream(stream))
+    return counts
+
+
+def csc(col_idx, n_loc, csc_perm, csc_ptr, stream=None):
+    E = col_idx.numel()
+    sz = SZ()
+    _call("csc_workspace_size", E, n_loc, C.byref(sz))
+    ws = _ws(sz.value, col_idx.device)
+    _call("csc", _p(col_idx), E, n_loc, _p(csc_perm), _p(csc_ptr), _p(ws), ws.numel(), _stream(stream))
+
+
+# ---------------------------------------------------------------- a3 -----
+def partition(coords, gid, nparts, overlap_l, radius, rank, owner, boxes, internal, local_rows, counts, send_idx,
+              sync=True, ws=None, stream=None):
+    n, dim = coords.shape
+    sz = SZ()
+    _call("partition_workspace_size", n, dim, nparts, C.byref(sz))
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, coords.device)
+    nc = 4 + 2 * (nparts + 1)
+    host = (I64 * nc)() if sync else None
+    _call("partition", _p(coords), _p(gid), n, dim, nparts, float(overlap_l), float(radius), rank, _p(owner),
+          _p(boxes), _p(internal), _p(local_rows), _p(counts), _p(send_idx), host, _p(ws), ws.numel(),
+          _stream(stream))
+    return [int(x) for x in host] if sync else None
+
+
+def gather_rows(inp, rows, out, stream=None):
+    n_rows = rows.numel()
+    row_elems = inp[0].numel() if inp.dim() > 1 else 1
+    _call("gather_rows", _p(inp), _p(rows), n_rows, row_elems, inp.element_size(), _p(out), _stream(stream))
+    return out
+
+
+def edge_features(mode, coords, attr, row_ptr, col_idx, n_dst, e32=None, e16=None, stream=None):
+    dim = coords.shape[1]
+    n_attr = attr.shape[1] if attr is not None else 0
+    _call("edge_features", mode, _p(coords), dim, _p(attr), n_attr, _p(row_ptr), _p(col_idx), n_dst,
+          col_idx.numel(), _p(e32), _p(e16), _stream(stream))
+
+
+# ----------------------------------------------------------- a4/a5/a7 -----
+def make_desc(d_e, d_in, d_out, k, dtype=F32, root=ROOT_DENSE, act=ACT_RELU):
+    return LayerDesc(d_e, d_in, d_out, k, dtype, root, act, 0)
+
+
+def make_weights(W, packed=None):
+    return Weights(*[_p(W.get(n)) for n in ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")], _p(packed))
+
+
+def make_grads(G):
+    return Grads(*[_p(G.get(n)) for n in ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")])
+
+
+def packed_weights_size(desc):
+    sz = SZ()
+    _call("packed_weights_size", C.byref(desc), C.byref(sz))
+    return sz.value
+
+
+def pack_weights(desc, W, packed, stream=None):
+    w = make_weights(W)
+    _call("pack_weights", C.byref(desc), C.byref(w), _p(packed), packed.numel(), _stream(stream))
+    return packed
+
+
+def layer_workspace_size(desc, n_dst, n_edges):
+    sz = SZ()
+    _call("layer_workspace_size", C.byref(desc), n_dst, n_edges, C.byref(sz))
+    return sz.value
+
+
+def layer_bwd_workspace_size(desc, n_dst, n_loc, n_edges):
+    sz = SZ()
+    _call("layer_bwd_workspace_size", C.byref(desc), n_dst, n_loc, n_edges, C.byref(sz))
+    return sz.value
+
+
+def _host_ptr_i64(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def layer_fwd(desc, W, packed, v, e, row_ptr, col_idx, n_dst, row_begin, row_end, out, out_lowp, ws,
+              row_ptr_host=None, stream=None):
+    w = make_weights(W, packed)
+    _call("layer_fwd", C.byref(desc), C.byref(w), _p(v), _p(e), _p(row_ptr), _host_ptr_i64(row_ptr_host),
+          _p(col_idx), n_dst, row_begin, row_end, _p(out), _p(out_lowp), _p(ws), ws.numel(), _stream(stream))
+
+
+def layer_bwd(desc, W, packed, v, e, row_ptr, col_idx, csc_perm, csc_ptr, n_dst, n_loc, row_begin, row_end,
+              grad_out, grad_v, grad_e, grads, ws, bwd_ws, row_ptr_host=None, stream=None):
+    w = make_weights(W, packed)
+    g = make_grads(grads)
+    _call("layer_bwd", C.byref(desc), C.byref(w), _p(v), _p(e), _p(row_ptr), _host_ptr_i64(row_ptr_host),
+          _p(col_idx), _p(csc_perm), _p(csc_ptr), n_dst, n_loc, row_begin, row_end, _p(grad_out), _p(grad_v),
+          _p(grad_e), C.byref(g), _p(ws), _p(bwd_ws), bwd_ws.numel(), _stream(stream))
+
+
+# ---------------------------------------------------------------- a6 -----
+def halo_gather(values, rows, out, dtype, stream=None):
+    width = values.shape[1]
+    _call("halo_gather", _p(values), _p(rows), rows.numel(), width, dtype, _p(out), _stream(stream))
+
+
+def halo_scatter_add(inp, rows, values, stream=None):
+    _call("halo_scatter_add", _p(inp), _p(rows), rows.numel(), values.shape[1], _p(values), _stream(stream))
+
+
+def halo_exchange_loopback(values_list, halo_ptr_list, send_ptr_list, send_idx_list, dtype, stream=None):
+    P_ = len(values_list)
+    width = values_list[0].shape[1]
+    vals = (P * P_)(*[v.data_ptr() for v in values_list])
+    hp = [(I64 * (P_ + 1))(*[int(x) for x in h]) for h in halo_ptr_list]
+    sp = [(I64 * (P_ + 1))(*[int(x) for x in s]) for s in send_ptr_list]
+    hpp = (C.POINTER(I64) * P_)(*[C.cast(h, C.POINTER(I64)) for h in hp])
+    spp = (C.POINTER(I64) * P_)(*[C.cast(s, C.POINTER(I64)) for s in sp])
+    sidx = (P * P_)(*[s.data_ptr() for s in send_idx_list])
+    _call("halo_exchange_loopback", P_, vals, hpp, spp, sidx, width, dtype, _stream(stream))

@@ -1,0 +1,66 @@
+// common.cuh - shared helpers of libdsmpnn.so (sm_100a).  Status handling,
+// workspace carving, launch helpers.  No method arithmetic lives here except
+// the counter hash (hash.cuh).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/dsmpnn.h"
+
+namespace dsmpnn {
+
+void set_error(const char *fmt, ...);
+
+#define DS_CHECK_ARG(cond, code, ...)      \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::dsmpnn::set_error(__VA_ARGS__);    \
+      return code;                         \
+    }                                      \
+  } while (0)
+
+#define DS_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      ::dsmpnn::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__,  \
+                          __LINE__, cudaGetErrorString(_e));                            \
+      return DSMPNN_ERR_CUDA;                                                           \
+    }                                                                                   \
+  } while (0)
+
+#define DS_LAUNCH_CHECK() DS_CUDA(cudaGetLastError())
+
+#define DS_TRY(expr)                       \
+  do {                                     \
+    dsmpnn_status _s = (expr);             \
+    if (_s != DSMPNN_OK) return _s;        \
+  } while (0)
+
+static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+struct Carver {
+  char *base;
+  size_t cap;
+  size_t off = 0;
+  Carver(void *b, size_t c) : base(static_cast<char *>(b)), cap(c) {}
+  template <typename T>
+  T *take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return off <= cap; }
+  size_t used() const { return (off + 255) & ~size_t(255); }
+};
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int kNumSMs = 148;
+
+}  // namespace dsmpnn

@@ -1,0 +1,419 @@
+// graph.cu - a2 radius graph kernel with random edge cap (PAPER.md:27,
+// Alg. 1 :395-396; readings R7, R8, R10, R11).
+//
+// Cell list: points are binned into cells of edge h >= r(1+2^-8) over the
+// local bounding box and sorted by cell (stable radix sort).  One warp owns one
+// destination row and scans the 3^dim neighbouring cells (32 candidates per
+// step, ballot-compacted).  Pass 1 counts candidates; the CSR offsets are an
+// exclusive scan of min(count, n_e); pass 2 either keeps all candidates or
+// selects the n_e smallest (key_edge, gid) by a most-significant-digit radix
+// select (8-bit digits, early exit once the boundary bucket is taken whole),
+// then orders the kept row by gid with a rank sort and writes it.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "hash.cuh"
+
+namespace dsmpnn {
+
+struct GridParams {
+  float lo[3];
+  float inv_h;
+  int n[3];
+  int n_cells;
+};
+
+// fp32 predicate in the fixed order of R7 (no FMA contraction)
+__device__ __forceinline__ bool within(const float *xi, const float *xj, int dim, float r2) {
+  float dx = __fsub_rn(xi[0], xj[0]);
+  float d2 = __fmul_rn(dx, dx);
+  dx = __fsub_rn(xi[1], xj[1]);
+  d2 = __fadd_rn(d2, __fmul_rn(dx, dx));
+  if (dim == 3) {
+    dx = __fsub_rn(xi[2], xj[2]);
+    d2 = __fadd_rn(d2, __fmul_rn(dx, dx));
+  }
+  return d2 <= r2;
+}
+
+__global__ void bbox_kernel(const float *__restrict__ x, int64_t n, int dim, float *__restrict__ out /*lo[3],hi[3]*/) {
+  __shared__ float slo[3][32], shi[3][32];
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    for (int d = 0; d < dim; ++d) {
+      float v = x[i * dim + d];
+      lo[d] = fminf(lo[d], v);
+      hi[d] = fmaxf(hi[d], v);
+    }
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int d = 0; d < 3; ++d) { slo[d][w] = lo[d]; shi[d][w] = hi[d]; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    int d = threadIdx.x;
+    float a = INFINITY, b = -INFINITY;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { a = fminf(a, slo[d][k]); b = fmaxf(b, shi[d][k]); }
+    out[d] = a;
+    out[3 + d] = b;
+  }
+}
+
+__global__ void grid_params_kernel(const float *__restrict__ bb, int dim, float h0, int64_t max_cells,
+                                   GridParams *__restrict__ gp) {
+  float h = h0;
+  int n[3] = {1, 1, 1};
+  for (int it = 0; it < 200; ++it) {
+    int64_t tot = 1;
+    for (int d = 0; d < dim; ++d) {
+      float ext = bb[3 + d] - bb[d];
+      n[d] = (int)floorf(ext / h) + 1;
+      tot *= n[d];
+    }
+    if (tot <= max_cells) break;
+    h *= 1.25f;
+  }
+  GridParams p;
+  for (int d = 0; d < 3; ++d) { p.lo[d] = d < dim ? bb[d] : 0.f; p.n[d] = d < dim ? n[d] : 1; }
+  p.inv_h = 1.0f / h;
+  p.n_cells = p.n[0] * p.n[1] * p.n[2];
+  *gp = p;
+}
+
+__device__ __forceinline__ int cell_coord(float v, float lo, float inv_h, int n) {
+  int c = (int)floorf((v - lo) * inv_h);
+  return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+__global__ void cell_id_kernel(const float *__restrict__ x, int64_t n, int dim, const GridParams *__restrict__ gp,
+                               int32_t *__restrict__ cell, int32_t *__restrict__ idx) {
+  GridParams p = *gp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) c[d] = cell_coord(x[i * dim + d], p.lo[d], p.inv_h, p.n[d]);
+    cell[i] = (c[2] * p.n[1] + c[1]) * p.n[0] + c[0];
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void cell_start_kernel(const int32_t *__restrict__ sorted_cell, int64_t n, const GridParams *__restrict__ gp,
+                                  int32_t *__restrict__ start, int64_t max_cells) {
+  int64_t nc = gp->n_cells;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= nc; c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sorted_cell[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    start[c] = (int32_t)lo;
+  }
+}
+
+// Visit every candidate j != i of row i; F(j, ok) is called warp-uniformly per
+// 32-wide step with `ok` this lane's predicate result.
+template <typename F>
+__device__ __forceinline__ void scan_candidates(int64_t i, const float *__restrict__ x, int dim, float r2,
+                                                const GridParams &p, const int32_t *__restrict__ start,
+                                                const int32_t *__restrict__ sorted_idx, F &&f) {
+  int lane = threadIdx.x & 31;
+  float xi[3] = {0.f, 0.f, 0.f};
+  for (int d = 0; d < dim; ++d) xi[d] = x[i * dim + d];
+  int c[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) c[d] = cell_coord(xi[d], p.lo[d], p.inv_h, p.n[d]);
+  int z0 = dim == 3 ? max(c[2] - 1, 0) : 0, z1 = dim == 3 ? min(c[2] + 1, p.n[2] - 1) : 0;
+  int y0 = max(c[1] - 1, 0), y1 = min(c[1] + 1, p.n[1] - 1);
+  int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, p.n[0] - 1);
+  for (int cz = z0; cz <= z1; ++cz)
+    for (int cy = y0; cy <= y1; ++cy) {
+      // cells (x0..x1, cy, cz) are contiguous in the sorted order
+      int base = (cz * p.n[1] + cy) * p.n[0];
+      int a = start[base + x0], b = start[base + x1 + 1];
+      for (int t0 = a; t0 < b; t0 += 32) {
+        int t = t0 + lane;
+        int j = -1;
+        bool ok = false;
+        if (t < b) {
+          j = sorted_idx[t];
+          float xj[3] = {0.f, 0.f, 0.f};
+          for (int d = 0; d < dim; ++d) xj[d] = x[(int64_t)j * dim + d];
+          ok = (j != i) && within(xi, xj, dim, r2);
+        }
+        f(j, ok);
+      }
+    }
+}
+
+__global__ void count_kernel(const float *__restrict__ x, int64_t n_dst, int dim, float r,
+                             const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
+                             const int32_t *__restrict__ sorted_idx, int32_t *__restrict__ counts,
+                             int64_t *__restrict__ deg, int32_t n_e) {
+  GridParams p = *gp;
+  float r2 = __fmul_rn(r, r);
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_dst; i += nwarps) {
+    int cnt = 0;
+    scan_candidates(i, x, dim, r2, p, start, sorted_idx, [&](int, bool ok) {
+      cnt += __popc(__ballot_sync(0xffffffffu, ok));
+    });
+    if ((threadIdx.x & 31) == 0) {
+      if (counts) counts[i] = cnt;
+      if (deg) deg[i] = cnt < n_e ? cnt : n_e;
+    }
+  }
+}
+
+constexpr int kMaxNe = 128;
+constexpr int kSelWarps = 4;
+
+// digit d (0..15) of the 128-bit composite (key, gid), most significant first
+__device__ __forceinline__ uint32_t comp_digit(uint64_t key, uint64_t gid, int d) {
+  return d < 8 ? (uint32_t)(key >> (56 - 8 * d)) & 0xffu : (uint32_t)(gid >> (56 - 8 * (d - 8))) & 0xffu;
+}
+// does the composite's top D digits equal (pk, pg)'s top D digits?
+__device__ __forceinline__ bool comp_prefix_eq(uint64_t key, uint64_t gid, uint64_t pk, uint64_t pg, int D) {
+  if (D == 0) return true;
+  if (D <= 8) {
+    int sh = 64 - 8 * D;
+    return (key >> sh) == (pk >> sh);
+  }
+  if (key != pk) return false;
+  int sh = 64 - 8 * (D - 8);
+  return D == 16 ? gid == pg : (gid >> sh) == (pg >> sh);
+}
+__device__ __forceinline__ bool comp_prefix_le(uint64_t key, uint64_t gid, uint64_t pk, uint64_t pg, int D) {
+  if (D <= 8) {
+    int sh = 64 - 8 * D;
+    return D == 0 ? true : (key >> sh) <= (pk >> sh);
+  }
+  if (key != pk) return key < pk;
+  int sh = 64 - 8 * (D - 8);
+  return D == 16 ? gid <= pg : (gid >> sh) <= (pg >> sh);
+}
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_kernel(
+    const float *__restrict__ x, const int64_t *__restrict__ gid, int64_t n_dst, int dim, float r, int32_t n_e,
+    uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
+    const int32_t *__restrict__ sorted_idx, const int32_t *__restrict__ counts, const int64_t *__restrict__ row_ptr,
+    int32_t *__restrict__ col) {
+  __shared__ uint32_t hist[kSelWarps][256];
+  __shared__ int32_t lidx[kSelWarps][kMaxNe];
+  __shared__ int64_t lgid[kSelWarps][kMaxNe];
+  GridParams p = *gp;
+  float r2 = __fmul_rn(r, r);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_dst; i += nwarps) {
+    int cnt = counts[i];
+    uint64_t gi = (uint64_t)gid[i];
+    uint64_t si = smx(s0 ^ gi);
+    uint64_t pk = 0, pg = 0;
+    int D = 0;
+    if (cnt > n_e) {
+      int need = n_e;
+      for (int d = 0; d < 16; ++d) {
+        for (int b = lane; b < 256; b += 32) hist[w][b] = 0;
+        __syncwarp();
+        scan_candidates(i, x, dim, r2, p, start, sorted_idx, [&](int j, bool ok) {
+          if (ok) {
+            uint64_t gj = (uint64_t)gid[j];
+            uint64_t k = key_edge(si, gj);
+            if (comp_prefix_eq(k, gj, pk, pg, d)) atomicAdd(&hist[w][comp_digit(k, gj, d)], 1u);
+          }
+        });
+        __syncwarp();
+        // find bucket b with cum_before < need <= cum_before + hist[b]; lane owns bins 8*lane..8*lane+7
+        uint32_t loc[8];
+        uint32_t s = 0;
+        for (int q = 0; q < 8; ++q) { loc[q] = hist[w][lane * 8 + q]; s += loc[q]; }
+        uint32_t incl = s;
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        uint32_t excl = incl - s;
+        int found = -1, taken_before = 0, bcnt = 0;
+        if ((int)excl < need && need <= (int)incl) {
+          uint32_t c0 = excl;
+          for (int q = 0; q < 8; ++q) {
+            if ((int)(c0 + loc[q]) >= need) { found = lane * 8 + q; taken_before = c0; bcnt = loc[q]; break; }
+            c0 += loc[q];
+          }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, found >= 0);
+        int src = __ffs(m) - 1;
+        found = __shfl_sync(0xffffffffu, found, src);
+        taken_before = __shfl_sync(0xffffffffu, taken_before, src);
+        bcnt = __shfl_sync(0xffffffffu, bcnt, src);
+        if (d < 8) pk |= (uint64_t)found << (56 - 8 * d);
+        else pg |= (uint64_t)found << (56 - 8 * (d - 8));
+        need -= taken_before;
+        D = d + 1;
+        __syncwarp();
+        if (bcnt == need) break;
+      }
+    }
+    // collect the kept candidates (all, or those with top-D digits <= prefix)
+    int nk = 0;
+    scan_candidates(i, x, dim, r2, p, start, sorted_idx, [&](int j, bool ok) {
+      bool keep = false;
+      uint64_t gj = 0;
+      if (ok) {
+        gj = (uint64_t)gid[j];
+        keep = (cnt <= n_e) || comp_prefix_le(key_edge(si, gj), gj, pk, pg, D);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        int slot = nk + __popc(m & ((1u << lane) - 1));
+        lidx[w][slot] = j;
+        lgid[w][slot] = (int64_t)gj;
+      }
+      nk += __popc(m);
+    });
+    __syncwarp();
+    int64_t off = row_ptr[i];
+    for (int a = lane; a < nk; a += 32) {
+      int64_t g = lgid[w][a];
+      int rank = 0;
+      for (int b = 0; b < nk; ++b) rank += lgid[w][b] < g;
+      col[off + rank] = lidx[w][a];
+    }
+    __syncwarp();
+  }
+}
+
+static int64_t max_cells_for(int64_t n_loc) { return std::max<int64_t>(4 * n_loc, 4096); }
+
+static size_t graph_ws(int64_t n_loc, int64_t n_dst, size_t *sort_tmp, size_t *scan_tmp) {
+  cub::DeviceRadixSort::SortPairs(nullptr, *sort_tmp, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_loc);
+  cub::DeviceScan::ExclusiveSum(nullptr, *scan_tmp, (const int64_t *)nullptr, (int64_t *)nullptr, (int)(n_dst + 1));
+  Carver c(nullptr, 0);
+  c.take<float>(8);
+  c.take<GridParams>(1);
+  c.take<int32_t>(n_loc); c.take<int32_t>(n_loc); c.take<int32_t>(n_loc); c.take<int32_t>(n_loc);
+  c.take<int32_t>(max_cells_for(n_loc) + 1);
+  c.take<int32_t>(n_dst);
+  c.take<int64_t>(n_dst + 1);
+  c.take<char>(*sort_tmp);
+  c.take<char>(*scan_tmp);
+  return c.used();
+}
+
+struct GraphState {
+  GridParams *gp;
+  int32_t *sorted_idx, *start, *counts;
+  int64_t *deg;
+  void *scan_tmp;
+  size_t scan_bytes;
+};
+
+static dsmpnn_status build_cells(const float *coords, int64_t n_loc, int64_t n_dst, int dim, float r, void *ws,
+                                 size_t ws_bytes, cudaStream_t s, GraphState &st) {
+  size_t sort_tmp, scan_tmp;
+  size_t need = graph_ws(n_loc, n_dst, &sort_tmp, &scan_tmp);
+  DS_CHECK_ARG(ws_bytes >= need, DSMPNN_ERR_CAPACITY, "radius_graph: workspace %zu < %zu", ws_bytes, need);
+  Carver c(ws, ws_bytes);
+  float *bb = c.take<float>(8);
+  st.gp = c.take<GridParams>(1);
+  int32_t *cell = c.take<int32_t>(n_loc), *cell_sorted = c.take<int32_t>(n_loc);
+  int32_t *idx = c.take<int32_t>(n_loc);
+  st.sorted_idx = c.take<int32_t>(n_loc);
+  int64_t maxc = max_cells_for(n_loc);
+  st.start = c.take<int32_t>(maxc + 1);
+  st.counts = c.take<int32_t>(n_dst);
+  st.deg = c.take<int64_t>(n_dst + 1);
+  void *t1 = c.take<char>(sort_tmp);
+  st.scan_tmp = c.take<char>(scan_tmp);
+  st.scan_bytes = scan_tmp;
+  bbox_kernel<<<1, 1024, 0, s>>>(coords, n_loc, dim, bb);
+  float h0 = r * 1.00390625f;  // cell edge r(1+2^-8): only needs to be >= r
+  grid_params_kernel<<<1, 1, 0, s>>>(bb, dim, h0, maxc, st.gp);
+  int g = (int)std::min<int64_t>(ceil_div(n_loc, 256), 148 * 8);
+  cell_id_kernel<<<g, 256, 0, s>>>(coords, n_loc, dim, st.gp, cell, idx);
+  DS_LAUNCH_CHECK();
+  int end_bit = 1;
+  while ((1ll << end_bit) <= maxc) ++end_bit;
+  DS_CUDA(cub::DeviceRadixSort::SortPairs(t1, sort_tmp, cell, cell_sorted, idx, st.sorted_idx, (int)n_loc, 0,
+                                          end_bit, s));
+  cell_start_kernel<<<(int)std::min<int64_t>(ceil_div(maxc + 1, 256), 148 * 8), 256, 0, s>>>(cell_sorted, n_loc,
+                                                                                            st.gp, st.start, maxc);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+}  // namespace dsmpnn
+
+using namespace dsmpnn;
+
+extern "C" {
+
+dsmpnn_status dsmpnn_radius_graph_workspace_size(int64_t n_loc, int64_t n_dst, int dim, size_t *bytes) {
+  DS_CHECK_ARG(n_loc >= 0 && n_dst >= 0 && n_dst <= n_loc && n_loc < (1ll << 31), DSMPNN_ERR_INVALID_ARG,
+               "radius_graph: sizes");
+  size_t a, b;
+  *bytes = graph_ws(n_loc, n_dst, &a, &b);
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_radius_counts(const float *coords, int64_t n_loc, int64_t n_dst, int dim, float r,
+                                   int32_t *counts, void *ws, size_t ws_bytes, void *stream) {
+  DS_CHECK_ARG(r > 0.f && (dim == 2 || dim == 3) && n_dst <= n_loc && n_loc < (1ll << 31), DSMPNN_ERR_INVALID_ARG,
+               "radius_counts: bad arguments");
+  if (n_dst == 0) return DSMPNN_OK;
+  cudaStream_t s = as_stream(stream);
+  GraphState st;
+  DS_TRY(build_cells(coords, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
+  int blocks = (int)std::min<int64_t>(ceil_div(n_dst * 32, 256), 148 * 16);
+  count_kernel<<<blocks, 256, 0, s>>>(coords, n_dst, dim, r, st.gp, st.start, st.sorted_idx, counts, nullptr, 1);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64_t n_loc, int64_t n_dst, int dim,
+                                  float r, int32_t n_e, uint64_t seed, int64_t *row_ptr, int32_t *col_idx,
+                                  int64_t col_capacity, int64_t *n_edges, void *ws, size_t ws_bytes, void *stream) {
+  DS_CHECK_ARG(r > 0.f, DSMPNN_ERR_INVALID_ARG, "radius_graph: r must be > 0");
+  DS_CHECK_ARG(n_e >= 1, DSMPNN_ERR_INVALID_ARG, "radius_graph: n_e must be >= 1");
+  DS_CHECK_ARG(n_e <= kMaxNe, DSMPNN_ERR_UNSUPPORTED, "radius_graph: n_e <= %d supported", kMaxNe);
+  DS_CHECK_ARG(dim == 2 || dim == 3, DSMPNN_ERR_INVALID_ARG, "radius_graph: dim must be 2 or 3");
+  DS_CHECK_ARG(n_loc >= 0 && n_dst >= 0 && n_dst <= n_loc && n_loc < (1ll << 31), DSMPNN_ERR_INVALID_ARG,
+               "radius_graph: need 0 <= n_dst <= n_loc < 2^31");
+  cudaStream_t s = as_stream(stream);
+  if (n_dst == 0) {
+    DS_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t), s));
+    if (n_edges) *n_edges = 0;
+    return DSMPNN_OK;
+  }
+  if (!n_edges)
+    DS_CHECK_ARG(col_capacity >= n_dst * (int64_t)n_e, DSMPNN_ERR_CAPACITY,
+                 "radius_graph: without n_edges, col_capacity must be >= n_dst*n_e");
+  GraphState st;
+  DS_TRY(build_cells(coords, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
+  int blocks = (int)std::min<int64_t>(ceil_div(n_dst * 32, 256), 148 * 16);
+  count_kernel<<<blocks, 256, 0, s>>>(coords, n_dst, dim, r, st.gp, st.start, st.sorted_idx, st.counts, st.deg, n_e);
+  DS_LAUNCH_CHECK();
+  DS_CUDA(cudaMemsetAsync(st.deg + n_dst, 0, sizeof(int64_t), s));
+  size_t sb = st.scan_bytes;
+  DS_CUDA(cub::DeviceScan::ExclusiveSum(st.scan_tmp, sb, st.deg, row_ptr, (int)(n_dst + 1), s));
+  if (n_edges) {
+    DS_CUDA(cudaMemcpyAsync(n_edges, row_ptr + n_dst, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaStreamSynchronize(s));
+    if (*n_edges > col_capacity) {
+      set_error("radius_graph: col_capacity %lld < E %lld", (long long)col_capacity, (long long)*n_edges);
+      return DSMPNN_ERR_CAPACITY;
+    }
+  }
+  int sblocks = (int)std::min<int64_t>(ceil_div(n_dst, kSelWarps), 148 * 16);
+  select_kernel<<<sblocks, kSelWarps * 32, 0, s>>>(coords, gid, n_dst, dim, r, n_e, smx(seed), st.gp, st.start,
+                                                  st.sorted_idx, st.counts, row_ptr, col_idx);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// misc.cu - error text, version, row gathers, edge attributes, halo gather /
+// scatter-add, loopback exchange, CSC view.
+#include <cub/cub.cuh>
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace dsmpnn {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+// ---------------------------------------------------------------- gathers --
+template <typename T>
+__global__ void gather_rows_kernel(const T *__restrict__ in, const int64_t *__restrict__ rows, int64_t n_rows,
+                                   int64_t row_elems, T *__restrict__ out) {
+  int64_t total = n_rows * row_elems;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / row_elems, c = t - r * row_elems;
+    out[t] = in[rows[r] * row_elems + c];
+  }
+}
+
+// ------------------------------------------------------- edge attributes --
+// PAPER.md:27 / Alg. 1 :397, reading R21.  One thread per (edge, column).
+__global__ void edge_features_kernel(int32_t mode, const float *__restrict__ x, int dim, const float *__restrict__ a,
+                                     int n_attr, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                     int64_t n_dst, int64_t n_edges, float *__restrict__ e32,
+                                     __nv_bfloat16 *__restrict__ e16) {
+  int de = (mode == DSMPNN_EDGE_DIFF) ? (dim + n_attr) : 2 * (dim + n_attr);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_edges; p += (int64_t)gridDim.x * blockDim.x) {
+    // destination row of edge p: binary search in row_ptr
+    int64_t lo = 0, hi = n_dst;  // find largest i with row_ptr[i] <= p
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (row_ptr[mid] <= p) lo = mid; else hi = mid;
+    }
+    int64_t i = lo, j = col[p];
+    float vals[32];
+    int c = 0;
+    if (mode == DSMPNN_EDGE_DIFF) {
+      for (int d = 0; d < dim; ++d) vals[c++] = __fsub_rn(x[i * dim + d], x[j * dim + d]);
+      for (int d = 0; d < n_attr; ++d) vals[c++] = __fsub_rn(a[i * n_attr + d], a[j * n_attr + d]);
+    } else {
+      for (int d = 0; d < dim; ++d) vals[c++] = x[i * dim + d];
+      for (int d = 0; d < dim; ++d) vals[c++] = x[j * dim + d];
+      for (int d = 0; d < n_attr; ++d) vals[c++] = a[i * n_attr + d];
+      for (int d = 0; d < n_attr; ++d) vals[c++] = a[j * n_attr + d];
+    }
+    if (e32)
+      for (int d = 0; d < de; ++d) e32[p * de + d] = vals[d];
+    if (e16) {
+      __nv_bfloat16 *o = e16 + p * 16;
+      for (int d = 0; d < 16; ++d) o[d] = __float2bfloat16_rn(d < de ? vals[d] : 0.f);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ halo --
+template <typename T>
+__global__ void halo_gather_kernel(const T *__restrict__ v, const int32_t *__restrict__ rows, int64_t n_rows,
+                                   int width, T *__restrict__ out) {
+  int64_t total = n_rows * width;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / width, c = t - r * width;
+    out[t] = v[(int64_t)rows[r] * width + c];
+  }
+}
+
+__global__ void halo_scatter_add_kernel(const float *__restrict__ in, const int32_t *__restrict__ rows,
+                                        int64_t n_rows, int width, float *__restrict__ v) {
+  // rows within one call are distinct (a send list), so plain read-modify-write is race free
+  int64_t total = n_rows * width;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / width, c = t - r * width;
+    float *dst = v + (int64_t)rows[r] * width + c;
+    *dst = __fadd_rn(*dst, in[t]);
+  }
+}
+
+// ------------------------------------------------------------------- CSC --
+__global__ void iota_i32(int32_t *o, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    o[t] = (int32_t)t;
+}
+// csc_ptr[j] = first position in sorted keys with key >= j (lower bound)
+__global__ void csc_ptr_kernel(const int32_t *__restrict__ sorted_col, int64_t n_edges, int64_t n_loc,
+                               int64_t *__restrict__ ptr) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= n_loc; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n_edges;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sorted_col[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    ptr[j] = lo;
+  }
+}
+
+static int grid_for(int64_t n, int block = 256) {
+  int64_t g = ceil_div(n, block);
+  if (g < 1) g = 1;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)g;
+}
+
+}  // namespace dsmpnn
+
+using namespace dsmpnn;
+
+extern "C" {
+
+const char *dsmpnn_last_error(void) { return g_last_error.c_str(); }
+int32_t dsmpnn_version(void) { return 1; }
+
+dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
+                                 int32_t elem_bytes, void *out, void *stream) {
+  DS_CHECK_ARG(n_rows >= 0 && row_elems >= 0, DSMPNN_ERR_INVALID_ARG, "gather_rows: negative size");
+  if (n_rows == 0 || row_elems == 0) return DSMPNN_OK;
+  cudaStream_t s = as_stream(stream);
+  int g = grid_for(n_rows * row_elems);
+  if (elem_bytes == 4)
+    gather_rows_kernel<uint32_t><<<g, 256, 0, s>>>((const uint32_t *)in, rows, n_rows, row_elems, (uint32_t *)out);
+  else if (elem_bytes == 8)
+    gather_rows_kernel<uint64_t><<<g, 256, 0, s>>>((const uint64_t *)in, rows, n_rows, row_elems, (uint64_t *)out);
+  else if (elem_bytes == 2)
+    gather_rows_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t *)in, rows, n_rows, row_elems, (uint16_t *)out);
+  else
+    DS_CHECK_ARG(false, DSMPNN_ERR_INVALID_ARG, "gather_rows: elem_bytes must be 2, 4 or 8");
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_edge_features(int32_t mode, const float *coords, int dim, const float *attr, int n_attr,
+                                   const int64_t *row_ptr, const int32_t *col_idx, int64_t n_dst,
+                                   int64_t n_edges, float *e32, void *e16, void *stream) {
+  DS_CHECK_ARG(mode == DSMPNN_EDGE_DIFF || mode == DSMPNN_EDGE_CONCAT, DSMPNN_ERR_INVALID_ARG, "edge_features: mode");
+  DS_CHECK_ARG(dim == 2 || dim == 3, DSMPNN_ERR_INVALID_ARG, "edge_features: dim must be 2 or 3");
+  DS_CHECK_ARG(n_attr >= 0 && n_attr <= 6, DSMPNN_ERR_INVALID_ARG, "edge_features: n_attr in [0,6]");
+  int de = (mode == DSMPNN_EDGE_DIFF) ? (dim + n_attr) : 2 * (dim + n_attr);
+  DS_CHECK_ARG(!e16 || de <= 16, DSMPNN_ERR_SHAPE, "edge_features: d_e=%d > 16 for bf16 output", de);
+  if (n_edges <= 0) return DSMPNN_OK;
+  edge_features_kernel<<<grid_for(n_edges), 256, 0, as_stream(stream)>>>(
+      mode, coords, dim, attr, n_attr, row_ptr, col_idx, n_dst, n_edges, e32, (__nv_bfloat16 *)e16);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_halo_gather(const void *values, const int32_t *rows, int64_t n_rows, int32_t width,
+                                 int32_t dtype, void *out, void *stream) {
+  DS_CHECK_ARG(width > 0 && n_rows >= 0, DSMPNN_ERR_INVALID_ARG, "halo_gather: bad size");
+  if (n_rows == 0) return DSMPNN_OK;
+  cudaStream_t s = as_stream(stream);
+  int g = grid_for(n_rows * width);
+  if (dtype == DSMPNN_F32)
+    halo_gather_kernel<float><<<g, 256, 0, s>>>((const float *)values, rows, n_rows, width, (float *)out);
+  else if (dtype == DSMPNN_BF16)
+    halo_gather_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t *)values, rows, n_rows, width, (uint16_t *)out);
+  else
+    DS_CHECK_ARG(false, DSMPNN_ERR_INVALID_ARG, "halo_gather: dtype");
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_halo_scatter_add(const float *in, const int32_t *rows, int64_t n_rows, int32_t width,
+                                      float *values, void *stream) {
+  DS_CHECK_ARG(width > 0 && n_rows >= 0, DSMPNN_ERR_INVALID_ARG, "halo_scatter_add: bad size");
+  if (n_rows == 0) return DSMPNN_OK;
+  halo_scatter_add_kernel<<<grid_for(n_rows * width), 256, 0, as_stream(stream)>>>(in, rows, n_rows, width, values);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_halo_exchange_loopback(int32_t nparts, void *const *values, const int64_t *const *halo_ptr,
+                                            const int64_t *const *send_ptr, const int32_t *const *send_idx,
+                                            int32_t width, int32_t dtype, void *stream) {
+  DS_CHECK_ARG(nparts >= 1, DSMPNN_ERR_INVALID_ARG, "halo_exchange_loopback: nparts");
+  size_t esz = dtype == DSMPNN_BF16 ? 2 : 4;
+  for (int q = 0; q < nparts; ++q)
+    for (int p = 0; p < nparts; ++p) {
+      if (p == q) continue;
+      int64_t a = halo_ptr[q][p], b = halo_ptr[q][p + 1];
+      int64_t s0 = send_ptr[p][q], s1 = send_ptr[p][q + 1];
+      DS_CHECK_ARG(b - a == s1 - s0, DSMPNN_ERR_SHAPE, "halo_exchange_loopback: %d->%d sizes differ", p, q);
+      if (b == a) continue;
+      char *dst = (char *)values[q] + (size_t)a * width * esz;
+      DS_TRY(dsmpnn_halo_gather(values[p], send_idx[p] + s0, b - a, width, dtype, dst, stream));
+    }
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_csc_workspace_size(int64_t n_edges, int64_t n_loc, size_t *bytes) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_edges);
+  Carver c(nullptr, 0);
+  c.take<int32_t>(n_edges);  // iota
+  c.take<int32_t>(n_edges);  // sorted keys
+  c.take<char>(tmp);
+  *bytes = c.used();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_csc(const int32_t *col_idx, int64_t n_edges, int64_t n_loc, int32_t *csc_perm,
+                         int64_t *csc_ptr, void *ws, size_t ws_bytes, void *stream) {
+  DS_CHECK_ARG(n_edges >= 0 && n_loc >= 0 && n_edges < (1ll << 31), DSMPNN_ERR_INVALID_ARG, "csc: sizes");
+  cudaStream_t s = as_stream(stream);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, (int)n_edges);
+  Carver c(ws, ws_bytes);
+  int32_t *iota = c.take<int32_t>(n_edges);
+  int32_t *keys = c.take<int32_t>(n_edges);
+  void *t = c.take<char>(tmp);
+  DS_CHECK_ARG(c.ok(), DSMPNN_ERR_CAPACITY, "csc: workspace too small");
+  if (n_edges > 0) {
+    iota_i32<<<grid_for(n_edges), 256, 0, s>>>(iota, n_edges);
+    int end_bit = 1;
+    while ((1ll << end_bit) <= n_loc) ++end_bit;
+    DS_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, col_idx, keys, iota, csc_perm, (int)n_edges, 0, end_bit, s));
+  }
+  csc_ptr_kernel<<<grid_for(n_loc + 1), 256, 0, s>>>(keys, n_edges, n_loc, csc_ptr);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+"""Orchestration of the hot path over the C ABI (no arithmetic here).
+
+Graph build per Alg. 1: sample -> decompose
+-> local arrays -> radius graph -> edge attributes (+ CSC view for the
+backward scatter); then the layer loop of lines 404-417 with the halo refresh
+of line 411.  Every step is one call into libdsmpnn.so; torch
+only allocates device memory and provides streams / process groups.
+"""
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L
+
+
+@dataclass
+class Subdomain:
+    rank: int
+    nparts: int
+    n_deep: int
+    n_near: int
+    n_halo: int
+    halo_ptr: list
+    send_ptr: list
+    local_rows: torch.Tensor        # int64 [n_loc] indices into the sampled set
+    send_idx: torch.Tensor          # int32 [n_send]
+    coords: torch.Tensor            # float32 [n_loc x dim]
+    gid: torch.Tensor               # int64 [n_loc]
+    attr: torch.Tensor              # float32 [n_loc x n_attr]
+    row_ptr: torch.Tensor = None    # int64 [n_own+1]
+    row_ptr_host: torch.Tensor = None
+    col_idx: torch.Tensor = None    # int32 [E]
+    n_edges: int = 0
+    e32: torch.Tensor = None
+    e16: torch.Tensor = None
+    csc_perm: torch.Tensor = None
+    csc_ptr: torch.Tensor = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n_own(self):
+        return self.n_deep + self.n_near
+
+    @property
+    def n_loc(self):
+        return self.n_own + self.n_halo
+
+
+def sample_nodes(n_points, s, seed, device):
+    ids = torch.empty(min(s, n_points), dtype=torch.int32, device=device)
+    L.sample(n_points, s, seed, ids)
+    return ids
+
+
+def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks):
+    """Partition the sampled set and build the local arrays of the given ranks."""
+    dev = coords_s.device
+    n, dim = coords_s.shape
+    owner = torch.empty(n, dtype=torch.int32, device=dev)
+    boxes = torch.empty(nparts * 2 * dim, dtype=torch.float32, device=dev)
+    internal = torch.empty(nparts * 2 * dim, dtype=torch.uint8, device=dev)
+    counts = torch.empty(4 + 2 * (nparts + 1), dtype=torch.int64, device=dev)
+    out = []
+    for q in ranks:
+        local_rows = torch.empty(n, dtype=torch.int64, device=dev)
+        send_idx = torch.empty(max(1, n * max(1, nparts - 1)), dtype=torch.int32, device=dev)
+        h = L.partition(coords_s, gid_s, nparts, overlap_l, radius, q, owner, boxes, internal, local_rows, counts,
+                        send_idx, sync=True)
+        nd, nn, nh, ns = h[0], h[1], h[2], h[3]
+        halo_ptr = h[4:4 + nparts + 1]
+        send_ptr = h[4 + nparts + 1:4 + 2 * (nparts + 1)]
+        n_loc = nd + nn + nh
+        lr = local_rows[:n_loc].clone()
+        c = torch.empty((n_loc, dim), dtype=torch.float32, device=dev)
+        L.gather_rows(coords_s, lr, c)
+        g = torch.empty(n_loc, dtype=torch.int64, device=dev)
+        L.gather_rows(gid_s, lr, g)
+        a = torch.empty((n_loc, attr_s.shape[1]), dtype=torch.float32, device=dev)
+        L.gather_rows(attr_s, lr, a)
+        out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[:max(ns, 0)].clone(), c, g, a))
+    return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
+
+
+def build_graph(sd: Subdomain, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
+    dev = sd.coords.device
+    n_own = sd.n_own
+    sd.row_ptr = torch.empty(n_own + 1, dtype=torch.int64, device=dev)
+    cap = max(1, n_own * n_e)
+    col = torch.empty(cap, dtype=torch.int32, device=dev)
+    E = L.radius_graph(sd.coords, sd.gid, n_own, r, n_e, seed, sd.row_ptr, col)
+    sd.col_idx = col[:E]
+    sd.n_edges = E
+    sd.row_ptr_host = sd.row_ptr.cpu()
+    de = (sd.coords.shape[1] + sd.attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
+    sd.e32 = torch.empty((max(E, 1), de), dtype=torch.float32, device=dev) if want_f32 else None
+    sd.e16 = torch.zeros((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None
+    L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, n_own, sd.e32, sd.e16)
+    sd.csc_perm = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)
+    L.csc(sd.col_idx, sd.n_loc, sd.csc_perm, sd.csc_ptr)
+    return sd
+
+
+def halo_exchange_loopback(subs, values, dtype):
+    """FORWARD halo refresh among virtual ranks resident on this device."""
+    L.halo_exchange_loopback(values, [s.halo_ptr for s in subs], [s.send_ptr for s in subs],
+                             [s.send_idx for s in subs], dtype)
+
+
+def halo_exchange_dist(sd: Subdomain, values, dtype, group=None, bufs=None):
+    """FORWARD halo refresh across processes: gather the send rows of every peer
+    into a contiguous buffer and exchange with NCCL send/recv (torch.distributed
+    batch_isend_irecv); receive slices are contiguous halo rows, so they land in
+    place."""
+    import torch.distributed as dist
+    width = values.shape[1]
+    ops = []
+    for q in range(sd.nparts):
+        if q == sd.rank:
+            continue
+        s0, s1 = sd.send_ptr[q], sd.send_ptr[q + 1]
+        if s1 > s0:
+            buf = bufs[q] if bufs is not None else torch.empty((s1 - s0, width), dtype=values.dtype,
+                                                                device=values.device)
+            L.halo_gather(values, sd.send_idx[s0:s1], buf, dtype)
+            ops.append(dist.P2POp(dist.isend, buf, q, group))
+        a, b = sd.halo_ptr[q], sd.halo_ptr[q + 1]
+        if b > a:
+            ops.append(dist.P2POp(dist.irecv, values[a:b], q, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()

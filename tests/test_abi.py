@@ -1,0 +1,66 @@
+"""The C-ABI library builds, loads and exports every symbol include/*.h declares
+(no compute calls: this runs without a GPU)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def _declared():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(dsmpnn_[a-z0-9_]+)\s*\(", src):
+            names.add(m.group(1))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_2402_15106_b200 import build
+    return build.build()
+
+
+def test_header_declares_the_six_calls():
+    d = _declared()
+    for name in ("dsmpnn_sample", "dsmpnn_radius_graph", "dsmpnn_partition", "dsmpnn_layer_fwd",
+                 "dsmpnn_layer_bwd", "dsmpnn_halo_exchange_loopback", "dsmpnn_halo_gather",
+                 "dsmpnn_halo_scatter_add"):
+        assert name in d
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    lib = ctypes.CDLL(lib_path)
+    missing = [n for n in sorted(_declared()) if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_covers_header(lib_path):
+    from paper_2402_15106_b200 import _lib
+    assert set(_lib.EXPORTED) == _declared()
+    assert _lib.version() == 1
+
+
+def test_error_path_without_gpu(lib_path):
+    # argument validation runs before any device work, so it is testable on CPU
+    from paper_2402_15106_b200 import _lib
+    with pytest.raises(_lib.DsmpnnError) as ei:
+        _lib._call("sample", 10, 0, 1, None, None, 0, None)
+    assert ei.value.status == -1 and "s >= 1" in str(ei.value)
+    d = _lib.make_desc(3, 4, 5, 8, root=_lib.ROOT_IDENTITY)
+    sz = _lib.SZ()
+    with pytest.raises(_lib.DsmpnnError) as ei:
+        _lib._call("layer_workspace_size", ctypes.byref(d), 10, 10, ctypes.byref(sz))
+    assert ei.value.status == -2
+
+
+def test_no_oracle_import_in_product():
+    # the product package never imports the oracle (test infrastructure only)
+    for f in glob.glob(os.path.join(ROOT, "paper_2402_15106_b200", "**", "*.py"), recursive=True):
+        src = open(f).read()
+        assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f

@@ -1,0 +1,192 @@
+"""GPU parity for a1 (sample), a2 (radius graph + cap), a3 (partition) and the
+edge attributes: bit-exact against the oracle."""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import features, graph, partition, sample
+from paper_2402_15106_b200 import synth
+from gpu_util import T, N, cuda, hash_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2402_15106_b200 import build
+    build.build()
+    from paper_2402_15106_b200 import _lib
+    return _lib
+
+
+@pytest.mark.parametrize("n,s,seed", [(1, 1, 0), (100, 10, 3), (256, 64, 7), (1000, 1000, 1), (500, 900, 2),
+                                      (58081, 16384, synth.BASE_SEED + 3), (200_000, 150_000, 9)])
+def test_sample_bit_exact(L, n, s, seed):
+    ids = torch.empty(min(n, s), dtype=torch.int32, device=cuda())
+    L.sample(n, s, seed, ids)
+    assert np.array_equal(N(ids), sample.sample(n, s, seed))
+
+
+def _graph_gpu(L, x, gid, n_dst, r, n_e, seed):
+    xc = T(x.astype(np.float32))
+    gc = T(gid.astype(np.int64))
+    rp = torch.empty(n_dst + 1, dtype=torch.int64, device=cuda())
+    col = torch.empty(max(1, n_dst * n_e), dtype=torch.int32, device=cuda())
+    E = L.radius_graph(xc, gc, n_dst, r, n_e, seed, rp, col)
+    return N(rp), N(col[:E]), E
+
+
+def _grid(n, dim):
+    t = (np.arange(n, dtype=np.float64) / (n - 1)).astype(np.float32)
+    g = np.meshgrid(*([t] * dim), indexing="ij")
+    return np.stack([a.ravel() for a in g[::-1]], axis=1).astype(np.float32)
+
+
+CASES = [
+    # name, points, r, n_e, n_dst fraction
+    ("uniform2d", lambda g: g.random((700, 2)), 0.08, 64, 1.0),
+    ("uniform3d", lambda g: g.random((900, 3)), 0.15, 16, 1.0),
+    ("grid_ties2d", lambda g: _grid(24, 2), 0.2, 64, 1.0),          # exact axis ties
+    ("grid_ties3d", lambda g: _grid(9, 3), 0.25, 20, 1.0),
+    ("cap1", lambda g: g.random((300, 2)), 0.2, 1, 1.0),
+    ("dense_cluster", lambda g: 0.01 * g.random((1500, 2)), 0.05, 64, 1.0),  # 1499 candidates per row
+    ("ragged_dst", lambda g: g.random((1000, 2)), 0.07, 8, 0.37),
+    ("isolated", lambda g: np.concatenate([g.random((50, 2)), 10 + g.random((3, 2)) * 100]), 0.1, 64, 1.0),
+]
+
+
+@pytest.mark.parametrize("name,gen,r,n_e,frac", CASES, ids=[c[0] for c in CASES])
+def test_radius_graph_bit_exact(L, name, gen, r, n_e, frac):
+    g = np.random.default_rng(zlib.crc32(name.encode()) % 1000)
+    x = gen(g).astype(np.float32)
+    n = len(x)
+    gid = g.permutation(10 * n)[:n].astype(np.int64)
+    n_dst = max(1, int(frac * n))
+    rp, col, E = _graph_gpu(L, x, gid, n_dst, r, n_e, 77)
+    orp, ocol = graph.radius_graph(x, gid, n_dst, r, n_e, 77)
+    assert np.array_equal(rp, orp)
+    assert np.array_equal(col, ocol)
+
+
+def test_radius_graph_empty_and_errors(L):
+    x = np.random.default_rng(0).random((10, 2)).astype(np.float32)
+    rp, col, E = _graph_gpu(L, x, np.arange(10), 0, 0.1, 8, 1)
+    assert E == 0 and rp[0] == 0
+    with pytest.raises(L.DsmpnnError):
+        _graph_gpu(L, x, np.arange(10), 10, -1.0, 8, 1)
+    with pytest.raises(L.DsmpnnError):
+        _graph_gpu(L, x, np.arange(10), 10, 0.1, 0, 1)
+
+
+def test_radius_graph_darcy_full_size_sampled_rows(L):
+    # BASELINE configs[1] at full size: 16,384 sampled nodes of the 241^2 grid,
+    # r = 0.2, n_e = 64; every row is capped.  Rows checked one by one.
+    cfg = synth.CONFIGS["darcy"]
+    coords, _ = synth.points(cfg)
+    ids = sample.sample(len(coords), cfg.s, synth.BASE_SEED + synth.SEED_SAMPLING)
+    x = coords[ids]
+    gid = ids.astype(np.int64)
+    n = len(x)
+    rp, col, E = _graph_gpu(L, x, gid, n, cfg.r, cfg.n_e, synth.BASE_SEED + synth.SEED_CAPPING)
+    assert E == n * cfg.n_e
+    rows = hash_rows(n, 200)
+    ref = graph.radius_graph_rows(x, gid, rows, cfg.r, cfg.n_e, synth.BASE_SEED + synth.SEED_CAPPING)
+    for i, want in zip(rows, ref):
+        assert np.array_equal(col[rp[i]:rp[i + 1]], want)
+
+
+def test_radius_counts(L):
+    g = np.random.default_rng(5)
+    x = g.random((800, 3)).astype(np.float32)
+    cnt = torch.empty(800, dtype=torch.int32, device=cuda())
+    L.radius_counts(T(x), 800, 0.2, cnt)
+    want = [graph.candidate_count(x, i, 0.2) for i in range(800)]
+    assert np.array_equal(N(cnt), want)
+
+
+def _plan_gpu(L, x, gid, P, l, r, q):
+    n, dim = x.shape
+    owner = torch.empty(n, dtype=torch.int32, device=cuda())
+    boxes = torch.empty(P * 2 * dim, dtype=torch.float32, device=cuda())
+    internal = torch.empty(P * 2 * dim, dtype=torch.uint8, device=cuda())
+    local_rows = torch.empty(n, dtype=torch.int64, device=cuda())
+    counts = torch.empty(4 + 2 * (P + 1), dtype=torch.int64, device=cuda())
+    send_idx = torch.empty(max(1, n * max(1, P - 1)), dtype=torch.int32, device=cuda())
+    h = L.partition(T(x), T(gid.astype(np.int64)), P, l, r, q, owner, boxes, internal, local_rows, counts, send_idx)
+    assert np.array_equal(N(counts), h)
+    return N(owner), N(boxes).reshape(P, 2, dim), N(internal).reshape(P, 2, dim), N(local_rows), h, N(send_idx)
+
+
+PCASES = [
+    ("u2d_P4", lambda g: g.random((2000, 2)), 4, 0.1),
+    ("u3d_P8", lambda g: g.random((3000, 3)), 8, 0.12),
+    ("u2d_P2", lambda g: g.random((501, 2)), 2, 0.05),
+    ("P1", lambda g: g.random((300, 2)), 1, 0.1),
+    ("grid_P4", lambda g: _grid(33, 2), 4, 0.1),
+    ("grid3d_P8", lambda g: _grid(12, 3), 8, 0.2),
+    ("neg_coords_P4", lambda g: g.random((1000, 2)) * 6 - 3, 4, 0.3),
+]
+
+
+@pytest.mark.parametrize("name,gen,P,r", PCASES, ids=[c[0] for c in PCASES])
+def test_partition_bit_exact(L, name, gen, P, r):
+    g = np.random.default_rng(zlib.crc32(name.encode()) % 997)
+    x = gen(g).astype(np.float32)
+    n = len(x)
+    gid = g.permutation(5 * n)[:n].astype(np.int64)
+    for l in (r, 0.0, 0.5 * r):
+        o_owner, o_boxes, o_int, ranks = partition.plan(x, gid, P, l, r)
+        for q in range(P):
+            owner, boxes, internal, lr, h, sidx = _plan_gpu(L, x, gid, P, l, r, q)
+            assert np.array_equal(owner, o_owner)
+            assert np.array_equal(boxes.view(np.uint32), o_boxes.view(np.uint32))
+            assert np.array_equal(internal.astype(bool), o_int)
+            rq = ranks[q]
+            n_loc = len(rq["local_rows"])
+            assert h[0] == rq["n_deep"] and h[1] == rq["n_near"] and h[2] == rq["n_halo"]
+            assert np.array_equal(lr[:n_loc], rq["local_rows"])
+            assert list(h[4:4 + P + 1]) == list(rq["halo_ptr"])
+            assert list(h[5 + P:5 + 2 * P + 1]) == list(rq["send_ptr"])
+            assert np.array_equal(sidx[:h[3]], rq["send_idx"])
+
+
+def test_partition_degenerate(L):
+    x = np.zeros((16, 2), np.float32)
+    with pytest.raises(L.DsmpnnError) as ei:
+        _plan_gpu(L, x, np.arange(16), 2, 0.1, 0.1, 0)
+    assert ei.value.status == -9
+
+
+@pytest.mark.parametrize("mode", ["diff", "concat"])
+def test_edge_features_bit_exact(L, mode):
+    g = np.random.default_rng(8)
+    x = g.random((400, 3)).astype(np.float32)
+    a = g.normal(size=(400, 3)).astype(np.float32)
+    gid = np.arange(400)
+    rp, col = graph.radius_graph(x, gid, 300, 0.15, 16, 4)
+    want = features.edge_features(mode, x, a, features.dst_of_edges(rp), col)
+    E = len(col)
+    e32 = torch.empty((E, want.shape[1]), dtype=torch.float32, device=cuda())
+    e16 = torch.empty((E, 16), dtype=torch.bfloat16, device=cuda())
+    m = L.EDGE_DIFF if mode == "diff" else L.EDGE_CONCAT
+    L.edge_features(m, T(x), T(a), T(rp), T(col), 300, e32, e16)
+    assert np.array_equal(N(e32), want)
+    w16 = synth.round_bf16(want)
+    got16 = N(e16)
+    assert np.array_equal(got16[:, :want.shape[1]], w16)
+    assert not got16[:, want.shape[1]:].any()
+
+
+def test_csc_view(L):
+    g = np.random.default_rng(9)
+    x = g.random((500, 2)).astype(np.float32)
+    rp, col = graph.radius_graph(x, np.arange(500), 400, 0.1, 12, 4)
+    E = len(col)
+    perm = torch.empty(E, dtype=torch.int32, device=cuda())
+    ptr = torch.empty(501, dtype=torch.int64, device=cuda())
+    L.csc(T(col), 500, perm, ptr)
+    want_perm = np.lexsort((np.arange(E), col))
+    assert np.array_equal(N(perm), want_perm)
+    assert np.array_equal(N(ptr), np.searchsorted(col[want_perm], np.arange(501), side="left"))

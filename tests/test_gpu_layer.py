@@ -1,0 +1,194 @@
+"""GPU parity for a4/a5 (layer forward) and a7 (layer backward) against the
+fp64 oracle: normwise-inf relative error <= 1e-5 in F32 mode and <= 2e-2 in
+BF16 mode (BASELINE.json north_star), on every output and gradient."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import features, graph, layer, sample
+from oracle.layer import LayerDesc
+from paper_2402_15106_b200 import synth
+from gpu_util import T, N, cuda, hash_rows, nerr
+
+pytestmark = pytest.mark.gpu
+
+TOL = {0: 1e-5, 1: 2e-2}
+GNAMES = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2402_15106_b200 import build
+    build.build()
+    from paper_2402_15106_b200 import _lib
+    return _lib
+
+
+def _problem(n, dim, r, n_e, d_e_mode, d, k, seed, n_dst=None, isolated=0):
+    """Oracle-built graph + inputs (nothing comes from the CUDA path)."""
+    g = np.random.default_rng(seed)
+    x = g.random((n, dim)).astype(np.float32)
+    if isolated:
+        x[-isolated:] += 50.0 + 10 * np.arange(isolated, dtype=np.float32)[:, None]
+    a = g.normal(size=(n, 1)).astype(np.float32)
+    gid = g.permutation(10 * n)[:n].astype(np.int64)
+    n_dst = n if n_dst is None else n_dst
+    rp, col = graph.radius_graph(x, gid, n_dst, r, n_e, seed)
+    e = features.edge_features(d_e_mode, x, a, features.dst_of_edges(rp), col)
+    d_e = e.shape[1]
+    W = synth.weights(d_e, d, d, k, salt=seed)
+    v = synth.node_features(n, d, salt=seed)
+    G = synth.upstream_grad(n_dst, d, salt=seed)
+    return dict(x=x, a=a, gid=gid, rp=rp, col=col, e=e, W=W, v=v, G=G, n_dst=n_dst, n=n, d_e=d_e, d=d, k=k)
+
+
+def _to_dtype_inputs(p, dtype):
+    """BF16 mode: the oracle receives the bf16-rounded v, e, W1, W2, W3, b3, W_root."""
+    if dtype == 0:
+        return p["v"], p["e"], p["W"]
+    W = dict(p["W"])
+    for n in ("W1", "W2", "W3", "b3", "W_root"):
+        W[n] = synth.round_bf16(W[n])
+    return synth.round_bf16(p["v"]), synth.round_bf16(p["e"]), W
+
+
+def _run_gpu(L, p, dtype, root, act, ranges=None, want_bwd=True, G=None):
+    d, k, d_e = p["d"], p["k"], p["d_e"]
+    desc = L.make_desc(d_e, d, d, k, dtype, root, act)
+    Wd = {n: T(p["W"][n]) for n in GNAMES}
+    packed = torch.empty(L.packed_weights_size(desc), dtype=torch.uint8, device=cuda())
+    L.pack_weights(desc, Wd, packed)
+    n, n_dst = p["n"], p["n_dst"]
+    E = len(p["col"])
+    if dtype == 0:
+        v = T(p["v"])
+        e = T(p["e"]) if E else torch.zeros((1, d_e), device=cuda())
+    else:
+        v = T(p["v"]).to(torch.bfloat16)
+        e16 = np.zeros((max(E, 1), 16), np.float32)
+        e16[:E, :d_e] = p["e"]
+        e = T(e16).to(torch.bfloat16)
+    rp = T(p["rp"])
+    col = T(p["col"]) if E else torch.zeros(1, dtype=torch.int32, device=cuda())
+    out = torch.full((n_dst, d), float("nan"), device=cuda())
+    ws = torch.empty(L.layer_workspace_size(desc, n_dst, E), dtype=torch.uint8, device=cuda())
+    rph = torch.from_numpy(p["rp"])
+    for (a, b) in (ranges or [(0, n_dst)]):
+        L.layer_fwd(desc, Wd, packed, v, e, rp, col, n_dst, a, b, out, None, ws, row_ptr_host=rph)
+    res = dict(out=N(out))
+    if not want_bwd:
+        return res
+    perm = torch.empty(max(E, 1), dtype=torch.int32, device=cuda())
+    cptr = torch.empty(n + 1, dtype=torch.int64, device=cuda())
+    L.csc(col[:E], n, perm, cptr)
+    gv = torch.zeros((n, d), device=cuda())
+    ge = torch.zeros((max(E, 1), d_e), device=cuda())
+    grads = {nm: torch.zeros_like(Wd[nm]) for nm in GNAMES}
+    bws = torch.empty(L.layer_bwd_workspace_size(desc, n_dst, n, E), dtype=torch.uint8, device=cuda())
+    Gt = T(p["G"] if G is None else G)
+    L.layer_bwd(desc, Wd, packed, v, e, rp, col, perm, cptr, n_dst, n, 0, n_dst, Gt, gv, ge if dtype == 0 else None,
+                grads, ws, bws, row_ptr_host=rph)
+    torch.cuda.synchronize()
+    res.update(dv=N(gv), de=N(ge)[:E], grads={nm: N(t) for nm, t in grads.items()})
+    return res
+
+
+def _oracle(p, dtype, root, act, rows=None, G=None):
+    v, e, W = _to_dtype_inputs(p, dtype)
+    desc = LayerDesc(p["d_e"], p["d"], p["d"], p["k"], root, act)
+    out, _ = layer.layer_fwd(desc, W, v, e, p["rp"], p["col"], rows=rows)
+    Gr = p["G"] if G is None else G
+    if rows is not None:
+        Gr = Gr[rows]
+    dv, de, g = layer.layer_bwd(desc, W, v, e, p["rp"], p["col"], Gr, rows=rows)
+    return dict(out=out, dv=dv, de=de, grads=g)
+
+
+COMBOS = [(2, 1), (1, 0), (0, 1), (0, 0)]  # (root, act): GNO form, paper form, ...
+
+
+@pytest.mark.parametrize("root,act", COMBOS)
+def test_fwd_bwd_f32_tiny(L, root, act):
+    # BASELINE configs[0]-sized problem: 64 nodes, r = 0.25, width 16, k = 32
+    p = _problem(64, 2, 0.25, 64, "diff", 16, 32, seed=11)
+    got = _run_gpu(L, p, 0, root, act)
+    ref = _oracle(p, 0, root, act)
+    assert nerr(got["out"], ref["out"]) <= TOL[0]
+    assert nerr(got["dv"], ref["dv"]) <= TOL[0]
+    assert nerr(got["de"], ref["de"]) <= TOL[0]
+    for nm in GNAMES:
+        if root != 2 and nm == "W_root":
+            continue
+        assert nerr(got["grads"][nm], ref["grads"][nm]) <= TOL[0], nm
+
+
+def test_f32_tiles_ragged_and_empty_rows(L):
+    # several GEMM tiles with ragged tails, capped rows, isolated (deg 0) rows,
+    # n_dst < n_loc (halo-like sources), odd widths
+    p = _problem(700, 3, 0.18, 24, "concat", 24, 40, seed=12, n_dst=611, isolated=5)
+    p["n_dst"] = 611
+    got = _run_gpu(L, p, 0, 2, 1)
+    ref = _oracle(p, 0, 2, 1)
+    for key in ("out", "dv", "de"):
+        assert nerr(got[key], ref[key]) <= TOL[0], key
+    for nm in GNAMES:
+        assert nerr(got["grads"][nm], ref["grads"][nm]) <= TOL[0], nm
+
+
+def test_f32_row_ranges_equal_full(L):
+    p = _problem(300, 2, 0.15, 32, "diff", 16, 32, seed=13)
+    full = _run_gpu(L, p, 0, 2, 1, want_bwd=False)
+    split = _run_gpu(L, p, 0, 2, 1, ranges=[(0, 97), (97, 98), (98, 300)], want_bwd=False)
+    assert np.array_equal(full["out"], split["out"])
+
+
+def test_f32_deterministic(L):
+    p = _problem(400, 2, 0.12, 32, "diff", 16, 32, seed=14)
+    a = _run_gpu(L, p, 0, 2, 1)
+    b = _run_gpu(L, p, 0, 2, 1)
+    assert np.array_equal(a["out"], b["out"]) and np.array_equal(a["dv"], b["dv"])
+    for nm in GNAMES:
+        assert np.array_equal(a["grads"][nm], b["grads"][nm])
+
+
+def _darcy_full(L, dtype, n_rows):
+    """configs[1] sizes (d = 64, k = 256, n_e = 64, 16,384 sampled nodes of the
+    241^2 grid) on one 4,096-node-ish sub-domain-sized slice: the GPU runs every
+    row; the oracle checks sampled rows and the masked-upstream backward."""
+    cfg = synth.CONFIGS["darcy"]
+    coords, attr = synth.points(cfg)
+    ids = sample.sample(len(coords), cfg.s, synth.BASE_SEED + synth.SEED_SAMPLING)
+    x, a = coords[ids], attr[ids]
+    gid = ids.astype(np.int64)
+    # sub-domain sized: destinations = 4096 nodes nearest the lower-left quadrant (all sources kept)
+    n = len(x)
+    n_dst = 4096
+    order = np.lexsort((gid, np.maximum(x[:, 0], x[:, 1])))
+    x, a, gid = x[order], a[order], gid[order]
+    rows = hash_rows(n_dst, n_rows)
+    seedc = synth.BASE_SEED + synth.SEED_CAPPING
+    # oracle graph rows (sampled) and full graph for the GPU input: the full
+    # CSR is assembled from oracle rows too, so no input comes from the CUDA path
+    adj = graph.radius_graph_rows(x, gid, range(n_dst), cfg.r, cfg.n_e, seedc)
+    rp = np.zeros(n_dst + 1, np.int64)
+    rp[1:] = np.cumsum([len(r_) for r_ in adj])
+    col = np.concatenate(adj).astype(np.int32)
+    e = features.edge_features("diff", x, a, features.dst_of_edges(rp), col)
+    d, k = cfg.d, cfg.k
+    W = synth.weights(e.shape[1], d, d, k)
+    v = synth.node_features(n, d)
+    G = np.zeros((n_dst, d), np.float32)
+    G[rows] = synth.upstream_grad(n_dst, d)[rows]
+    p = dict(x=x, a=a, gid=gid, rp=rp, col=col, e=e, W=W, v=v, G=G, n_dst=n_dst, n=n, d_e=e.shape[1], d=d, k=k)
+    got = _run_gpu(L, p, dtype, 2, 1)
+    ref = _oracle(p, dtype, 2, 1, rows=rows)
+    assert nerr(got["out"][rows], ref["out"]) <= TOL[dtype]
+    assert nerr(got["dv"], ref["dv"]) <= TOL[dtype]
+    if dtype == 0:
+        assert nerr(got["de"], ref["de"]) <= TOL[dtype]
+    for nm in GNAMES:
+        assert nerr(got["grads"][nm], ref["grads"][nm]) <= TOL[dtype], nm
+
+
+def test_f32_darcy_full_size_sampled(L):
+    _darcy_full(L, 0, 24)

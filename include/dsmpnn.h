@@ -228,6 +228,36 @@ dsmpnn_status dsmpnn_halo_exchange_loopback(int32_t nparts, void *const *values,
                                             const int64_t *const *send_ptr, const int32_t *const *send_idx,
                                             int32_t width, int32_t dtype, void *stream);
 
+/* --------------------------------------------------------------- GEMM --- */
+/* Dense bf16 GEMM on the tcgen05 tensor cores, fp32 accumulate:
+ *   C[M x N] (+)= A[M x K] . B[K x N]
+ * A stored [M][K] (a_mn_major = 0) or [K][M] (1) with row stride lda elements;
+ * B stored [N][K] (b_mn_major = 0) or [K][N] (1) with row stride ldb.  Base
+ * pointers and row strides must be 16-byte aligned.  splits > 1 splits K
+ * across CTAs into `partial` (fp32 [splits x M x N], caller-owned) and sums
+ * the slices in a fixed order (deterministic).  The building block of the
+ * BF16 layer's dense contractions, exported for testing. */
+dsmpnn_status dsmpnn_gemm_bf16(int64_t M, int64_t N, int64_t K, const void *A, int64_t lda, int32_t a_mn_major,
+                               const void *B, int64_t ldb, int32_t b_mn_major, float *C, int64_t ldc, int32_t splits,
+                               float *partial, int32_t accumulate, void *stream);
+
+/* ------------------------------------------------------------ probes --- */
+/* Live kernel timing for the benchmark's roofline figure: while a probe is
+ * armed, the library records a CUDA event pair on the launching stream around
+ * every launch of the selected kernel; dsmpnn_probe_end synchronises those
+ * events and returns the summed duration and the number of launches.
+ * kernel_id: one of dsmpnn_probe_kernel.  Not thread safe (bench use). */
+typedef enum {
+  DSMPNN_PROBE_NONE = 0,
+  DSMPNN_PROBE_F32_MLP2 = 1,      /* F32: h = relu(a1 W2^T + b2) GEMM */
+  DSMPNN_PROBE_F32_EDGE_BWD = 2,  /* F32: per-row dh / u kernel */
+  DSMPNN_PROBE_BF16_EDGE_FWD = 3, /* BF16: fused kappa MLP + S formation (tcgen05) */
+  DSMPNN_PROBE_BF16_NODE_GEMM = 4,/* BF16: [S~ | v] . [Theta~ ; W_root^T] GEMM + epilogue (tcgen05) */
+  DSMPNN_PROBE_BF16_EDGE_BWD = 5  /* BF16: fused edge backward (tcgen05) */
+} dsmpnn_probe_kernel;
+dsmpnn_status dsmpnn_probe_begin(int32_t kernel_id, int32_t max_launches);
+dsmpnn_status dsmpnn_probe_end(float *total_ms /*host*/, int64_t *launches /*host*/);
+
 #ifdef __cplusplus
 }
 #endif

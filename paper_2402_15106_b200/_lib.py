@@ -89,6 +89,9 @@ _f = {
     "halo_scatter_add": _sig("halo_scatter_add", P, P, I64, I32, P, P),
     "halo_exchange_loopback": _sig("halo_exchange_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
                                    C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, P),
+    "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
+    "probe_begin": _sig("probe_begin", I32, I32),
+    "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
 }
 
 EXPORTED = sorted(["dsmpnn_" + k for k in _f] + ["dsmpnn_last_error", "dsmpnn_version"])
@@ -264,3 +267,32 @@ def halo_exchange_loopback(values_list, halo_ptr_list, send_ptr_list, send_idx_l
     spp = (C.POINTER(I64) * P_)(*[C.cast(s, C.POINTER(I64)) for s in sp])
     sidx = (P * P_)(*[s.data_ptr() for s in send_idx_list])
     _call("halo_exchange_loopback", P_, vals, hpp, spp, sidx, width, dtype, _stream(stream))
+
+
+def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=None, accumulate=False,
+              M=None, N=None, K=None, stream=None):
+    """C (+)= A . B with A [M,K] (or stored [K,M] if a_mn_major) and B [K,N]
+    (stored [N,K] if not b_mn_major, [K,N] if b_mn_major), bf16 in, fp32 out."""
+    if M is None:
+        M = A.shape[1] if a_mn_major else A.shape[0]
+        K = A.shape[0] if a_mn_major else A.shape[1]
+        N = B.shape[1] if b_mn_major else B.shape[0]
+    _call("gemm_bf16", M, N, K, _p(A), A.stride(0), int(a_mn_major), _p(B), B.stride(0), int(b_mn_major), _p(C),
+          C.stride(0), splits, _p(partial), int(accumulate), _stream(stream))
+    return C
+
+
+# ---------------------------------------------------------------- probes --
+PROBE_F32_MLP2, PROBE_F32_EDGE_BWD = 1, 2
+PROBE_BF16_EDGE_FWD, PROBE_BF16_NODE_GEMM, PROBE_BF16_EDGE_BWD = 3, 4, 5
+
+
+def probe_begin(kernel_id, max_launches=4096):
+    _call("probe_begin", kernel_id, max_launches)
+
+
+def probe_end():
+    ms = F(0.0)
+    n = I64(0)
+    _call("probe_end", C.byref(ms), C.byref(n))
+    return float(ms.value), int(n.value)

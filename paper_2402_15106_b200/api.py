@@ -1,0 +1,172 @@
+"""Public API: one DS-MPNN hot-path step (graph build + L layers forward with a
+halo refresh after each + L layers backward + gradient sum) over the C ABI.
+
+PAPER.md Alg. 1 (:385-422): lines 391-397 (sample, decompose, edge index,
+edge sampling, edge attributes), 404-411 (per-hop convolution with residual
+and overlap communication), 417-418 (local backprop, gradient sum).  The
+encoder/decoder and the optimiser are outside the hot path.
+
+A process owns one or more sub-domains ("virtual ranks"); halos between
+sub-domains on the same device are device copies, halos between processes go
+through torch.distributed (NCCL) point-to-point.  Received halo values are
+detached (reading R16): the backward drops gradients of halo rows.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import pipeline
+
+GNAMES = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
+
+
+@dataclass
+class StepConfig:
+    n_points: int
+    s: int
+    dim: int
+    n_attr: int
+    nparts: int
+    r: float
+    overlap_l: float
+    n_e: int
+    d: int
+    k: int
+    L: int
+    edge_mode: int
+    dtype: int = L.BF16
+    root: int = L.ROOT_DENSE
+    act: int = L.ACT_RELU
+    seed_sampling: int = 0
+    seed_capping: int = 0
+
+
+def parts_of_process(nparts, world, rank):
+    """Block mapping of sub-domains to processes (nparts is a multiple of world)."""
+    per = nparts // world
+    return list(range(rank * per, (rank + 1) * per))
+
+
+class HotPath:
+    def __init__(self, cfg: StepConfig, weights: dict, device, rank=0, world=1, group=None):
+        assert cfg.nparts % world == 0, "sub-domain count must be a multiple of the process count"
+        self.cfg, self.dev, self.rank, self.world, self.group = cfg, device, rank, world, group
+        self.my_parts = parts_of_process(cfg.nparts, world, rank)
+        self.proc_of = [p // (cfg.nparts // world) for p in range(cfg.nparts)]
+        d_e = (cfg.dim + cfg.n_attr) * (1 if cfg.edge_mode == L.EDGE_DIFF else 2)
+        self.d_e = d_e
+        self.desc = L.make_desc(d_e, cfg.d, cfg.d, cfg.k, cfg.dtype, cfg.root, cfg.act)
+        self.W = {n: torch.as_tensor(np.ascontiguousarray(weights[n]), dtype=torch.float32).to(device)
+                  for n in GNAMES}
+        self.packed = torch.empty(L.packed_weights_size(self.desc), dtype=torch.uint8, device=device)
+        L.pack_weights(self.desc, self.W, self.packed)
+        self.grads = {n: torch.zeros_like(t) for n, t in self.W.items()}
+        self.flat_grads = None
+        self.subs = []
+        self.ws = {}
+
+    # ------------------------------------------------------------- graph --
+    def build(self, coords, attr):
+        """Alg. 1 lines 391-397 on device-resident points (float32 [N x dim], [N x n_attr])."""
+        c = self.cfg
+        ids = pipeline.sample_nodes(c.n_points, c.s, c.seed_sampling, self.dev)
+        self.ids = ids
+        ids64 = ids.to(torch.int64)
+        cs = torch.empty((ids.numel(), c.dim), dtype=torch.float32, device=self.dev)
+        L.gather_rows(coords, ids64, cs)
+        a = torch.empty((ids.numel(), c.n_attr), dtype=torch.float32, device=self.dev)
+        L.gather_rows(attr, ids64, a)
+        self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts)
+        for sd in self.subs:
+            pipeline.build_graph(sd, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
+                                 want_bf16=(c.dtype == L.BF16))
+        return self
+
+    @property
+    def n_edges(self):
+        return sum(sd.n_edges for sd in self.subs)
+
+    # ------------------------------------------------------------ layers --
+    def _ws(self, key, nbytes):
+        t = self.ws.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(1, int(nbytes)), dtype=torch.uint8, device=self.dev)
+            self.ws[key] = t
+        return t
+
+    def halo(self, vals, dtype):
+        """Overlap update (Alg. 1) for every local sub-domain."""
+        if self.world == 1:
+            pipeline.halo_exchange_loopback(self.subs, vals, dtype)
+        else:
+            pipeline.halo_exchange_mixed(self.subs, vals, dtype, self.proc_of, self.rank, self.group)
+
+    def forward_backward(self, v0, G):
+        """v0: [s x d] initial latent of the sampled nodes (sampled order);
+        G: [s x d] dL/d(last layer output) (rows of owned nodes are used).
+        Returns the accumulated weight gradients (dict of device tensors)."""
+        c, desc = self.cfg, self.desc
+        lowp = c.dtype == L.BF16
+        vdt = torch.bfloat16 if lowp else torch.float32
+        for g in self.grads.values():
+            g.zero_()
+        # layer-0 inputs of every sub-domain (local order)
+        vals = []
+        for sd in self.subs:
+            v = torch.empty((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
+            L.gather_rows(v0, sd.local_rows, v)
+            vals.append(v.to(vdt) if lowp else v)
+        acts = [vals]
+        for layer in range(c.L):
+            nxt = []
+            for q, sd in enumerate(self.subs):
+                ws = self._ws(("fwd", layer, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
+                out = self._ws(("out", q), sd.n_own * c.d * 4).view(torch.float32)[: sd.n_own * c.d].view(sd.n_own, c.d)
+                nv = torch.empty((sd.n_loc, c.d), dtype=vdt, device=self.dev)
+                e = sd.e16 if lowp else sd.e32
+                L.layer_fwd(desc, self.W, self.packed, acts[-1][q], e, sd.row_ptr, sd.col_idx, sd.n_own, 0, sd.n_own,
+                            out, nv[: sd.n_own] if lowp else None, ws, row_ptr_host=sd.row_ptr_host)
+                if not lowp:
+                    nv[: sd.n_own].copy_(out)
+                nxt.append(nv)
+            self.halo(nxt, L.BF16 if lowp else L.F32)
+            acts.append(nxt)
+        # backward: DETACH halo rows (R16)
+        gouts = []
+        for sd in self.subs:
+            g = torch.empty((sd.n_own, c.d), dtype=torch.float32, device=self.dev)
+            L.gather_rows(G, sd.local_rows[: sd.n_own], g)
+            gouts.append(g)
+        for layer in reversed(range(c.L)):
+            new_g = []
+            for q, sd in enumerate(self.subs):
+                ws = self.ws[("fwd", layer, q)]
+                bws = self._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
+                gv = torch.zeros((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
+                e = sd.e16 if lowp else sd.e32
+                L.layer_bwd(desc, self.W, self.packed, acts[layer][q], e, sd.row_ptr, sd.col_idx, sd.csc_perm,
+                            sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, gouts[q], gv, None, self.grads, ws, bws,
+                            row_ptr_host=sd.row_ptr_host)
+                new_g.append(gv[: sd.n_own])
+            gouts = new_g
+        if self.world > 1:
+            self._allreduce_grads()
+        return self.grads
+
+    def _allreduce_grads(self):
+        """Gradient sum over processes (Alg. 1), one NCCL all-reduce."""
+        import torch.distributed as dist
+        flat = torch.cat([self.grads[n].reshape(-1) for n in GNAMES])
+        dist.all_reduce(flat, group=self.group)
+        off = 0
+        for n in GNAMES:
+            m = self.grads[n].numel()
+            self.grads[n].copy_(flat[off:off + m].view_as(self.grads[n]))
+            off += m
+
+    def step(self, coords, attr, v0, G):
+        """One full hot-path step on device inputs."""
+        self.build(coords, attr)
+        return self.forward_backward(v0, G)

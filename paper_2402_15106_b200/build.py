@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdsmpnn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "layer.cu", "layer_bf16.cu"]
+SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]
@@ -49,7 +49,7 @@ def build(force=False, verbose=False):
         for src, out in failed:
             sys.stderr.write(f"--- nvcc failed on {src}\n{out}\n")
         raise RuntimeError("libdsmpnn build failed: " + ", ".join(s for s, _ in failed))
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart", "-lcuda"]
     subprocess.run(cmd, check=True)
     return LIB
 

@@ -63,4 +63,16 @@ static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int kNumSMs = 148;
 
+// live timing probe (dsmpnn_probe_begin/end): true if launches of `id` are recorded
+bool probe_armed(int id);
+void probe_before(int id, cudaStream_t s);
+void probe_after(int id, cudaStream_t s);
+struct ProbeScope {
+  int id;
+  cudaStream_t s;
+  bool on;
+  ProbeScope(int id_, cudaStream_t s_) : id(id_), s(s_), on(probe_armed(id_)) { if (on) probe_before(id, s); }
+  ~ProbeScope() { if (on) probe_after(id, s); }
+};
+
 }  // namespace dsmpnn

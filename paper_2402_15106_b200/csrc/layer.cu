@@ -281,6 +281,7 @@ static dsmpnn_status fwd_f32(const dsmpnn_layer_desc &d, const dsmpnn_weights &w
     SgemmArgs g1{nE, d.k, d.d_e, e + eb * d.d_e, d.d_e, 1, w.W1, 1, d.d_e, f.A1 + eb * d.k, d.k, w.b1, 1, 0, 1.f};
     DS_TRY(sgemm(g1, 1, nullptr, s));
     SgemmArgs g2{nE, d.k, d.k, f.A1 + eb * d.k, d.k, 1, w.W2, 1, d.k, f.H + eb * d.k, d.k, w.b2, 1, 0, 1.f};
+    ProbeScope probe(DSMPNN_PROBE_F32_MLP2, s);
     DS_TRY(sgemm(g2, 1, nullptr, s));
   }
   if (nR > 0) {
@@ -353,6 +354,7 @@ static dsmpnn_status bwd_f32(const dsmpnn_layer_desc &d, const dsmpnn_weights &w
   {
     size_t smem = (size_t)(Kt + kEdgeChunk * d.d_in) * sizeof(float);
     DS_CUDA(cudaFuncSetAttribute(edge_bwd_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ProbeScope probe(DSMPNN_PROBE_F32_EDGE_BWD, s);
     edge_bwd_f32_kernel<<<(unsigned)nR, 256, smem, s>>>(b.dS, f.H, v, row_ptr, col, rb, d.k, d.d_in, b.dZ2, b.U);
     DS_LAUNCH_CHECK();
   }

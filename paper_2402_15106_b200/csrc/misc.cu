@@ -3,6 +3,8 @@
 #include <cub/cub.cuh>
 #include <stdarg.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace dsmpnn {
@@ -104,6 +106,22 @@ __global__ void csc_ptr_kernel(const int32_t *__restrict__ sorted_col, int64_t n
   }
 }
 
+// ---------------------------------------------------------------- probe --
+struct Probe {
+  int id = 0;
+  int cap = 0;
+  int n = 0;
+  std::vector<cudaEvent_t> ev;  // 2 per launch
+};
+static Probe g_probe;
+
+bool probe_armed(int id) { return g_probe.id == id && id != 0 && g_probe.n < g_probe.cap; }
+void probe_before(int id, cudaStream_t s) { cudaEventRecord(g_probe.ev[2 * g_probe.n], s); }
+void probe_after(int id, cudaStream_t s) {
+  cudaEventRecord(g_probe.ev[2 * g_probe.n + 1], s);
+  g_probe.n++;
+}
+
 static int grid_for(int64_t n, int block = 256) {
   int64_t g = ceil_div(n, block);
   if (g < 1) g = 1;
@@ -119,6 +137,34 @@ extern "C" {
 
 const char *dsmpnn_last_error(void) { return g_last_error.c_str(); }
 int32_t dsmpnn_version(void) { return 1; }
+
+dsmpnn_status dsmpnn_probe_begin(int32_t kernel_id, int32_t max_launches) {
+  DS_CHECK_ARG(max_launches >= 0 && max_launches <= 1 << 20, DSMPNN_ERR_INVALID_ARG, "probe: max_launches");
+  while ((int)g_probe.ev.size() < 2 * max_launches) {
+    cudaEvent_t e;
+    DS_CUDA(cudaEventCreate(&e));
+    g_probe.ev.push_back(e);
+  }
+  g_probe.id = kernel_id;
+  g_probe.cap = max_launches;
+  g_probe.n = 0;
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_probe_end(float *total_ms, int64_t *launches) {
+  double tot = 0.0;
+  for (int i = 0; i < g_probe.n; ++i) {
+    DS_CUDA(cudaEventSynchronize(g_probe.ev[2 * i + 1]));
+    float ms = 0.f;
+    DS_CUDA(cudaEventElapsedTime(&ms, g_probe.ev[2 * i], g_probe.ev[2 * i + 1]));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = (float)tot;
+  if (launches) *launches = g_probe.n;
+  g_probe.id = 0;
+  g_probe.n = 0;
+  return DSMPNN_OK;
+}
 
 dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
                                  int32_t elem_bytes, void *out, void *stream) {

@@ -1,0 +1,273 @@
+// tgemm.cu - bf16 GEMM on the 5th-generation tensor cores (sm_100a).
+//
+// One CTA per 128 x BN output tile (and per split-K slice).  Warp 0 (one
+// elected lane) streams 128x64 A and BNx64 B tiles with TMA into a 4-stage
+// shared-memory ring (128-byte swizzle); warp 1 (one elected lane) issues
+// tcgen05.mma (M=128, N=BN, K=16) accumulating in TMEM and releases ring
+// slots with tcgen05.commit; then all 4 warps drain TMEM (tcgen05.ld
+// 32x32b, one thread per output row) to fp32 global memory.  TMA zero-fills
+// out-of-range boxes, so ragged M/N/K tails need no special path.
+#include <cuda.h>
+
+#include "tc.cuh"
+#include "tgemm.cuh"
+
+namespace dsmpnn {
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous), `outer` rows of
+// `ld` elements; box {box_inner, box_outer}; swizzle from the box row bytes.
+dsmpnn_status make_tmap_bf16(CUtensorMap *m, const void *base, int64_t inner, int64_t outer, int64_t ld,
+                             int box_inner, int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  DS_CHECK_ARG(fn != nullptr, DSMPNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  DS_CHECK_ARG(((uintptr_t)base & 15) == 0 && ((ld * 2) & 15) == 0, DSMPNN_ERR_SHAPE,
+               "TMA operand needs 16-byte aligned base and row stride (ld=%lld)", (long long)ld);
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  int row_bytes = box_inner * 2;
+  CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DS_CHECK_ARG(r == CUDA_SUCCESS, DSMPNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DSMPNN_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+struct TG {
+  static constexpr int BM = 128, BK = 64, STAGES = 4;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
+  static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
+  static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(128, 1)
+    tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int64_t M, int64_t N,
+                 int64_t K, int kb_per_split, float *__restrict__ C, int64_t ldc, int64_t split_stride,
+                 int accumulate, int splits) {
+  using T = TG<BN, A_MN, B_MN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + T::STAGES * T::A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + T::STAGES * T::B_BYTES);
+  uint64_t *empty = full + T::STAGES;
+  uint64_t *done = empty + T::STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * T::BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t nkb_total = (K + T::BK - 1) / T::BK;
+  const int64_t kb0 = (int64_t)blockIdx.z * kb_per_split;
+  const int64_t kb1 = kb0 + kb_per_split < nkb_total ? kb0 + kb_per_split : nkb_total;
+  const int nkb = (int)(kb1 > kb0 ? kb1 - kb0 : 0);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < T::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&ta);
+    tc::tma_prefetch(&tb);
+  }
+  if (warp == 1) tc::tmem_alloc<T::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (tc::elect_one()) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % T::STAGES;
+        const int r = i / T::STAGES;
+        if (r > 0) tc::mbar_wait(&empty[s], (r - 1) & 1);
+        tc::mbar_expect_tx(&full[s], T::A_BYTES + T::B_BYTES);
+        const int32_t kc = (int32_t)((kb0 + i) * T::BK);
+        uint8_t *a = sA + s * T::A_BYTES;
+        uint8_t *b = sB + s * T::B_BYTES;
+        if (!A_MN) {
+          tc::tma_load_2d(a, &ta, &full[s], kc, (int32_t)m0);
+        } else {
+          tc::tma_load_2d(a, &ta, &full[s], (int32_t)m0, kc);
+          tc::tma_load_2d(a + 8192, &ta, &full[s], (int32_t)(m0 + 64), kc);
+        }
+        if (!B_MN) {
+          tc::tma_load_2d(b, &tb, &full[s], kc, (int32_t)n0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / T::B_INNER; ++j)
+            tc::tma_load_2d(b + j * (T::B_ROW * T::BK), &tb, &full[s], (int32_t)(n0 + j * T::B_INNER), kc);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(T::BM, BN, A_MN, B_MN);
+    if (tc::elect_one()) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % T::STAGES;
+        tc::mbar_wait(&full[s], (i / T::STAGES) & 1);
+        tc::tc_fence_after();
+        const uint32_t a = tc::smem_u32(sA + s * T::A_BYTES);
+        const uint32_t b = tc::smem_u32(sB + s * T::B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < T::BK / 16; ++kk) {
+          uint64_t ad = A_MN ? tc::sdesc(a + kk * 2048, 8192, 1024, tc::kSw128)
+                             : tc::sdesc(a + kk * 32, 16, 1024, tc::kSw128);
+          uint64_t bd;
+          if (!B_MN) {
+            bd = tc::sdesc(b + kk * 32, 16, 1024, tc::kSw128);
+          } else {
+            constexpr uint32_t swz = T::B_ROW == 128 ? tc::kSw128 : (T::B_ROW == 64 ? tc::kSw64 : tc::kSw32);
+            bd = tc::sdesc(b + kk * 16 * T::B_ROW, T::B_ROW * T::BK, 8 * T::B_ROW, swz);
+          }
+          tc::mma_bf16_ss(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(done);
+    }
+    __syncwarp();
+  }
+  tc::mbar_wait(done, 0);
+  tc::tc_fence_after();
+
+  // epilogue: thread <-> row m0 + 32*warp + lane
+  const int64_t row = m0 + warp * 32 + lane;
+  float *out = C + (splits > 1 ? (int64_t)blockIdx.z * split_stride : 0);
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    tc::tmem_ld_wait();
+    if (row < M) {
+      float *dst = out + row * ldc + n0 + c0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (n0 + c0 + j < N) {
+          float x = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+          dst[j] = (accumulate && splits == 1) ? dst[j] + x : x;
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<T::TMEM_COLS>(tmem);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
+  using T = TG<BN, A_MN, B_MN>;
+  CUtensorMap ta, tb;
+  if (!A_MN) DS_TRY(make_tmap_bf16(&ta, a.A, a.K, a.M, a.lda, 64, 128));
+  else DS_TRY(make_tmap_bf16(&ta, a.A, a.M, a.K, a.lda, 64, 64));
+  if (!B_MN) DS_TRY(make_tmap_bf16(&tb, a.B, a.K, a.N, a.ldb, 64, BN));
+  else DS_TRY(make_tmap_bf16(&tb, a.B, a.N, a.K, a.ldb, T::B_INNER, 64));
+  auto kern = tgemm_kernel<BN, A_MN, B_MN>;
+  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
+  int64_t nkb = (a.K + 63) / 64;
+  int splits = a.splits < 1 ? 1 : a.splits;
+  int kbps = (int)ceil_div(nkb, splits);
+  if (kbps < 1) kbps = 1;
+  splits = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
+  dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.M, T::BM), (unsigned)splits);
+  kern<<<grid, 128, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a.C, a.ldc, a.split_stride, a.accumulate, splits);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+template <bool A_MN, bool B_MN>
+static dsmpnn_status dispatch_bn(const TgemmArgs &a, cudaStream_t s) {
+  if (a.N <= 16) return launch_tgemm<16, A_MN, B_MN>(a, s);
+  if (a.N <= 32) return launch_tgemm<32, A_MN, B_MN>(a, s);
+  if (a.N <= 64) return launch_tgemm<64, A_MN, B_MN>(a, s);
+  if (a.N <= 128) return launch_tgemm<128, A_MN, B_MN>(a, s);
+  return launch_tgemm<256, A_MN, B_MN>(a, s);
+}
+
+dsmpnn_status tgemm(const TgemmArgs &a, cudaStream_t s) {
+  if (a.M <= 0 || a.N <= 0) return DSMPNN_OK;
+  DS_CHECK_ARG(!(a.N > 64 && a.N % 64 != 0 && a.b_mn_major), DSMPNN_ERR_UNSUPPORTED,
+               "tgemm: N-major B with N > 64 needs N %% 64 == 0");
+  if (!a.a_mn_major && !a.b_mn_major) return dispatch_bn<false, false>(a, s);
+  if (!a.a_mn_major && a.b_mn_major) return dispatch_bn<false, true>(a, s);
+  if (a.a_mn_major && !a.b_mn_major) return dispatch_bn<true, false>(a, s);
+  return dispatch_bn<true, true>(a, s);
+}
+
+__global__ void splitk_sum_kernel(const float *__restrict__ p, int splits, int64_t stride, int64_t M, int64_t N,
+                                  int64_t ld, float *__restrict__ C, int64_t ldc, int accumulate) {
+  int64_t total = M * N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = t / N, n = t - m * N;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += p[z * stride + m * ld + n];
+    float *c = C + m * ldc + n;
+    *c = accumulate ? *c + s : s;
+  }
+}
+
+dsmpnn_status splitk_sum(const float *partial, int splits, int64_t split_stride, int64_t M, int64_t N, int64_t ld,
+                         float *C, int64_t ldc, int accumulate, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return DSMPNN_OK;
+  int g = (int)std::min<int64_t>(ceil_div(M * N, 256), 148 * 8);
+  splitk_sum_kernel<<<g, 256, 0, s>>>(partial, splits, split_stride, M, N, ld, C, ldc, accumulate);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+}  // namespace dsmpnn
+
+using namespace dsmpnn;
+
+extern "C" dsmpnn_status dsmpnn_gemm_bf16(int64_t M, int64_t N, int64_t K, const void *A, int64_t lda,
+                                          int32_t a_mn_major, const void *B, int64_t ldb, int32_t b_mn_major,
+                                          float *C, int64_t ldc, int32_t splits, float *partial, int32_t accumulate,
+                                          void *stream) {
+  DS_CHECK_ARG(M >= 0 && N >= 0 && K >= 0, DSMPNN_ERR_INVALID_ARG, "gemm_bf16: negative size");
+  cudaStream_t s = as_stream(stream);
+  if (splits > 1) {
+    DS_CHECK_ARG(partial != nullptr, DSMPNN_ERR_INVALID_ARG, "gemm_bf16: split-K needs a partial buffer");
+    TgemmArgs a{M, N, K, A, lda, a_mn_major != 0, B, ldb, b_mn_major != 0, partial, N, splits, M * N, 0};
+    DS_TRY(tgemm(a, s));
+    int64_t nkb = (K + 63) / 64;
+    int kbps = (int)std::max<int64_t>(1, ceil_div(nkb, splits));
+    int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
+    return splitk_sum(partial, real, M * N, M, N, N, C, ldc, accumulate, s);
+  }
+  TgemmArgs a{M, N, K, A, lda, a_mn_major != 0, B, ldb, b_mn_major != 0, C, ldc, 1, 0, accumulate};
+  return tgemm(a, s);
+}

@@ -107,26 +107,51 @@ def halo_exchange_loopback(subs, values, dtype):
                              [s.send_idx for s in subs], dtype)
 
 
-def halo_exchange_dist(sd: Subdomain, values, dtype, group=None, bufs=None):
-    """FORWARD halo refresh across processes: gather the send rows of every peer
-    into a contiguous buffer and exchange with NCCL send/recv (torch.distributed
-    batch_isend_irecv); receive slices are contiguous halo rows, so they land in
-    place."""
+def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gather=None):
+    """FORWARD halo refresh when sub-domains are spread over processes.
+
+    subs/values: this process's sub-domains and their [n_loc x width] arrays.
+    proc_of[p]: process holding sub-domain p.  A peer on the same process is a
+    device gather straight into the halo slice; a peer on another process is
+    a contiguous send buffer + NCCL send/recv (torch.distributed
+    batch_isend_irecv).  Receive slices are contiguous halo rows, so they land
+    in place.  Messages between two processes are issued in (source
+    sub-domain, destination sub-domain) order on both sides, which is how
+    NCCL matches them.  `gather(values, rows, out)` defaults to the library's
+    halo gather kernel."""
     import torch.distributed as dist
-    width = values.shape[1]
+    if gather is None:
+        def gather(vals, rows, out):
+            L.halo_gather(vals, rows, out, dtype)
+    local = {sd.rank: (sd, v) for sd, v in zip(subs, values)}
+    nparts = subs[0].nparts
     ops = []
-    for q in range(sd.nparts):
-        if q == sd.rank:
-            continue
-        s0, s1 = sd.send_ptr[q], sd.send_ptr[q + 1]
-        if s1 > s0:
-            buf = bufs[q] if bufs is not None else torch.empty((s1 - s0, width), dtype=values.dtype,
-                                                                device=values.device)
-            L.halo_gather(values, sd.send_idx[s0:s1], buf, dtype)
-            ops.append(dist.P2POp(dist.isend, buf, q, group))
-        a, b = sd.halo_ptr[q], sd.halo_ptr[q + 1]
-        if b > a:
-            ops.append(dist.P2POp(dist.irecv, values[a:b], q, group))
+    keep = []
+    for s_id in range(nparts):
+        for t_id in range(nparts):
+            if s_id == t_id:
+                continue
+            src_local, dst_local = s_id in local, t_id in local
+            if src_local and dst_local:
+                ssd, sv = local[s_id]
+                tsd, tv = local[t_id]
+                s0, s1 = ssd.send_ptr[t_id], ssd.send_ptr[t_id + 1]
+                a, b = tsd.halo_ptr[s_id], tsd.halo_ptr[s_id + 1]
+                if b > a:
+                    gather(sv, ssd.send_idx[s0:s1], tv[a:b])
+            elif src_local:
+                ssd, sv = local[s_id]
+                s0, s1 = ssd.send_ptr[t_id], ssd.send_ptr[t_id + 1]
+                if s1 > s0:
+                    buf = torch.empty((s1 - s0, sv.shape[1]), dtype=sv.dtype, device=sv.device)
+                    gather(sv, ssd.send_idx[s0:s1], buf)
+                    keep.append(buf)
+                    ops.append(dist.P2POp(dist.isend, buf, proc_of[t_id], group))
+            elif dst_local:
+                tsd, tv = local[t_id]
+                a, b = tsd.halo_ptr[s_id], tsd.halo_ptr[s_id + 1]
+                if b > a:
+                    ops.append(dist.P2POp(dist.irecv, tv[a:b], proc_of[s_id], group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()

@@ -1,27 +1,552 @@
-// layer_bf16.cu - BF16 mode (tcgen05) of the layer.  (stub: filled in next)
+// layer_bf16.cu - BF16 mode of the edge-conditioned convolution on the
+// tcgen05 tensor cores (sm_100a).  Formulation: DESIGN.md §4 ("aggregate
+// first", see layer.cu).  Widths supported: k = 256, d_in = d_out = D in
+// {32, 64}, d_e <= 16 (zero-padded).
+//
+// Forward of rows [rb, re):
+//   1. fill kernel   : S~_aug[i][k*D + c] = mean_p v_j[c]  (the h~ = 1 row),
+//                      S~_aug[i][(k+1)*D + c] = v_i[c]      (root operand),
+//                      zero S~ rows of isolated nodes.
+//   2. edge kernel   : per 128-slot tile (each row padded to a multiple of 16
+//                      slots): a1 = relu(E W1^T + b1), h = relu(a1 W2^T + b2)
+//                      as two tcgen05 GEMMs (W1, W2 resident in SMEM, D in
+//                      TMEM), then S_i = H_i^T V_i per row (tcgen05, A = H^T
+//                      read MN-major from the same SMEM tile, B = gathered v
+//                      rows), scaled by 1/deg_i -> S~_aug[i][kap*D + c] (bf16).
+//                      K_p = kappa(e_p) (D x D) is never formed.
+//   3. node GEMM     : [S~_aug] . [Theta~ ; W_root^T] on tcgen05 (split-K),
+//   4. node epilogue : + b (+ v_i), sigma, out (fp32), out_lowp (bf16), pre.
+#include <cuda.h>
+
 #include "layer_bf16.cuh"
+#include "simt.cuh"
+#include "tc.cuh"
+#include "tgemm.cuh"
 
 namespace dsmpnn {
 
+constexpr int KH = 256;  // kappa hidden width supported by the BF16 kernels
+
+static inline int64_t kpad_of(const dsmpnn_layer_desc &d) {
+  int64_t kp = (int64_t)(d.k + 2) * d.d_in;
+  return (kp + 63) / 64 * 64;
+}
+
+// ---------------------------------------------------------- packed weights
+struct Packed {
+  __nv_bfloat16 *W1;   // [KH x 16]   zero-padded d_e
+  __nv_bfloat16 *W2;   // [KH x KH]
+  __nv_bfloat16 *ThT;  // [D x Kpad]  Theta~_aug^T  (K-major B of the node GEMM)
+  __nv_bfloat16 *Th;   // [Kpad x D]  Theta~_aug    (K-major B of the dS GEMM)
+};
+static Packed carve_packed(const dsmpnn_layer_desc &d, void *base) {
+  Carver c(base, SIZE_MAX);
+  Packed p;
+  int64_t kp = kpad_of(d);
+  p.W1 = c.take<__nv_bfloat16>((int64_t)d.k * 16);
+  p.W2 = c.take<__nv_bfloat16>((int64_t)d.k * d.k);
+  p.ThT = c.take<__nv_bfloat16>((int64_t)d.d_out * kp);
+  p.Th = c.take<__nv_bfloat16>(kp * d.d_out);
+  return p;
+}
+
+__global__ void pack_bf16_kernel(const float *__restrict__ W1, const float *__restrict__ W2,
+                                 const float *__restrict__ W3, const float *__restrict__ b3,
+                                 const float *__restrict__ Wr, int root_dense, int k, int de, int di, int dout,
+                                 int64_t kp, Packed p) {
+  int64_t n1 = (int64_t)k * 16, n2 = (int64_t)k * k, n3 = kp * dout;
+  int64_t total = n1 + n2 + n3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < n1) {
+      int r = (int)(t / 16), c = (int)(t % 16);
+      p.W1[t] = __float2bfloat16_rn(c < de ? W1[(int64_t)r * de + c] : 0.f);
+    } else if (t < n1 + n2) {
+      p.W2[t - n1] = __float2bfloat16_rn(W2[t - n1]);
+    } else {
+      int64_t u = t - n1 - n2;
+      int64_t row = u / dout;  // Theta~_aug row
+      int o = (int)(u - row * dout);
+      int kap = (int)(row / di), c = (int)(row - (int64_t)kap * di);
+      float val = 0.f;
+      if (kap < k) val = W3[((int64_t)c * dout + o) * k + kap];
+      else if (kap == k) val = b3[(int64_t)c * dout + o];
+      else if (kap == k + 1 && root_dense) val = Wr[(int64_t)o * di + c];
+      __nv_bfloat16 bv = __float2bfloat16_rn(val);
+      p.Th[row * dout + o] = bv;
+      p.ThT[(int64_t)o * kp + row] = bv;
+    }
+  }
+}
+
 dsmpnn_status bf16_check_desc(const dsmpnn_layer_desc &d) {
-  DS_CHECK_ARG(false, DSMPNN_ERR_UNSUPPORTED, "layer: BF16 mode not built yet");
+  DS_CHECK_ARG(d.k == KH, DSMPNN_ERR_UNSUPPORTED, "layer BF16: k must be %d (got %d)", KH, d.k);
+  DS_CHECK_ARG(d.d_in == d.d_out && (d.d_in == 32 || d.d_in == 64), DSMPNN_ERR_UNSUPPORTED,
+               "layer BF16: d_in = d_out in {32, 64} (got %d, %d)", d.d_in, d.d_out);
+  DS_CHECK_ARG(d.d_e <= 16, DSMPNN_ERR_SHAPE, "layer BF16: d_e <= 16 (got %d)", d.d_e);
   return DSMPNN_OK;
 }
-size_t bf16_packed_bytes(const dsmpnn_layer_desc &) { return 0; }
-dsmpnn_status bf16_pack(const dsmpnn_layer_desc &, const dsmpnn_weights &, void *, cudaStream_t) {
-  return DSMPNN_ERR_UNSUPPORTED;
+
+size_t bf16_packed_bytes(const dsmpnn_layer_desc &d) {
+  Carver c(nullptr, 0);
+  int64_t kp = kpad_of(d);
+  c.take<__nv_bfloat16>((int64_t)d.k * 16);
+  c.take<__nv_bfloat16>((int64_t)d.k * d.k);
+  c.take<__nv_bfloat16>((int64_t)d.d_out * kp);
+  c.take<__nv_bfloat16>(kp * d.d_out);
+  return c.used();
 }
-size_t bf16_fwd_ws_bytes(const dsmpnn_layer_desc &, int64_t, int64_t) { return 0; }
-size_t bf16_bwd_ws_bytes(const dsmpnn_layer_desc &, int64_t, int64_t, int64_t) { return 0; }
-dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &, const dsmpnn_weights &, const __nv_bfloat16 *,
-                       const __nv_bfloat16 *, const int64_t *, const int32_t *, int64_t, int64_t, int64_t, int64_t,
-                       int64_t, int64_t, float *, __nv_bfloat16 *, void *, size_t, cudaStream_t) {
-  return DSMPNN_ERR_UNSUPPORTED;
+
+dsmpnn_status bf16_pack(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, void *packed, cudaStream_t s) {
+  DS_CHECK_ARG(d.root != DSMPNN_ROOT_DENSE || w.W_root, DSMPNN_ERR_INVALID_ARG, "pack: W_root is NULL");
+  Packed p = carve_packed(d, packed);
+  int64_t kp = kpad_of(d);
+  DS_CUDA(cudaMemsetAsync(p.ThT, 0, (size_t)d.d_out * kp * 2, s));
+  int64_t total = (int64_t)d.k * 16 + (int64_t)d.k * d.k + kp * d.d_out;
+  pack_bf16_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(
+      w.W1, w.W2, w.W3, w.b3, w.W_root, d.root == DSMPNN_ROOT_DENSE, d.k, d.d_e, d.d_in, d.d_out, kp, p);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
 }
+
+// ------------------------------------------------------------- fill kernel
+// one warp per row: bias row (mean of v_j), root operand copy, zero rows w/o edges
+template <int D>
+__global__ void s_fill_kernel(const __nv_bfloat16 *__restrict__ v, const int64_t *__restrict__ row_ptr,
+                              const int32_t *__restrict__ col, int64_t rb, int64_t re, int64_t kp,
+                              __nv_bfloat16 *__restrict__ S) {
+  const int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = rb + warp; i < re; i += nw) {
+    int64_t p0 = row_ptr[i], p1 = row_ptr[i + 1];
+    int deg = (int)(p1 - p0);
+    __nv_bfloat16 *Si = S + i * kp;
+    constexpr int PER = D / 32;  // columns per lane
+    float acc[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) acc[q] = 0.f;
+    for (int64_t p = p0; p < p1; ++p) {
+      const __nv_bfloat16 *vj = v + (int64_t)col[p] * D;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) acc[q] += __bfloat162float(vj[lane * PER + q]);
+    }
+    float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      Si[(int64_t)KH * D + lane * PER + q] = __float2bfloat16_rn(acc[q] * inv);
+      Si[(int64_t)(KH + 1) * D + lane * PER + q] = v[i * D + lane * PER + q];
+    }
+    for (int64_t t = (int64_t)(KH + 2) * D + lane; t < kp; t += 32) Si[t] = __float2bfloat16_rn(0.f);
+    if (deg == 0)
+      for (int64_t t = lane; t < (int64_t)KH * D; t += 32) Si[t] = __float2bfloat16_rn(0.f);
+  }
+}
+
+// ------------------------------------------------------------- edge kernel
+struct Seg {
+  int64_t node;
+  int32_t slot0, nslots;  // slots [slot0, slot0 + nslots), multiple of 16
+  int32_t deg;
+  int32_t start;          // 1: first segment of the node (no accumulation)
+  int32_t complete;       // 1: last segment of the node
+  int32_t tslot;          // TMEM S slot
+};
+constexpr int kMaxSeg = 8;
+
+template <int D>
+struct EF {
+  static constexpr int W2_BYTES = KH * KH * 2;          // 131072
+  static constexpr int AH_BYTES = 128 * KH * 2;         // 65536
+  static constexpr int V_BYTES = 128 * D * 2;           // 16384 / 8192
+  static constexpr int W1_BYTES = KH * 32;              // 8192
+  static constexpr int E_BYTES = 128 * 32;              // 4096
+  static constexpr int OFF_W2 = 0;
+  static constexpr int OFF_AH = OFF_W2 + W2_BYTES;
+  static constexpr int OFF_V = OFF_AH + AH_BYTES;
+  static constexpr int OFF_W1 = OFF_V + V_BYTES;
+  static constexpr int OFF_E = OFF_W1 + W1_BYTES;
+  static constexpr int OFF_MISC = OFF_E + E_BYTES;
+  static constexpr int SMEM = OFF_MISC + 1024 + 1024;   // misc + alignment slack
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr int NSLOT = (512 - KH) / (2 * D);    // TMEM S slots: 2 (D=64) or 4 (D=32)
+};
+
+struct EdgeMisc {
+  int32_t slot_edge[128];   // edge id per slot, -1 = padding
+  Seg seg[kMaxSeg];
+  int32_t nseg;
+  int32_t more;             // 1 if this tile has slots
+  int64_t cur_row;          // walker state
+  int32_t cur_off;
+  int32_t node_ctr;
+  int64_t row_end;
+  uint64_t bar;             // MMA completion barrier
+  uint32_t tmem;
+};
+
+// interleaved (no swizzle) K-major K=16 operand: row r, 16-byte chunk u
+__device__ __forceinline__ uint32_t il_off(uint32_t r, uint32_t u) { return (r >> 3) * 256u + u * 128u + (r & 7u) * 16u; }
+__device__ __forceinline__ uint32_t sw64_off(uint32_t r, uint32_t c) { return r * 64u + ((c ^ ((r >> 1) & 3u)) << 4); }
+
+template <int D>
+__device__ __forceinline__ uint32_t v_off(uint32_t s, uint32_t c) {
+  return D == 64 ? tc::sw128_off(s, c) : sw64_off(s, c);
+}
+
+// build the next tile: segments of whole 16-slot blocks, rows padded to 16
+__device__ void build_tile(EdgeMisc *m, const int64_t *__restrict__ row_ptr) {
+  int used = 0, ns = 0;
+  for (int s = 0; s < 128; ++s) m->slot_edge[s] = -1;
+  while (used < 128 && m->cur_row < m->row_end && ns < kMaxSeg) {
+    int64_t i = m->cur_row;
+    int64_t p0 = row_ptr[i];
+    int deg = (int)(row_ptr[i + 1] - p0);
+    if (deg == 0) {
+      m->cur_row++;
+      continue;
+    }
+    int padded = (deg + 15) & ~15;
+    int off = m->cur_off;
+    int take = padded - off;
+    if (take > 128 - used) take = 128 - used;
+    Seg &g = m->seg[ns++];
+    g.node = i;
+    g.slot0 = used;
+    g.nslots = take;
+    g.deg = deg;
+    g.start = off == 0;
+    if (off == 0) m->node_ctr++;
+    g.tslot = (m->node_ctr - 1) & 1;  // two TMEM S slots: the open row and the next one
+    for (int q = 0; q < take; ++q) {
+      int eidx = off + q;
+      m->slot_edge[used + q] = eidx < deg ? (int32_t)(p0 + eidx) : -1;
+    }
+    off += take;
+    used += take;
+    g.complete = off >= padded;
+    if (g.complete) {
+      m->cur_row++;
+      m->cur_off = 0;
+    } else {
+      m->cur_off = off;
+    }
+  }
+  m->nseg = ns;
+  m->more = used > 0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    edge_fwd_kernel(const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
+                    const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int64_t eb, int64_t ee,
+                    Packed pw, const float *__restrict__ b1, const float *__restrict__ b2,
+                    __nv_bfloat16 *__restrict__ S, int64_t kp, const int32_t *__restrict__ col) {
+  using C = EF<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sV = sm + C::OFF_V, *sW1 = sm + C::OFF_W1,
+          *sE = sm + C::OFF_E;
+  EdgeMisc *m = reinterpret_cast<EdgeMisc *>(sm + C::OFF_MISC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- setup: row range of this CTA (balanced by edges), weights -> SMEM, TMEM
+  if (tid == 0) {
+    int64_t E = ee - eb;
+    int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
+    int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
+    // first row whose edge range starts at or after t (lower bound on row_ptr over [rb, re])
+    auto lb = [&](int64_t t) {
+      int64_t lo = rb, hi = re;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] < t) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
+    m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
+    m->cur_off = 0;
+    m->node_ctr = 0;
+    tc::mbar_init(&m->bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&m->tmem);
+  {  // W2 (K-major SW128, 4 K-blocks of 64) and W1 (interleaved K=16)
+    const uint4 *g2 = reinterpret_cast<const uint4 *>(pw.W2);
+    for (int q = tid; q < KH * KH / 8; q += 256) {
+      int n = q / (KH / 8), rem = q % (KH / 8);
+      int j = rem / 8, c = rem % 8;
+      *reinterpret_cast<uint4 *>(sW2 + j * (KH * 128) + tc::sw128_off(n, c)) = g2[q];
+    }
+    const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
+    for (int q = tid; q < KH * 2; q += 256) {
+      int r = q / 2, u = q % 2;
+      *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
+    }
+  }
+  tc::fence_async_shared();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = m->tmem;
+  uint32_t phase = 0;  // completed commits on m->bar (uniform across threads)
+
+  const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aV = tc::smem_u32(sV), aW1 = tc::smem_u32(sW1),
+                 aE = tc::smem_u32(sE);
+  constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
+  constexpr uint32_t IDESC_S = tc::idesc_bf16(128, D, true, true);
+  const bool epi = warp >= 4;
+  const int erow = tid - 128;                                    // slot row of an epilogue thread
+  const uint32_t lane_base = epi ? ((uint32_t)(32 * (warp - 4)) << 16) : 0u;
+
+  auto wait_mma = [&]() {
+    tc::mbar_wait(&m->bar, phase & 1);
+    phase++;
+    tc::tc_fence_after();
+  };
+
+  for (;;) {
+    if (tid == 0) build_tile(m, row_ptr);
+    __syncthreads();
+    if (!m->more) break;
+
+    // ---- gather E (interleaved) and V (swizzled) rows of the 128 slots
+    {
+      int s = tid >> 1, u = tid & 1;
+      int p = m->slot_edge[s];
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (p >= 0) val = reinterpret_cast<const uint4 *>(e16 + (int64_t)p * 16)[u];
+      *reinterpret_cast<uint4 *>(sE + il_off(s, u)) = val;
+      constexpr int CH = D / 8;  // 16-byte chunks per v row
+#pragma unroll
+      for (int q = tid; q < 128 * CH; q += 256) {
+        int sl = q / CH, c = q % CH;
+        int pe = m->slot_edge[sl];
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (pe >= 0) x = reinterpret_cast<const uint4 *>(v + (int64_t)col[pe] * D)[c];
+        *reinterpret_cast<uint4 *>(sV + v_off<D>(sl, c)) = x;
+      }
+    }
+    tc::fence_async_shared();
+    tc::tc_fence_before();
+    __syncthreads();
+
+    // ---- MMA1: z1 = E . W1^T  (M=128 slots, N=KH, K=16)
+    if (tid == 0) {
+      tc::tc_fence_after();
+      tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC_MLP,
+                      0u);
+      tc::mma_commit(&m->bar);
+    }
+    wait_mma();
+    // ---- epilogue 1: a1 = relu(z1 + b1) -> AH (K-major SW128)
+    if (epi) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < KH; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(tmem + lane_base + c0, r);
+        tc::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b1 + c0 + 2 * j), 0.f),
+                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b1 + c0 + 2 * j + 1), 0.f));
+        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
+        int ch = (c0 % 64) / 8;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+    tc::fence_async_shared();
+    tc::tc_fence_before();
+    __syncthreads();
+
+    // ---- MMA2: z2 = a1 . W2^T  (M=128, N=KH, K=KH)
+    if (tid == 0) {
+      tc::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < KH / 16; ++kk) {
+        uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
+        uint64_t bd = tc::sdesc(aW2 + (kk / 4) * (KH * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
+        tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, kk > 0 ? 1u : 0u);
+      }
+      tc::mma_commit(&m->bar);
+    }
+    wait_mma();
+    // ---- epilogue 2: h = relu(z2 + b2) -> AH
+    if (epi) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < KH; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(tmem + lane_base + c0, r);
+        tc::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b2 + c0 + 2 * j), 0.f),
+                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b2 + c0 + 2 * j + 1), 0.f));
+        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
+        int ch = (c0 % 64) / 8;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+    tc::fence_async_shared();
+    tc::tc_fence_before();
+    __syncthreads();
+
+    // ---- per row segment: S_i += H_seg^T V_seg (two kappa halves), then write S~_i
+    const int nseg = m->nseg;
+    for (int g = 0; g < nseg; ++g) {
+      const Seg sg = m->seg[g];
+      const uint32_t ts = (uint32_t)(KH + sg.tslot * 2 * D);
+      if (tid == 0) {
+        tc::tc_fence_after();
+        for (int h = 0; h < 2; ++h) {
+          for (int q = 0; q < sg.nslots / 16; ++q) {
+            int s = sg.slot0 + 16 * q;
+            uint64_t ad = tc::sdesc(aAH + (2 * h) * (128 * 128) + (s / 8) * 1024, 128 * 128, 1024, tc::kSw128);
+            uint64_t bd = D == 64 ? tc::sdesc(aV + (s / 8) * 1024, 8192, 1024, tc::kSw128)
+                                  : tc::sdesc(aV + (s / 8) * 512, 4096, 512, tc::kSw64);
+            tc::mma_bf16_ss(tmem + ts + h * D, ad, bd, IDESC_S, (sg.start && q == 0) ? 0u : 1u);
+          }
+        }
+        tc::mma_commit(&m->bar);
+      }
+      wait_mma();
+      if (epi && sg.complete) {
+        const float inv = 1.0f / (float)sg.deg;
+        __nv_bfloat16 *Si = S + sg.node * kp;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kap = 128 * h + erow;
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t r[16];
+            tc::tmem_ld16(tmem + lane_base + ts + h * D + c0, r);
+            tc::tmem_ld_wait();
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              pk[j] = tc::pack_bf16(__uint_as_float(r[2 * j]) * inv, __uint_as_float(r[2 * j + 1]) * inv);
+            uint4 *dst = reinterpret_cast<uint4 *>(Si + (int64_t)kap * D + c0);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncthreads();
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// ------------------------------------------------------- node epilogue
+// pre = sum_z partial[z] + b (+ v_i for IDENTITY); out = sigma(pre)
+__global__ void node_epi_bf16_kernel(const float *__restrict__ part, int splits, int64_t split_stride, int64_t rb,
+                                     int64_t re, int D, const float *__restrict__ b,
+                                     const __nv_bfloat16 *__restrict__ v, int root, int act, float *__restrict__ pre,
+                                     float *__restrict__ out, __nv_bfloat16 *__restrict__ out_lowp) {
+  int64_t total = (re - rb) * D;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    float x = 0.f;
+    for (int z = 0; z < splits; ++z) x += part[z * split_stride + t];
+    int64_t idx = rb * D + t;
+    int o = (int)(t % D);
+    x += b[o];
+    if (root == DSMPNN_ROOT_IDENTITY) x += __bfloat162float(v[idx]);
+    pre[idx] = x;
+    float y = act == DSMPNN_ACT_RELU ? fmaxf(x, 0.f) : x;
+    out[idx] = y;
+    if (out_lowp) out_lowp[idx] = __float2bfloat16_rn(y);
+  }
+}
+
+// ------------------------------------------------------------ workspace
+struct BFwd {
+  __nv_bfloat16 *S;  // [n_dst x kp]
+  float *pre;        // [n_dst x D]
+  float *part;       // [kSplitsFwd x n_dst x D]
+};
+constexpr int kSplitsFwd = 6;
+static BFwd carve_bf16_fwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst) {
+  BFwd f;
+  f.S = c.take<__nv_bfloat16>(n_dst * kpad_of(d));
+  f.pre = c.take<float>(n_dst * d.d_out);
+  f.part = c.take<float>((int64_t)kSplitsFwd * n_dst * d.d_out);
+  return f;
+}
+
+size_t bf16_fwd_ws_bytes(const dsmpnn_layer_desc &d, int64_t n_dst, int64_t E) {
+  Carver c(nullptr, 0);
+  carve_bf16_fwd(c, d, n_dst);
+  return c.used();
+}
+
+template <int D>
+static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16 *v, const int64_t *row_ptr,
+                                     const int32_t *col, int64_t rb, int64_t re, int64_t eb, int64_t ee,
+                                     const Packed &pw, const float *b1, const float *b2, __nv_bfloat16 *S,
+                                     int64_t kp, cudaStream_t s) {
+  using C = EF<D>;
+  auto kern = edge_fwd_kernel<D>;
+  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  int64_t tiles = (ee - eb + 127) / 128 + 1;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
+  ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_FWD, s);
+  kern<<<grid, 256, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, const __nv_bfloat16 *v,
+                       const __nv_bfloat16 *e, const int64_t *row_ptr, const int32_t *col, int64_t n_dst, int64_t E,
+                       int64_t rb, int64_t re, int64_t eb, int64_t ee, float *out, __nv_bfloat16 *out_lowp, void *ws,
+                       size_t ws_bytes, cudaStream_t s) {
+  Carver c(ws, ws_bytes);
+  BFwd f = carve_bf16_fwd(c, d, n_dst);
+  DS_CHECK_ARG(c.ok(), DSMPNN_ERR_CAPACITY, "layer_fwd: workspace too small");
+  Packed pw = carve_packed(d, const_cast<void *>(w.packed));
+  const int D = d.d_in;
+  const int64_t kp = kpad_of(d);
+  const int64_t nR = re - rb;
+  // 1. bias row, root operand, isolated rows
+  {
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * 32, 256), 148 * 8));
+    if (D == 64) s_fill_kernel<64><<<blocks, 256, 0, s>>>(v, row_ptr, col, rb, re, kp, f.S);
+    else s_fill_kernel<32><<<blocks, 256, 0, s>>>(v, row_ptr, col, rb, re, kp, f.S);
+    DS_LAUNCH_CHECK();
+  }
+  // 2. fused kappa MLP + S formation
+  if (ee > eb) {
+    if (D == 64) DS_TRY(launch_edge_fwd<64>(e, v, row_ptr, col, rb, re, eb, ee, pw, w.b1, w.b2, f.S, kp, s));
+    else DS_TRY(launch_edge_fwd<32>(e, v, row_ptr, col, rb, re, eb, ee, pw, w.b1, w.b2, f.S, kp, s));
+  }
+  // 3. node GEMM [S~_aug] . [Theta~_aug]  (split-K partials)
+  {
+    ProbeScope probe(DSMPNN_PROBE_BF16_NODE_GEMM, s);
+    TgemmArgs a{nR, D, kp, f.S + rb * kp, kp, false, pw.ThT, kp, false, f.part, D, kSplitsFwd, nR * D, 0};
+    DS_TRY(tgemm(a, s));
+  }
+  int64_t nkb = (kp + 63) / 64;
+  int kbps = (int)ceil_div(nkb, kSplitsFwd);
+  int real = (int)ceil_div(nkb, kbps);
+  node_epi_bf16_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * D, 256), 148 * 8)), 256, 0, s>>>(
+      f.part, real, nR * D, rb, re, D, w.b, v, d.root, d.act, f.pre, out, out_lowp);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+size_t bf16_bwd_ws_bytes(const dsmpnn_layer_desc &, int64_t, int64_t, int64_t) { return 256; }
+
 dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &, const dsmpnn_weights &, const __nv_bfloat16 *,
                        const __nv_bfloat16 *, const int64_t *, const int32_t *, const int32_t *, const int64_t *,
                        int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, const float *, float *, float *,
                        const dsmpnn_grads &, const void *, void *, size_t, cudaStream_t) {
+  set_error("layer_bwd: BF16 backward not built yet");
   return DSMPNN_ERR_UNSUPPORTED;
 }
 

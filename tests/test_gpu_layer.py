@@ -192,3 +192,41 @@ def _darcy_full(L, dtype, n_rows):
 
 def test_f32_darcy_full_size_sampled(L):
     _darcy_full(L, 0, 24)
+
+
+@pytest.mark.parametrize("d,dim,mode,root,act", [(64, 2, "diff", 2, 1), (32, 3, "concat", 2, 1),
+                                                  (64, 2, "diff", 1, 0), (32, 2, "diff", 0, 1)])
+def test_fwd_bf16(L, d, dim, mode, root, act):
+    # tiles with several rows each, rows straddling tiles (deg 24..40 -> 32..48 slots), isolated rows,
+    # n_dst < n_loc; compared with the fp64 oracle on bf16-rounded inputs
+    p = _problem(900, dim, 0.09 if dim == 2 else 0.2, 40, mode, d, 256, seed=21 + d, n_dst=850, isolated=3)
+    got = _run_gpu(L, p, 1, root, act, want_bwd=False)
+    v, e, W = _to_dtype_inputs(p, 1)
+    desc = LayerDesc(p["d_e"], d, d, 256, root, act)
+    ref, _ = layer.layer_fwd(desc, W, v, e, p["rp"], p["col"])
+    assert np.isfinite(got["out"]).all()
+    assert nerr(got["out"], ref) <= TOL[1]
+
+
+def test_fwd_bf16_darcy_full_size_sampled(L):
+    cfg = synth.CONFIGS["darcy"]
+    coords, attr = synth.points(cfg)
+    ids = sample.sample(len(coords), cfg.s, synth.BASE_SEED + synth.SEED_SAMPLING)
+    x, a = coords[ids], attr[ids]
+    gid = ids.astype(np.int64)
+    n, n_dst = len(x), 4096
+    order = np.lexsort((gid, np.maximum(x[:, 0], x[:, 1])))
+    x, a, gid = x[order], a[order], gid[order]
+    adj = graph.radius_graph_rows(x, gid, range(n_dst), cfg.r, cfg.n_e, synth.BASE_SEED + synth.SEED_CAPPING)
+    rp = np.zeros(n_dst + 1, np.int64)
+    rp[1:] = np.cumsum([len(r_) for r_ in adj])
+    col = np.concatenate(adj).astype(np.int32)
+    e = features.edge_features("diff", x, a, features.dst_of_edges(rp), col)
+    W = synth.weights(e.shape[1], cfg.d, cfg.d, cfg.k)
+    p = dict(x=x, a=a, gid=gid, rp=rp, col=col, e=e, W=W, v=synth.node_features(n, cfg.d), G=None, n_dst=n_dst,
+             n=n, d_e=e.shape[1], d=cfg.d, k=cfg.k)
+    got = _run_gpu(L, p, 1, 2, 1, want_bwd=False)
+    rows = hash_rows(n_dst, 64)
+    v, e16, W16 = _to_dtype_inputs(p, 1)
+    ref, _ = layer.layer_fwd(LayerDesc(3, cfg.d, cfg.d, cfg.k, 2, 1), W16, v, e16, rp, col, rows=rows)
+    assert nerr(got["out"][rows], ref) <= TOL[1]

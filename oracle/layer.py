@@ -24,6 +24,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .precision import round_bf16
+
 ROOT_NONE, ROOT_IDENTITY, ROOT_DENSE = 0, 1, 2
 ACT_IDENTITY, ACT_RELU = 0, 1
 
@@ -36,19 +38,23 @@ class LayerDesc:
     k: int
     root: int = ROOT_DENSE
     act: int = ACT_RELU
+    act_round: str = "none"   # "bf16": BF16-mode operand rounding of a1, h (oracle/precision.py)
 
 
 def _w(W, name):
     return np.asarray(W[name], dtype=np.float64)
 
 
-def kappa(W, e):
-    """kappa_phi on a batch of edge attributes (R5).  Returns (a1, h, Kflat)."""
+def kappa(W, e, act_round="none"):
+    """kappa_phi on a batch of edge attributes (R5).  Returns (a1, h, Kflat).
+    act_round="bf16" rounds the activations a1, h to bf16 (BF16-mode operand
+    precision, reading R18)."""
+    rnd = round_bf16 if act_round == "bf16" else (lambda x: x)
     e = np.asarray(e, dtype=np.float64)
     z1 = e @ _w(W, "W1").T + _w(W, "b1")
-    a1 = np.maximum(z1, 0.0)
+    a1 = rnd(np.maximum(z1, 0.0))
     z2 = a1 @ _w(W, "W2").T + _w(W, "b2")
-    h = np.maximum(z2, 0.0)
+    h = rnd(np.maximum(z2, 0.0))
     Kflat = h @ _w(W, "W3").T + _w(W, "b3")
     return a1, h, Kflat
 
@@ -63,7 +69,7 @@ def _edge_chunks(p0, p1, chunk):
 
 def messages(desc, W, v, e, col_idx, p0, p1):
     """m_p = K_p^T v_j for edges p in [p0, p1), K_p materialised (R4)."""
-    _, _, Kflat = kappa(W, e[p0:p1])
+    _, _, Kflat = kappa(W, e[p0:p1], desc.act_round)
     K = Kflat.reshape(p1 - p0, desc.d_in, desc.d_out)          # K[p, c, o]
     vj = np.asarray(v, dtype=np.float64)[col_idx[p0:p1]]
     return np.einsum("pc,pco->po", vj, K)
@@ -148,7 +154,7 @@ def layer_bwd(desc, W, v, e, row_ptr, col_idx, G, rows=None, want_de=True):
         if deg == 0:
             continue
         dm = ghat[t] / deg                                   # d loss / d m_p
-        a1, h, Kflat = kappa(W, e64[p0:p1])
+        a1, h, Kflat = kappa(W, e64[p0:p1], desc.act_round)
         K = Kflat.reshape(deg, desc.d_in, desc.d_out)
         for q in range(deg):
             p = p0 + q
@@ -186,7 +192,7 @@ def pack_theta(desc, W):
 
 def messages_contraction(desc, W, v, e, col_idx, p0, p1):
     """m_p = vec(h~_p (x) v_j) . Theta~  (K_p never formed)."""
-    _, h, _ = kappa(W, e[p0:p1])
+    _, h, _ = kappa(W, e[p0:p1], desc.act_round)
     ht = np.concatenate([h, np.ones((p1 - p0, 1))], axis=1)
     vj = np.asarray(v, dtype=np.float64)[np.asarray(col_idx)[p0:p1]]
     Z = np.einsum("pk,pc->pkc", ht, vj).reshape(p1 - p0, -1)

@@ -72,8 +72,10 @@ struct TG {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(128, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int64_t M, int64_t N,
-                 int64_t K, int kb_per_split, float *__restrict__ C, int64_t ldc, int64_t split_stride,
-                 int accumulate, int splits) {
+                 int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
+  float *__restrict__ C = ep.C;
+  const int64_t ldc = ep.ldc, split_stride = ep.split_stride;
+  const int accumulate = ep.accumulate;
   using T = TG<BN, A_MN, B_MN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -166,19 +168,62 @@ __global__ void __launch_bounds__(128, 1)
 
   // epilogue: thread <-> row m0 + 32*warp + lane
   const int64_t row = m0 + warp * 32 + lane;
-  float *out = C + (splits > 1 ? (int64_t)blockIdx.z * split_stride : 0);
+  if (ep.out16 == nullptr) {
+    float *out = C + (splits > 1 ? (int64_t)blockIdx.z * split_stride : 0);
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    uint32_t v[16];
-    tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-    tc::tmem_ld_wait();
-    if (row < M) {
-      float *dst = out + row * ldc + n0 + c0;
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      tc::tmem_ld_wait();
+      if (row < M) {
+        float *dst = out + row * ldc + n0 + c0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (n0 + c0 + j < N) {
-          float x = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-          dst[j] = (accumulate && splits == 1) ? dst[j] + x : x;
+        for (int j = 0; j < 16; ++j) {
+          if (n0 + c0 + j < N) {
+            float x = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+            dst[j] = (accumulate && splits == 1) ? dst[j] + x : x;
+          }
+        }
+      }
+    }
+  } else {
+    const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      tc::tmem_ld_wait();
+      float x[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
+      if (ep.mask16 && row < M) {
+        const __nv_bfloat16 *mk = ep.mask16 + row * ep.ldmask + n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
+      }
+      __nv_bfloat16 xb[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) xb[j] = __float2bfloat16_rn(x[j]);
+      if (row < M) {
+        __nv_bfloat16 *dst = ep.out16 + row * ep.ld16 + n0 + c0;
+        if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          reinterpret_cast<uint4 *>(dst)[0] = *reinterpret_cast<uint4 *>(&xb[0]);
+          reinterpret_cast<uint4 *>(dst)[1] = *reinterpret_cast<uint4 *>(&xb[8]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + c0 + j < N) dst[j] = xb[j];
+        }
+      }
+      if (ep.colsum_part) {
+        // sum of the written (bf16-rounded) values over this warp's 32 rows
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float y = row < M ? __bfloat162float(xb[j]) : 0.f;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+          if (lane == 0 && n0 + c0 + j < N) ep.colsum_part[((int64_t)blockIdx.y * 4 + warp) * N + n0 + c0 + j] = y;
         }
       }
     }
@@ -204,7 +249,7 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (kbps < 1) kbps = 1;
   splits = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
   dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.M, T::BM), (unsigned)splits);
-  kern<<<grid, 128, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a.C, a.ldc, a.split_stride, a.accumulate, splits);
+  kern<<<grid, 128, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a, splits);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -220,6 +265,7 @@ static dsmpnn_status dispatch_bn(const TgemmArgs &a, cudaStream_t s) {
 
 dsmpnn_status tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return DSMPNN_OK;
+  DS_CHECK_ARG(a.out16 == nullptr || a.splits <= 1, DSMPNN_ERR_INVALID_ARG, "tgemm: bf16 epilogue needs splits == 1");
   DS_CHECK_ARG(!(a.N > 64 && a.N % 64 != 0 && a.b_mn_major), DSMPNN_ERR_UNSUPPORTED,
                "tgemm: N-major B with N > 64 needs N %% 64 == 0");
   if (!a.a_mn_major && !a.b_mn_major) return dispatch_bn<false, false>(a, s);

@@ -2,6 +2,8 @@
 // TMEM -> fp32 epilogue) used by the BF16 layer for its dense contractions.
 #pragma once
 #include "common.cuh"
+#include <cuda.h>
+#include <cuda_bf16.h>
 
 namespace dsmpnn {
 
@@ -22,7 +24,24 @@ struct TgemmArgs {
   int splits;        // split-K count; > 1 writes partial z at C + z * split_stride
   int64_t split_stride;
   int accumulate;    // 1: C += result (only when splits == 1)
+  // optional bf16 epilogue (splits == 1): if out16 != null the tile is written
+  // as bf16 to out16[m*ld16 + n] instead of C, after
+  //   x *= row_scale[m]             (row_scale != null)
+  //   x  = mask16[m*ldmask + n] > 0 ? x : 0   (mask16 != null)
+  // and per-warp column sums of the written values go to
+  //   colsum_part[(blockIdx.y*4 + warp) * N + n]   (colsum_part != null)
+  __nv_bfloat16 *out16 = nullptr;
+  int64_t ld16 = 0;
+  const float *row_scale = nullptr;
+  const __nv_bfloat16 *mask16 = nullptr;
+  int64_t ldmask = 0;
+  float *colsum_part = nullptr;
 };
+
+// 2-D bf16 TMA descriptor: `inner` contiguous elements, `outer` rows of `ld`
+// elements, box {box_inner, box_outer}; swizzle = box row bytes (32/64/128).
+dsmpnn_status make_tmap_bf16(CUtensorMap *m, const void *base, int64_t inner, int64_t outer, int64_t ld,
+                             int box_inner, int box_outer);
 
 // C = A * B (+ C).  N-tile = min(N rounded up to 16, 256) per CTA.
 dsmpnn_status tgemm(const TgemmArgs &a, cudaStream_t s);

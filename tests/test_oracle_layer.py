@@ -295,3 +295,29 @@ def test_zero_overlap_differs():
         idx = [pos[int(rw)] for rw in q["local_rows"][:n_own]]
         diff += int(np.sum(np.any(o != ref[idx], axis=1)))
     assert diff > 0
+
+
+def test_round_bf16_matches_torch():
+    # the oracle's own bf16 rounding == torch's CPU float32 -> bfloat16 conversion (library routine)
+    import torch
+    from oracle.precision import round_bf16
+    g = np.random.default_rng(0)
+    x = np.concatenate([g.normal(size=20000) * 10.0 ** g.integers(-30, 30, 20000),
+                        [0.0, -0.0, 1.0, 1.00390625, 1.01171875, 3.0e38, -1e-40]])
+    want = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(round_bf16(x), want)
+
+
+def test_act_round_only_changes_activations():
+    # with act_round="bf16" the layer equals the plain layer on bf16-valued activations:
+    # identical when the kappa activations are already bf16-representable (W2 = 0, b2 bf16)
+    desc, W, v, e, rp, ci = _rand_problem(15)
+    from oracle.precision import round_bf16
+    W["W1"] = np.zeros_like(W["W1"])
+    W["b1"] = round_bf16(W["b1"])
+    W["W2"] = np.zeros_like(W["W2"])
+    W["b2"] = round_bf16(W["b2"])
+    a = layer.layer_fwd(desc, W, v, e, rp, ci)[0]
+    desc.act_round = "bf16"
+    b = layer.layer_fwd(desc, W, v, e, rp, ci)[0]
+    assert np.array_equal(a, b)

@@ -59,15 +59,6 @@ __global__ void unpack_dtheta_aug_kernel(const float *__restrict__ dT, int k, in
   }
 }
 
-// out[n] (+)= sum_r part[r*N + n], fixed order
-__global__ void sum_rows_kernel(const float *__restrict__ part, int rows, int N, float *__restrict__ out) {
-  int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N || !out) return;
-  float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += part[(int64_t)r * N + n];
-  out[n] += s;
-}
-
 // dW1[r, c] += full[r, c] for c < d_e (full is [k x 16]); same for de rows
 __global__ void add_cols_kernel(const float *__restrict__ full, int64_t rows, int ld_full, int ncols,
                                 float *__restrict__ dst, int accumulate) {
@@ -544,8 +535,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   int grid = 1;
   if (D == 64) DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, &grid, s));
   else DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, &grid, s));
-  sum_rows_kernel<<<(k + 255) / 256, 256, 0, s>>>(b.db2_part, grid, k, gr.b2);
-  DS_LAUNCH_CHECK();
+  DS_TRY(colsum(b.db2_part, grid, k, k, gr.b2, 1, s));
   // B4: dW2 += dz2^T a1   (M = k, N = k, K = edges)
   if (gr.W2) {
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
@@ -566,8 +556,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     a.colsum_part = b.db1_part;
     DS_TRY(tgemm(a, s));
     int rows = (int)(ceil_div(nE, 128) * 4);
-    sum_rows_kernel<<<(k + 255) / 256, 256, 0, s>>>(b.db1_part, rows, k, gr.b1);
-    DS_LAUNCH_CHECK();
+    DS_TRY(colsum(b.db1_part, rows, k, k, gr.b1, 1, s));
   }
   // B6: dW1 += dz1^T e ;  de = dz1 W1
   if (gr.W1) {

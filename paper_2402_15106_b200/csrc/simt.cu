@@ -103,27 +103,27 @@ dsmpnn_status sgemm(const SgemmArgs &a, int splits, float *partial, cudaStream_t
   return DSMPNN_OK;
 }
 
-// one block per 32 columns; 8 row lanes per column, fixed reduction order
-__global__ void colsum_kernel(const float *__restrict__ A, int64_t M, int64_t N, int64_t lda, float *__restrict__ out,
-                              int accumulate) {
-  __shared__ float red[8][33];
+// one block per 32 columns; 32 row lanes per column, fixed reduction order
+__global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ A, int64_t M, int64_t N, int64_t lda,
+                                                      float *__restrict__ out, int accumulate) {
+  __shared__ float red[32][33];
   int c = threadIdx.x & 31, r = threadIdx.x >> 5;
   int64_t n = (int64_t)blockIdx.x * 32 + c;
   float s = 0.f;
   if (n < N)
-    for (int64_t m = r; m < M; m += 8) s += A[m * lda + n];
+    for (int64_t m = r; m < M; m += 32) s += A[m * lda + n];
   red[r][c] = s;
   __syncthreads();
   if (r == 0 && n < N) {
     float t = 0.f;
-    for (int k = 0; k < 8; ++k) t += red[k][c];
+    for (int k = 0; k < 32; ++k) t += red[k][c];
     out[n] = accumulate ? out[n] + t : t;
   }
 }
 
 dsmpnn_status colsum(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, cudaStream_t s) {
   if (N <= 0 || !out) return DSMPNN_OK;
-  colsum_kernel<<<(unsigned)ceil_div(N, 32), 256, 0, s>>>(A, M, N, lda, out, accumulate);
+  colsum_kernel<<<(unsigned)ceil_div(N, 32), 1024, 0, s>>>(A, M, N, lda, out, accumulate);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

@@ -198,9 +198,19 @@ __global__ void __launch_bounds__(128, 1)
       for (int j = 0; j < 16; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
       if (ep.mask16 && row < M) {
         const __nv_bfloat16 *mk = ep.mask16 + row * ep.ldmask + n0 + c0;
+        if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(mk) & 15) == 0)) {
+          uint4 mv[2];
+          mv[0] = reinterpret_cast<const uint4 *>(mk)[0];
+          mv[1] = reinterpret_cast<const uint4 *>(mk)[1];
+          const __nv_bfloat16 *mb = reinterpret_cast<const __nv_bfloat16 *>(mv);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
+          for (int j = 0; j < 16; ++j)
+            if (!(__bfloat162float(mb[j]) > 0.f)) x[j] = 0.f;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
+        }
       }
       __nv_bfloat16 xb[16];
 #pragma unroll
@@ -217,14 +227,19 @@ __global__ void __launch_bounds__(128, 1)
         }
       }
       if (ep.colsum_part) {
-        // sum of the written (bf16-rounded) values over this warp's 32 rows
+        // sum of the written (bf16-rounded) values over this warp's 32 rows:
+        // transpose through the (now idle) pipeline buffers, lane j sums column j
+        float *scr = reinterpret_cast<float *>(sA) + warp * (32 * 17);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float y = row < M ? __bfloat162float(xb[j]) : 0.f;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-          if (lane == 0 && n0 + c0 + j < N) ep.colsum_part[((int64_t)blockIdx.y * 4 + warp) * N + n0 + c0 + j] = y;
+        for (int j = 0; j < 16; ++j) scr[lane * 17 + j] = row < M ? __bfloat162float(xb[j]) : 0.f;
+        __syncwarp();
+        if (lane < 16) {
+          float y = 0.f;
+#pragma unroll 8
+          for (int q = 0; q < 32; ++q) y += scr[q * 17 + lane];
+          if (n0 + c0 + lane < N) ep.colsum_part[((int64_t)blockIdx.y * 4 + warp) * N + n0 + c0 + lane] = y;
         }
+        __syncwarp();
       }
     }
   }

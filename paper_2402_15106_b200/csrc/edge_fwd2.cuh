@@ -1,0 +1,393 @@
+// edge_fwd2.cuh - pipelined, warp-specialised fused edge kernel (forward):
+// kappa_phi MLP on tcgen05 + per-row S_i = H_i^T V_i, K_p never formed.
+//
+// Tiles hold whole rows (each padded to a multiple of 16 slots, at most NMAX
+// rows and 128 slots per tile).  Roles (12 warps):
+//   loader  (warps 0,2,3) : tile walker; cp.async gathers of e rows (double
+//                           buffered) and of v_{j(p)} rows (single buffer)
+//   MMA     (warp 1)      : MMA1 z1 = E W1^T (K=16); MMA2 z2 = a1 W2^T in two
+//                           N=128 halves, K-block j issued as soon as the
+//                           epilogue has written block j of a1; S MMAs per
+//                           row and kappa half as soon as h half is written
+//   EPI_A   (warps 4-7)   : a1 = relu(z1+b1), h = relu(z2+b2) TMEM -> SMEM
+//   EPI_B   (warps 8-11)  : S_i TMEM -> scaled bf16 -> S~_aug (global)
+// TMEM: two 256-column regions, tile t uses region t&1 for z1 (0..255), z2
+// (kappa half 0 at columns 128..255, half 1 at 0..127) and the S accumulators
+// (row g, kappa half h at the columns of z2 half h, offset g*D), so EPI_B of
+// tile t overlaps MMA1/MMA2 of tile t+1 and epi1 overlaps MMA2.
+#pragma once
+#include "layer_bf16_common.cuh"
+
+namespace dsmpnn {
+
+struct TileDesc2 {
+  int32_t slot_edge[128];
+  int64_t node[4];
+  int32_t slot0[4], deg[4];
+  int32_t nnodes, more;
+};
+
+struct Misc2 {
+  TileDesc2 desc[2];
+  uint64_t e_full[2], e_empty[2], d1_full[2], region_free[2], desc_free[2];
+  uint64_t v_full, v_empty, ah_free, s_full;
+  uint64_t a1_ready[4], d2_full[2], h_ready[2];
+  int64_t cur_row, row_end;
+  uint32_t tmem;
+};
+
+template <int D>
+struct EF2 {
+  static constexpr int NMAX = D == 64 ? 2 : 4;          // rows per tile (S accumulators per region half)
+  static constexpr int W2_BYTES = KH * KH * 2;          // 131072
+  static constexpr int AH_BYTES = 128 * KH * 2;         // 65536
+  static constexpr int V_BYTES = 128 * D * 2;           // 16384 / 8192
+  static constexpr int W1_BYTES = KH * 32;              // 8192
+  static constexpr int E_BYTES = 128 * 32;              // 4096
+  static constexpr int OFF_W2 = 0;
+  static constexpr int OFF_AH = OFF_W2 + W2_BYTES;
+  static constexpr int OFF_V = OFF_AH + AH_BYTES;
+  static constexpr int OFF_W1 = OFF_V + V_BYTES;
+  static constexpr int OFF_E = OFF_W1 + W1_BYTES;       // 2 buffers
+  static constexpr int OFF_MISC = OFF_E + 2 * E_BYTES;
+  static constexpr int SMEM = OFF_MISC + (int)sizeof(Misc2) + 1024;
+  static constexpr uint32_t ROWB = D * 2;
+};
+
+// walker: next tile of whole rows (thread 0 of the loader group)
+template <int NMAX>
+__device__ __forceinline__ void walk_tile(Misc2 *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr) {
+  int used = 0, nn = 0;
+  while (m->cur_row < m->row_end && nn < NMAX) {
+    int64_t i = m->cur_row;
+    int64_t p0 = row_ptr[i];
+    int deg = (int)(row_ptr[i + 1] - p0);
+    if (deg == 0) { m->cur_row++; continue; }
+    int padded = (deg + 15) & ~15;
+    if (padded > 128) __trap();  // rows longer than 128 edges are rejected on the host
+    if (used + padded > 128) break;
+    d->node[nn] = i;
+    d->slot0[nn] = used;
+    d->deg[nn] = deg;
+    used += padded;
+    nn++;
+    m->cur_row++;
+  }
+  d->nnodes = nn;
+  d->more = nn > 0;
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    edge_fwd2_kernel(const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
+                     const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int64_t eb, int64_t ee, Packed pw,
+                     const float *__restrict__ b1, const float *__restrict__ b2, __nv_bfloat16 *__restrict__ S,
+                     int64_t kp, const int32_t *__restrict__ col) {
+  using C = EF2<D>;
+  constexpr int NMAX = C::NMAX;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sV = sm + C::OFF_V, *sW1 = sm + C::OFF_W1,
+          *sE = sm + C::OFF_E;
+  Misc2 *m = reinterpret_cast<Misc2 *>(sm + C::OFF_MISC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---------------------------------------------------------------- setup
+  if (tid == 0) {
+    int64_t E = ee - eb;
+    int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
+    int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
+    auto lb = [&](int64_t t) {
+      int64_t lo = rb, hi = re;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] < t) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
+    m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&m->e_full[b], 96);
+      tc::mbar_init(&m->e_empty[b], 1);
+      tc::mbar_init(&m->d1_full[b], 1);
+      tc::mbar_init(&m->region_free[b], 4);
+      tc::mbar_init(&m->desc_free[b], 3);
+      tc::mbar_init(&m->d2_full[b], 1);
+      tc::mbar_init(&m->h_ready[b], 128);
+    }
+    tc::mbar_init(&m->v_full, 96);
+    tc::mbar_init(&m->v_empty, 1);
+    tc::mbar_init(&m->ah_free, 1);
+    tc::mbar_init(&m->s_full, 1);
+    for (int j = 0; j < 4; ++j) tc::mbar_init(&m->a1_ready[j], 128);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&m->tmem);
+  {  // W2 (K-major SW128, 4 K-blocks of 64) and W1 (interleaved K=16), resident
+    const uint4 *g2 = reinterpret_cast<const uint4 *>(pw.W2);
+    for (int q = tid; q < KH * KH / 8; q += 384) {
+      int n = q / (KH / 8), rem = q % (KH / 8);
+      int j = rem / 8, c = rem % 8;
+      *reinterpret_cast<uint4 *>(sW2 + j * (KH * 128) + tc::sw128_off(n, c)) = g2[q];
+    }
+    const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
+    for (int q = tid; q < KH * 2; q += 384) {
+      int r = q / 2, u = q % 2;
+      *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
+    }
+  }
+  tc::fence_async_shared();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = m->tmem;
+
+  if (warp == 0 || warp == 2 || warp == 3) {
+    // ============================================================ loader
+    const int li = warp == 0 ? lane : (warp - 1) * 32 + lane;  // 0..95
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      TileDesc2 *dsc = &m->desc[b];
+      if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
+      if (li == 0) walk_tile<NMAX>(m, dsc, row_ptr);
+      tc::named_sync(1, 96);
+      const int nn = dsc->nnodes;
+      for (int s = li; s < 128; s += 96) {
+        int32_t pe = -1;
+        for (int g = 0; g < nn; ++g) {
+          int o = s - dsc->slot0[g];
+          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(row_ptr[dsc->node[g]] + o);
+        }
+        dsc->slot_edge[s] = pe;
+      }
+      tc::named_sync(1, 96);
+      if (!dsc->more) {
+        tc::mbar_arrive(&m->e_full[b]);
+        break;
+      }
+      if (t >= 2) tc::mbar_wait(&m->e_empty[b], ((t >> 1) - 1) & 1);
+      uint8_t *eb_s = sE + b * C::E_BYTES;
+      for (int q = li; q < 256; q += 96) {
+        int s = q >> 1, u = q & 1;
+        int pe = dsc->slot_edge[s];
+        tc::cp_async16(eb_s + il_off(s, u), e16 + (int64_t)(pe < 0 ? 0 : pe) * 16 + u * 8, pe < 0 ? 0u : 16u);
+      }
+      tc::cp_async_wait_all();
+      tc::fence_async_shared();
+      tc::mbar_arrive(&m->e_full[b]);
+      if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
+      constexpr int CH = D / 8;
+      for (int q = li; q < 128 * CH; q += 96) {
+        int s = q / CH, c = q % CH;
+        int pe = dsc->slot_edge[s];
+        const __nv_bfloat16 *src = v + (int64_t)(pe < 0 ? 0 : col[pe]) * D + c * 8;
+        tc::cp_async16(sV + v_off<D>(s, c), src, pe < 0 ? 0u : 16u);
+      }
+      tc::cp_async_wait_all();
+      tc::fence_async_shared();
+      tc::mbar_arrive(&m->v_full);
+    }
+  } else if (warp == 1) {
+    // =============================================================== MMA
+    if (lane == 0) {
+      const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aV = tc::smem_u32(sV),
+                     aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
+      constexpr uint32_t IDESC1 = tc::idesc_bf16(128, KH, false, false);
+      constexpr uint32_t IDESC2 = tc::idesc_bf16(128, 128, false, false);
+      constexpr uint32_t IDESC_S = tc::idesc_bf16(128, D, true, true);
+      for (uint32_t t = 0;; ++t) {
+        const int b = t & 1;
+        const uint32_t ph = (t >> 1) & 1, p1 = t & 1;
+        const TileDesc2 *dsc = &m->desc[b];
+        tc::mbar_wait(&m->e_full[b], ph);
+        if (!dsc->more) break;
+        if (t >= 2) tc::mbar_wait(&m->region_free[b], ((t >> 1) - 1) & 1);
+        tc::tc_fence_after();
+        const uint32_t r = tmem + b * 256;
+        // MMA1: z1 = E W1^T (one K=16 step)
+        tc::mma_bf16_ss(r, tc::sdesc(aE + b * C::E_BYTES, 128, 256, tc::kSwNone),
+                        tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC1, 0u);
+        tc::mma_commit(&m->d1_full[b]);
+        tc::mma_commit(&m->e_empty[b]);
+        // MMA2: z2 = a1 W2^T in two N halves.  Half 0 (kappa 0..127) goes to
+        // columns 128..255, whose z1 the epilogue drains first (a1 blocks 2, 3),
+        // and consumes a1 K-blocks in the order they arrive (2, 3, 0, 1); half 1
+        // (kappa 128..255) goes to columns 0..127 once all of z1 is drained.
+        for (int nh = 0; nh < 2; ++nh) {
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = (jj + 2) & 3;
+            // the first MMA writes all 128 accumulator columns: z1 columns
+            // 128..255 (a1 blocks 2 and 3) must both be drained first
+            if (jj == 0) tc::mbar_wait(&m->a1_ready[3], p1);
+            tc::mbar_wait(&m->a1_ready[j], p1);
+            tc::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = tc::sdesc(aAH + j * (128 * 128) + kk * 32, 16, 1024, tc::kSw128);
+              uint64_t bd = tc::sdesc(aW2 + j * (KH * 128) + nh * (128 * 128) + kk * 32, 16, 1024, tc::kSw128);
+              tc::mma_bf16_ss(r + (nh == 0 ? 128 : 0), ad, bd, IDESC2, (jj > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          tc::mma_commit(&m->d2_full[nh]);
+        }
+        // S_i = H_i^T V_i per row, kappa half h at column h*128 + g*D
+        tc::mbar_wait(&m->v_full, p1);
+        const int nn = dsc->nnodes;
+        for (int h = 0; h < 2; ++h) {
+          tc::mbar_wait(&m->h_ready[h], p1);
+          tc::tc_fence_after();
+          for (int g = 0; g < nn; ++g) {
+            const int s0 = dsc->slot0[g], nk = (dsc->deg[g] + 15) >> 4;
+            for (int q = 0; q < nk; ++q) {
+              int s = s0 + 16 * q;
+              uint64_t ad = tc::sdesc(aAH + (2 * h) * (128 * 128) + (s / 8) * 1024, 128 * 128, 1024, tc::kSw128);
+              uint64_t bd = D == 64 ? tc::sdesc(aV + (s / 8) * 1024, 8192, 1024, tc::kSw128)
+                                    : tc::sdesc(aV + (s / 8) * 512, 4096, 512, tc::kSw64);
+              tc::mma_bf16_ss(r + (h == 0 ? 128 : 0) + g * D, ad, bd, IDESC_S, q > 0 ? 1u : 0u);
+            }
+          }
+        }
+        tc::mma_commit(&m->s_full);
+        tc::mma_commit(&m->v_empty);
+        tc::mma_commit(&m->ah_free);
+        tc::mbar_arrive(&m->desc_free[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 8) {
+    // ============================================================= EPI_A
+    const int grp = warp & 3;
+    const int erow = grp * 32 + lane;  // slot row == TMEM lane
+    const uint32_t lane_off = (uint32_t)(grp * 32) << 16;
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      const uint32_t ph = (t >> 1) & 1, p1 = t & 1;
+      tc::mbar_wait(&m->e_full[b], ph);
+      if (!m->desc[b].more) break;
+      const uint32_t r = tmem + b * 256 + lane_off;
+      tc::mbar_wait(&m->d1_full[b], ph);
+      if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
+      tc::tc_fence_after();
+      // a1 = relu(z1 + b1) -> AH, block by block (MMA2 starts on block j at once)
+#pragma unroll 1
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = (jj + 2) & 3;  // columns 128..255 first (see MMA2)
+        uint8_t *blk = sAH + j * (128 * 128);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c0 = j * 64 + cc * 16;
+          uint32_t x[16];
+          tc::tmem_ld16(r + c0, x);
+          tc::tmem_ld_wait();
+          uint32_t pk[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b1 + c0 + 2 * q), 0.f),
+                                  fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b1 + c0 + 2 * q + 1), 0.f));
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        tc::fence_async_shared();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&m->a1_ready[j]);
+      }
+      // h = relu(z2 + b2): half 0 read while MMA2 half 1 runs, stored once MMA2 is done
+      tc::mbar_wait(&m->d2_full[0], p1);
+      tc::tc_fence_after();
+      uint32_t hp[64];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c0 = cc * 16;
+        uint32_t x[16];
+        tc::tmem_ld16(r + 128 + c0, x);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          hp[cc * 8 + q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b2 + c0 + 2 * q), 0.f),
+                                         fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b2 + c0 + 2 * q + 1), 0.f));
+      }
+      tc::mbar_wait(&m->d2_full[1], p1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        uint8_t *blk = sAH + (cc / 4) * (128 * 128);
+        const int ch = (cc % 4) * 2;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) =
+            make_uint4(hp[cc * 8 + 0], hp[cc * 8 + 1], hp[cc * 8 + 2], hp[cc * 8 + 3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) =
+            make_uint4(hp[cc * 8 + 4], hp[cc * 8 + 5], hp[cc * 8 + 6], hp[cc * 8 + 7]);
+      }
+      tc::fence_async_shared();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->h_ready[0]);
+#pragma unroll 1
+      for (int cc = 8; cc < 16; ++cc) {
+        const int c0 = cc * 16;
+        uint32_t x[16];
+        tc::tmem_ld16(r + c0 - 128, x);
+        tc::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b2 + c0 + 2 * q), 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b2 + c0 + 2 * q + 1), 0.f));
+        uint8_t *blk = sAH + (cc / 4) * (128 * 128);
+        const int ch = (cc % 4) * 2;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tc::fence_async_shared();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->h_ready[1]);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (warp == 4 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+    }
+  } else {
+    // ============================================================= EPI_B
+    const int grp = warp & 3;
+    const uint32_t lane_off = (uint32_t)(grp * 32) << 16;
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      const uint32_t ph = (t >> 1) & 1, p1 = t & 1;
+      const TileDesc2 *dsc = &m->desc[b];
+      tc::mbar_wait(&m->e_full[b], ph);
+      if (!dsc->more) break;
+      tc::mbar_wait(&m->s_full, p1);
+      tc::tc_fence_after();
+      const uint32_t r = tmem + b * 256 + lane_off;
+      const int nn = dsc->nnodes;
+      for (int g = 0; g < nn; ++g) {
+        const float inv = 1.0f / (float)dsc->deg[g];
+        __nv_bfloat16 *Si = S + dsc->node[g] * kp;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kap = 128 * h + grp * 32 + lane;
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t x[16];
+            tc::tmem_ld16(r + (h == 0 ? 128 : 0) + g * D + c0, x);
+            tc::tmem_ld_wait();
+            uint32_t pk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              pk[q] = tc::pack_bf16(__uint_as_float(x[2 * q]) * inv, __uint_as_float(x[2 * q + 1]) * inv);
+            uint4 *dst = reinterpret_cast<uint4 *>(Si + (int64_t)kap * D + c0);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->region_free[b]);
+      if (warp == 8 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace dsmpnn

@@ -20,6 +20,7 @@
 
 #include "layer_bf16.cuh"
 #include "layer_bf16_common.cuh"
+#include "edge_fwd2.cuh"
 #include "simt.cuh"
 #include "tc.cuh"
 #include "tgemm.cuh"
@@ -374,13 +375,13 @@ static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16
                                      const int32_t *col, int64_t rb, int64_t re, int64_t eb, int64_t ee,
                                      const Packed &pw, const float *b1, const float *b2, __nv_bfloat16 *S,
                                      int64_t kp, cudaStream_t s) {
-  using C = EF<D>;
-  auto kern = edge_fwd_kernel<D>;
+  using C = EF2<D>;
+  auto kern = edge_fwd2_kernel<D>;
   DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_FWD, s);
-  kern<<<grid, 256, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  kern<<<grid, 384, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

@@ -60,45 +60,52 @@ dsmpnn_status make_tmap_bf16(CUtensorMap *m, const void *base, int64_t inner, in
 
 template <int BN, bool A_MN, bool B_MN>
 struct TG {
-  static constexpr int BM = 128, BK = 64, STAGES = 4;
+  static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 5 : 6);
   static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
   static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
-  static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+  static constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  static constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                 // double-buffered accumulator
+  static constexpr int SCR_BYTES = 4 * 32 * 17 * 4;                  // colsum transpose scratch
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + SCR_BYTES + 512;
 };
 
+// Persistent: CTA c handles tiles c, c + G, ...  (tile = (m-block, n-block,
+// k-slice), m fastest).  Warp 0 = TMA producer, warp 1 = MMA issuer, warps
+// 2..5 = epilogue; the accumulator is double-buffered in TMEM so the epilogue
+// of tile i overlaps the mainloop of tile i+1.
 template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(192, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int64_t M, int64_t N,
                  int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
-  float *__restrict__ C = ep.C;
-  const int64_t ldc = ep.ldc, split_stride = ep.split_stride;
-  const int accumulate = ep.accumulate;
   using T = TG<BN, A_MN, B_MN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + T::STAGES * T::A_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + T::STAGES * T::B_BYTES);
+  float *scr = reinterpret_cast<float *>(sB + T::STAGES * T::B_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(scr) + T::SCR_BYTES);
   uint64_t *empty = full + T::STAGES;
-  uint64_t *done = empty + T::STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *tfull = empty + T::STAGES;   // [2]
+  uint64_t *tempty = tfull + 2;          // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * T::BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t nm = (M + T::BM - 1) / T::BM, nn = (N + BN - 1) / BN;
+  const int64_t ntiles = nm * nn * splits;
   const int64_t nkb_total = (K + T::BK - 1) / T::BK;
-  const int64_t kb0 = (int64_t)blockIdx.z * kb_per_split;
-  const int64_t kb1 = kb0 + kb_per_split < nkb_total ? kb0 + kb_per_split : nkb_total;
-  const int nkb = (int)(kb1 > kb0 ? kb1 - kb0 : 0);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < T::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
     tc::fence_mbar_init();
     tc::tma_prefetch(&ta);
     tc::tma_prefetch(&tb);
@@ -109,138 +116,186 @@ __global__ void __launch_bounds__(128, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  auto tile_coords = [&](int64_t t, int64_t &m0, int64_t &n0, int64_t &kb0, int &nkb, int &z) {
+    z = (int)(t / (nm * nn));
+    int64_t rem = t - (int64_t)z * nm * nn;
+    m0 = (rem % nm) * T::BM;
+    n0 = (rem / nm) * BN;
+    kb0 = (int64_t)z * kb_per_split;
+    int64_t kb1 = kb0 + kb_per_split < nkb_total ? kb0 + kb_per_split : nkb_total;
+    nkb = (int)(kb1 > kb0 ? kb1 - kb0 : 0);
+  };
+
   if (warp == 0) {
+    // ------------------------------------------------------------ producer
     if (tc::elect_one()) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % T::STAGES;
-        const int r = i / T::STAGES;
-        if (r > 0) tc::mbar_wait(&empty[s], (r - 1) & 1);
-        tc::mbar_expect_tx(&full[s], T::A_BYTES + T::B_BYTES);
-        const int32_t kc = (int32_t)((kb0 + i) * T::BK);
-        uint8_t *a = sA + s * T::A_BYTES;
-        uint8_t *b = sB + s * T::B_BYTES;
-        if (!A_MN) {
-          tc::tma_load_2d(a, &ta, &full[s], kc, (int32_t)m0);
-        } else {
-          tc::tma_load_2d(a, &ta, &full[s], (int32_t)m0, kc);
-          tc::tma_load_2d(a + 8192, &ta, &full[s], (int32_t)(m0 + 64), kc);
-        }
-        if (!B_MN) {
-          tc::tma_load_2d(b, &tb, &full[s], kc, (int32_t)n0);
-        } else {
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int64_t m0, n0, kb0;
+        int nkb, z;
+        tile_coords(t, m0, n0, kb0, nkb, z);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % T::STAGES, r = it / T::STAGES;
+          if (r > 0) tc::mbar_wait(&empty[s], (r - 1) & 1);
+          tc::mbar_expect_tx(&full[s], T::A_BYTES + T::B_BYTES);
+          const int32_t kc = (int32_t)((kb0 + i) * T::BK);
+          uint8_t *a = sA + s * T::A_BYTES;
+          uint8_t *b = sB + s * T::B_BYTES;
+          if (!A_MN) {
+            tc::tma_load_2d(a, &ta, &full[s], kc, (int32_t)m0);
+          } else {
+            tc::tma_load_2d(a, &ta, &full[s], (int32_t)m0, kc);
+            tc::tma_load_2d(a + 8192, &ta, &full[s], (int32_t)(m0 + 64), kc);
+          }
+          if (!B_MN) {
+            tc::tma_load_2d(b, &tb, &full[s], kc, (int32_t)n0);
+          } else {
 #pragma unroll
-          for (int j = 0; j < BN / T::B_INNER; ++j)
-            tc::tma_load_2d(b + j * (T::B_ROW * T::BK), &tb, &full[s], (int32_t)(n0 + j * T::B_INNER), kc);
+            for (int j = 0; j < BN / T::B_INNER; ++j)
+              tc::tma_load_2d(b + j * (T::B_ROW * T::BK), &tb, &full[s], (int32_t)(n0 + j * T::B_INNER), kc);
+          }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = tc::idesc_bf16(T::BM, BN, A_MN, B_MN);
     if (tc::elect_one()) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % T::STAGES;
-        tc::mbar_wait(&full[s], (i / T::STAGES) & 1);
+      uint32_t it = 0, li = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
+        int64_t m0, n0, kb0;
+        int nkb, z;
+        tile_coords(t, m0, n0, kb0, nkb, z);
+        const uint32_t acc = li & 1;
+        if (li >= 2) tc::mbar_wait(&tempty[acc], ((li >> 1) - 1) & 1);
         tc::tc_fence_after();
-        const uint32_t a = tc::smem_u32(sA + s * T::A_BYTES);
-        const uint32_t b = tc::smem_u32(sB + s * T::B_BYTES);
+        const uint32_t d = tmem + acc * T::ACC_COLS;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % T::STAGES;
+          tc::mbar_wait(&full[s], (it / T::STAGES) & 1);
+          tc::tc_fence_after();
+          const uint32_t a = tc::smem_u32(sA + s * T::A_BYTES);
+          const uint32_t b = tc::smem_u32(sB + s * T::B_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < T::BK / 16; ++kk) {
-          uint64_t ad = A_MN ? tc::sdesc(a + kk * 2048, 8192, 1024, tc::kSw128)
-                             : tc::sdesc(a + kk * 32, 16, 1024, tc::kSw128);
-          uint64_t bd;
-          if (!B_MN) {
-            bd = tc::sdesc(b + kk * 32, 16, 1024, tc::kSw128);
-          } else {
-            constexpr uint32_t swz = T::B_ROW == 128 ? tc::kSw128 : (T::B_ROW == 64 ? tc::kSw64 : tc::kSw32);
-            bd = tc::sdesc(b + kk * 16 * T::B_ROW, T::B_ROW * T::BK, 8 * T::B_ROW, swz);
+          for (int kk = 0; kk < T::BK / 16; ++kk) {
+            uint64_t ad = A_MN ? tc::sdesc(a + kk * 2048, 8192, 1024, tc::kSw128)
+                               : tc::sdesc(a + kk * 32, 16, 1024, tc::kSw128);
+            uint64_t bd;
+            if (!B_MN) {
+              bd = tc::sdesc(b + kk * 32, 16, 1024, tc::kSw128);
+            } else {
+              constexpr uint32_t swz = T::B_ROW == 128 ? tc::kSw128 : (T::B_ROW == 64 ? tc::kSw64 : tc::kSw32);
+              bd = tc::sdesc(b + kk * 16 * T::B_ROW, T::B_ROW * T::BK, 8 * T::B_ROW, swz);
+            }
+            tc::mma_bf16_ss(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           }
-          tc::mma_bf16_ss(tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_commit(&empty[s]);
         }
-        tc::mma_commit(&empty[s]);
+        tc::mma_commit(&tfull[acc]);
       }
-      tc::mma_commit(done);
     }
     __syncwarp();
-  }
-  tc::mbar_wait(done, 0);
-  tc::tc_fence_after();
-
-  // epilogue: thread <-> row m0 + 32*warp + lane
-  const int64_t row = m0 + warp * 32 + lane;
-  if (ep.out16 == nullptr) {
-    float *out = C + (splits > 1 ? (int64_t)blockIdx.z * split_stride : 0);
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int g = warp & 3;  // TMEM lane group accessible to this warp
+    float *wscr = scr + g * (32 * 17);
+    uint32_t li = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
+      int64_t m0, n0, kb0;
+      int nkb, z;
+      tile_coords(t, m0, n0, kb0, nkb, z);
+      const uint32_t acc = li & 1;
+      tc::mbar_wait(&tfull[acc], (li >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t dcol = tmem + acc * T::ACC_COLS + ((uint32_t)(g * 32) << 16);
+      const int64_t row = m0 + g * 32 + lane;
+      if (ep.out16 == nullptr) {
+        float *out = ep.C + (splits > 1 ? (int64_t)z * ep.split_stride : 0);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      tc::tmem_ld_wait();
-      if (row < M) {
-        float *dst = out + row * ldc + n0 + c0;
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(dcol + (uint32_t)c0, v);
+          tc::tmem_ld_wait();
+          if (row < M) {
+            float *dst = out + row * ep.ldc + n0 + c0;
+            if (n0 + c0 + 16 <= N && !(ep.accumulate && splits == 1) &&
+                ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (n0 + c0 + j < N) {
-            float x = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-            dst[j] = (accumulate && splits == 1) ? dst[j] + x : x;
+              for (int j = 0; j < 4; ++j)
+                reinterpret_cast<float4 *>(dst)[j] =
+                    nkb > 0 ? make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                          __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (n0 + c0 + j < N) {
+                  float x = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+                  dst[j] = (ep.accumulate && splits == 1) ? dst[j] + x : x;
+                }
+              }
+            }
+          }
+        }
+      } else {
+        const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(dcol + (uint32_t)c0, v);
+          tc::tmem_ld_wait();
+          float x[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
+          if (ep.mask16 && row < M) {
+            const __nv_bfloat16 *mk = ep.mask16 + row * ep.ldmask + n0 + c0;
+            if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(mk) & 15) == 0)) {
+              uint4 mv[2];
+              mv[0] = reinterpret_cast<const uint4 *>(mk)[0];
+              mv[1] = reinterpret_cast<const uint4 *>(mk)[1];
+              const __nv_bfloat16 *mb = reinterpret_cast<const __nv_bfloat16 *>(mv);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (!(__bfloat162float(mb[j]) > 0.f)) x[j] = 0.f;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
+            }
+          }
+          __nv_bfloat16 xb[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xb[j] = __float2bfloat16_rn(x[j]);
+          if (row < M) {
+            __nv_bfloat16 *dst = ep.out16 + row * ep.ld16 + n0 + c0;
+            if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+              reinterpret_cast<uint4 *>(dst)[0] = *reinterpret_cast<uint4 *>(&xb[0]);
+              reinterpret_cast<uint4 *>(dst)[1] = *reinterpret_cast<uint4 *>(&xb[8]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (n0 + c0 + j < N) dst[j] = xb[j];
+            }
+          }
+          if (ep.colsum_part) {
+            // column sums of the written (bf16-rounded) values over this warp's 32 rows
+#pragma unroll
+            for (int j = 0; j < 16; ++j) wscr[lane * 17 + j] = row < M ? __bfloat162float(xb[j]) : 0.f;
+            __syncwarp();
+            if (lane < 16) {
+              float y = 0.f;
+#pragma unroll 8
+              for (int q = 0; q < 32; ++q) y += wscr[q * 17 + lane];
+              if (n0 + c0 + lane < N) ep.colsum_part[((m0 / T::BM) * 4 + g) * N + n0 + c0 + lane] = y;
+            }
+            __syncwarp();
           }
         }
       }
-    }
-  } else {
-    const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      tc::tmem_ld_wait();
-      float x[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
-      if (ep.mask16 && row < M) {
-        const __nv_bfloat16 *mk = ep.mask16 + row * ep.ldmask + n0 + c0;
-        if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(mk) & 15) == 0)) {
-          uint4 mv[2];
-          mv[0] = reinterpret_cast<const uint4 *>(mk)[0];
-          mv[1] = reinterpret_cast<const uint4 *>(mk)[1];
-          const __nv_bfloat16 *mb = reinterpret_cast<const __nv_bfloat16 *>(mv);
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (!(__bfloat162float(mb[j]) > 0.f)) x[j] = 0.f;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
-        }
-      }
-      __nv_bfloat16 xb[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) xb[j] = __float2bfloat16_rn(x[j]);
-      if (row < M) {
-        __nv_bfloat16 *dst = ep.out16 + row * ep.ld16 + n0 + c0;
-        if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-          reinterpret_cast<uint4 *>(dst)[0] = *reinterpret_cast<uint4 *>(&xb[0]);
-          reinterpret_cast<uint4 *>(dst)[1] = *reinterpret_cast<uint4 *>(&xb[8]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (n0 + c0 + j < N) dst[j] = xb[j];
-        }
-      }
-      if (ep.colsum_part) {
-        // sum of the written (bf16-rounded) values over this warp's 32 rows:
-        // transpose through the (now idle) pipeline buffers, lane j sums column j
-        float *scr = reinterpret_cast<float *>(sA) + warp * (32 * 17);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) scr[lane * 17 + j] = row < M ? __bfloat162float(xb[j]) : 0.f;
-        __syncwarp();
-        if (lane < 16) {
-          float y = 0.f;
-#pragma unroll 8
-          for (int q = 0; q < 32; ++q) y += scr[q * 17 + lane];
-          if (n0 + c0 + lane < N) ep.colsum_part[((int64_t)blockIdx.y * 4 + warp) * N + n0 + c0 + lane] = y;
-        }
-        __syncwarp();
-      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
   }
   tc::tc_fence_before();
@@ -257,14 +312,23 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (!B_MN) DS_TRY(make_tmap_bf16(&tb, a.B, a.K, a.N, a.ldb, 64, BN));
   else DS_TRY(make_tmap_bf16(&tb, a.B, a.N, a.K, a.ldb, T::B_INNER, 64));
   auto kern = tgemm_kernel<BN, A_MN, B_MN>;
-  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
+  static bool attr_set = false;
+  if (!attr_set) {
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
+    attr_set = true;
+  }
   int64_t nkb = (a.K + 63) / 64;
   int splits = a.splits < 1 ? 1 : a.splits;
   int kbps = (int)ceil_div(nkb, splits);
   if (kbps < 1) kbps = 1;
   splits = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
-  dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.M, T::BM), (unsigned)splits);
-  kern<<<grid, 128, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a, splits);
+  int64_t ntiles = ceil_div(a.M, T::BM) * ceil_div(a.N, BN) * splits;
+  int per_sm = (227 * 1024) / T::SMEM;
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 2) per_sm = 2;
+  if (per_sm * T::TMEM_COLS > 512) per_sm = 512 / T::TMEM_COLS;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm));
+  kern<<<grid, 192, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a, splits);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

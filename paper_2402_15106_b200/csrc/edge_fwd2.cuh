@@ -2,15 +2,16 @@
 // kappa_phi MLP on tcgen05 + per-row S_i = H_i^T V_i, K_p never formed.
 //
 // Tiles hold whole rows (each padded to a multiple of 16 slots, at most NMAX
-// rows and 128 slots per tile).  Roles (12 warps):
+// rows and 128 slots per tile).  Roles (16 warps):
 //   loader  (warps 0,2,3) : tile walker; cp.async gathers of e rows (double
 //                           buffered) and of v_{j(p)} rows (single buffer)
 //   MMA     (warp 1)      : MMA1 z1 = E W1^T (K=16); MMA2 z2 = a1 W2^T in two
 //                           N=128 halves, K-block j issued as soon as the
 //                           epilogue has written block j of a1; S MMAs per
 //                           row and kappa half as soon as h half is written
-//   EPI_A   (warps 4-7)   : a1 = relu(z1+b1), h = relu(z2+b2) TMEM -> SMEM
-//   EPI_B   (warps 8-11)  : S_i TMEM -> scaled bf16 -> S~_aug (global)
+//   EPI_A   (warps 4-11)  : a1 = relu(z1+b1), h = relu(z2+b2) TMEM -> SMEM
+//                           (two column groups of 4 warps)
+//   EPI_B   (warps 12-15) : S_i TMEM -> scaled bf16 -> S~_aug (global)
 // TMEM: two 256-column regions, tile t uses region t&1 for z1 (0..255), z2
 // (kappa half 0 at columns 128..255, half 1 at 0..127) and the S accumulators
 // (row g, kappa half h at the columns of z2 half h, offset g*D), so EPI_B of
@@ -23,17 +24,19 @@ namespace dsmpnn {
 struct TileDesc2 {
   int32_t slot_edge[128];
   int64_t node[4];
+  int64_t ebase[4];       // row_ptr[node]
   int32_t slot0[4], deg[4];
   int32_t nnodes, more;
 };
 
 struct Misc2 {
   TileDesc2 desc[2];
-  uint64_t e_full[2], e_empty[2], d1_full[2], region_free[2], desc_free[2];
+  uint64_t e_full[2], e_empty, d1_full[2], region_free[2], desc_free[2];
   uint64_t v_full, v_empty, ah_free, s_full;
   uint64_t a1_ready[4], d2_full[2], h_ready[2];
   int64_t cur_row, row_end;
   uint32_t tmem;
+  float b1[KH], b2[KH];     // biases (L1 is all but absent at this SMEM carve-out)
 };
 
 template <int D>
@@ -48,37 +51,53 @@ struct EF2 {
   static constexpr int OFF_AH = OFF_W2 + W2_BYTES;
   static constexpr int OFF_V = OFF_AH + AH_BYTES;
   static constexpr int OFF_W1 = OFF_V + V_BYTES;
-  static constexpr int OFF_E = OFF_W1 + W1_BYTES;       // 2 buffers
-  static constexpr int OFF_MISC = OFF_E + 2 * E_BYTES;
+  static constexpr int OFF_E = OFF_W1 + W1_BYTES;
+  static constexpr int OFF_MISC = OFF_E + E_BYTES;
   static constexpr int SMEM = OFF_MISC + (int)sizeof(Misc2) + 1024;
   static constexpr uint32_t ROWB = D * 2;
 };
 
-// walker: next tile of whole rows (thread 0 of the loader group)
+// walker: next tile of whole rows, executed by one full warp: the lanes fetch
+// 32 consecutive row_ptr entries in one round trip, lane 0 packs the rows.
 template <int NMAX>
-__device__ __forceinline__ void walk_tile(Misc2 *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr) {
+__device__ __forceinline__ void walk_tile(Misc2 *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr, int lane) {
   int used = 0, nn = 0;
-  while (m->cur_row < m->row_end && nn < NMAX) {
-    int64_t i = m->cur_row;
-    int64_t p0 = row_ptr[i];
-    int deg = (int)(row_ptr[i + 1] - p0);
-    if (deg == 0) { m->cur_row++; continue; }
-    int padded = (deg + 15) & ~15;
-    if (padded > 128) __trap();  // rows longer than 128 edges are rejected on the host
-    if (used + padded > 128) break;
-    d->node[nn] = i;
-    d->slot0[nn] = used;
-    d->deg[nn] = deg;
-    used += padded;
-    nn++;
-    m->cur_row++;
+  int64_t cur = m->cur_row;
+  const int64_t end = m->row_end;
+  bool done = false;
+  while (!done && cur < end) {
+    const int64_t my = cur + lane <= end ? cur + lane : end;
+    const int64_t rp = row_ptr[my];
+    int k = 0;
+    for (; k < 31; ++k) {
+      const int64_t a = __shfl_sync(0xffffffffu, rp, k), z = __shfl_sync(0xffffffffu, rp, k + 1);
+      if (cur + k >= end) { done = true; break; }
+      const int deg = (int)(z - a);
+      if (deg == 0) continue;
+      const int padded = (deg + 15) & ~15;
+      if (padded > 128) __trap();  // rows longer than 128 edges are rejected on the host
+      if (used + padded > 128 || nn == NMAX) { done = true; break; }
+      if (lane == 0) {
+        d->node[nn] = cur + k;
+        d->ebase[nn] = a;
+        d->slot0[nn] = used;
+        d->deg[nn] = deg;
+      }
+      used += padded;
+      nn++;
+    }
+    cur += k;
   }
-  d->nnodes = nn;
-  d->more = nn > 0;
+  if (lane == 0) {
+    m->cur_row = cur;
+    d->nnodes = nn;
+    d->more = nn > 0;
+  }
+  __syncwarp();
 }
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     edge_fwd2_kernel(const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
                      const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int64_t eb, int64_t ee, Packed pw,
                      const float *__restrict__ b1, const float *__restrict__ b2, __nv_bfloat16 *__restrict__ S,
@@ -86,7 +105,7 @@ __global__ void __launch_bounds__(384, 1)
   using C = EF2<D>;
   constexpr int NMAX = C::NMAX;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space (LDS/STS)
   uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sV = sm + C::OFF_V, *sW1 = sm + C::OFF_W1,
           *sE = sm + C::OFF_E;
   Misc2 *m = reinterpret_cast<Misc2 *>(sm + C::OFF_MISC);
@@ -109,13 +128,14 @@ __global__ void __launch_bounds__(384, 1)
     m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&m->e_full[b], 96);
-      tc::mbar_init(&m->e_empty[b], 1);
+
       tc::mbar_init(&m->d1_full[b], 1);
       tc::mbar_init(&m->region_free[b], 4);
       tc::mbar_init(&m->desc_free[b], 3);
       tc::mbar_init(&m->d2_full[b], 1);
-      tc::mbar_init(&m->h_ready[b], 128);
+      tc::mbar_init(&m->h_ready[b], 256);
     }
+    tc::mbar_init(&m->e_empty, 1);
     tc::mbar_init(&m->v_full, 96);
     tc::mbar_init(&m->v_empty, 1);
     tc::mbar_init(&m->ah_free, 1);
@@ -126,15 +146,19 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 1) tc::tmem_alloc<512>(&m->tmem);
   {  // W2 (K-major SW128, 4 K-blocks of 64) and W1 (interleaved K=16), resident
     const uint4 *g2 = reinterpret_cast<const uint4 *>(pw.W2);
-    for (int q = tid; q < KH * KH / 8; q += 384) {
+    for (int q = tid; q < KH * KH / 8; q += 512) {
       int n = q / (KH / 8), rem = q % (KH / 8);
       int j = rem / 8, c = rem % 8;
       *reinterpret_cast<uint4 *>(sW2 + j * (KH * 128) + tc::sw128_off(n, c)) = g2[q];
     }
     const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
-    for (int q = tid; q < KH * 2; q += 384) {
+    for (int q = tid; q < KH * 2; q += 512) {
       int r = q / 2, u = q % 2;
       *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
+    }
+    for (int q = tid; q < KH; q += 512) {
+      m->b1[q] = b1[q];
+      m->b2[q] = b2[q];
     }
   }
   tc::fence_async_shared();
@@ -150,14 +174,14 @@ __global__ void __launch_bounds__(384, 1)
       const int b = t & 1;
       TileDesc2 *dsc = &m->desc[b];
       if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
-      if (li == 0) walk_tile<NMAX>(m, dsc, row_ptr);
+      if (warp == 0) walk_tile<NMAX>(m, dsc, row_ptr, lane);
       tc::named_sync(1, 96);
       const int nn = dsc->nnodes;
       for (int s = li; s < 128; s += 96) {
         int32_t pe = -1;
         for (int g = 0; g < nn; ++g) {
           int o = s - dsc->slot0[g];
-          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(row_ptr[dsc->node[g]] + o);
+          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(dsc->ebase[g] + o);
         }
         dsc->slot_edge[s] = pe;
       }
@@ -166,25 +190,44 @@ __global__ void __launch_bounds__(384, 1)
         tc::mbar_arrive(&m->e_full[b]);
         break;
       }
-      if (t >= 2) tc::mbar_wait(&m->e_empty[b], ((t >> 1) - 1) & 1);
-      uint8_t *eb_s = sE + b * C::E_BYTES;
-      for (int q = li; q < 256; q += 96) {
-        int s = q >> 1, u = q & 1;
-        int pe = dsc->slot_edge[s];
-        tc::cp_async16(eb_s + il_off(s, u), e16 + (int64_t)(pe < 0 ? 0 : pe) * 16 + u * 8, pe < 0 ? 0u : 16u);
+      // issue every global load of the tile first (registers), store to SMEM
+      // only once the consumers have released the buffers
+      constexpr int CH = D / 8;                        // 16-byte chunks per v row
+      constexpr int NE = (256 + 95) / 96, NV = (128 * CH + 95) / 96;
+      uint4 ev[NE], vv[NV];
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int q = li + 96 * k;
+        ev[k] = make_uint4(0, 0, 0, 0);
+        if (q < 256) {
+          const int pe = dsc->slot_edge[q >> 1];
+          if (pe >= 0) ev[k] = __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe * 16) + (q & 1));
+        }
       }
-      tc::cp_async_wait_all();
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int q = li + 96 * k;
+        vv[k] = make_uint4(0, 0, 0, 0);
+        if (q < 128 * CH) {
+          const int pe = dsc->slot_edge[q / CH];
+          if (pe >= 0) vv[k] = __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)__ldg(col + pe) * D) + (q % CH));
+        }
+      }
+      if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
+      uint8_t *eb_s = sE;
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int q = li + 96 * k;
+        if (q < 256) *reinterpret_cast<uint4 *>(eb_s + il_off(q >> 1, q & 1)) = ev[k];
+      }
       tc::fence_async_shared();
       tc::mbar_arrive(&m->e_full[b]);
       if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
-      constexpr int CH = D / 8;
-      for (int q = li; q < 128 * CH; q += 96) {
-        int s = q / CH, c = q % CH;
-        int pe = dsc->slot_edge[s];
-        const __nv_bfloat16 *src = v + (int64_t)(pe < 0 ? 0 : col[pe]) * D + c * 8;
-        tc::cp_async16(sV + v_off<D>(s, c), src, pe < 0 ? 0u : 16u);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int q = li + 96 * k;
+        if (q < 128 * CH) *reinterpret_cast<uint4 *>(sV + v_off<D>(q / CH, q % CH)) = vv[k];
       }
-      tc::cp_async_wait_all();
       tc::fence_async_shared();
       tc::mbar_arrive(&m->v_full);
     }
@@ -206,10 +249,10 @@ __global__ void __launch_bounds__(384, 1)
         tc::tc_fence_after();
         const uint32_t r = tmem + b * 256;
         // MMA1: z1 = E W1^T (one K=16 step)
-        tc::mma_bf16_ss(r, tc::sdesc(aE + b * C::E_BYTES, 128, 256, tc::kSwNone),
+        tc::mma_bf16_ss(r, tc::sdesc(aE, 128, 256, tc::kSwNone),
                         tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC1, 0u);
         tc::mma_commit(&m->d1_full[b]);
-        tc::mma_commit(&m->e_empty[b]);
+        tc::mma_commit(&m->e_empty);
         // MMA2: z2 = a1 W2^T in two N halves.  Half 0 (kappa 0..127) goes to
         // columns 128..255, whose z1 the epilogue drains first (a1 blocks 2, 3),
         // and consumes a1 K-blocks in the order they arrive (2, 3, 0, 1); half 1
@@ -255,9 +298,10 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (warp < 12) {
     // ============================================================= EPI_A
-    const int grp = warp & 3;
+    // 8 warps: rows by warp % 4 (TMEM lane group), column group cg = 0 / 1
+    const int grp = warp & 3, cg = (warp - 4) >> 2;
     const int erow = grp * 32 + lane;  // slot row == TMEM lane
     const uint32_t lane_off = (uint32_t)(grp * 32) << 16;
     for (uint32_t t = 0;; ++t) {
@@ -269,10 +313,11 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_wait(&m->d1_full[b], ph);
       if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
       tc::tc_fence_after();
-      // a1 = relu(z1 + b1) -> AH, block by block (MMA2 starts on block j at once)
+      // a1 = relu(z1 + b1) -> AH; group 1 drains blocks 3, 2 (columns MMA2
+      // half 0 overwrites first), group 0 blocks 0, 1
 #pragma unroll 1
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = (jj + 2) & 3;  // columns 128..255 first (see MMA2)
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = cg == 1 ? 3 - jj : jj;
         uint8_t *blk = sAH + j * (128 * 128);
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
@@ -283,8 +328,8 @@ __global__ void __launch_bounds__(384, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b1 + c0 + 2 * q), 0.f),
-                                  fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b1 + c0 + 2 * q + 1), 0.f));
+            pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b1[c0 + 2 * q], 0.f),
+                                  fmaxf(__uint_as_float(x[2 * q + 1]) + m->b1[c0 + 2 * q + 1], 0.f));
           *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
@@ -292,55 +337,57 @@ __global__ void __launch_bounds__(384, 1)
         tc::tc_fence_before();
         tc::mbar_arrive(&m->a1_ready[j]);
       }
-      // h = relu(z2 + b2): half 0 read while MMA2 half 1 runs, stored once MMA2 is done
+      // h = relu(z2 + b2).  kappa half 0 (TMEM columns 128..255): group cg
+      // takes kappa 64*cg.., read while MMA2 half 1 runs, stored once MMA2 is
+      // done (MMA2 half 1 still reads a1 from AH).
       tc::mbar_wait(&m->d2_full[0], p1);
       tc::tc_fence_after();
-      uint32_t hp[64];
+      uint32_t hp[32];
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c0 = cc * 16;
+      for (int cc = 0; cc < 4; ++cc) {
+        const int k0 = cg * 64 + cc * 16;  // kappa
         uint32_t x[16];
-        tc::tmem_ld16(r + 128 + c0, x);
+        tc::tmem_ld16(r + 128 + k0, x);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          hp[cc * 8 + q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b2 + c0 + 2 * q), 0.f),
-                                         fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b2 + c0 + 2 * q + 1), 0.f));
+          hp[cc * 8 + q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b2[k0 + 2 * q], 0.f),
+                                         fmaxf(__uint_as_float(x[2 * q + 1]) + m->b2[k0 + 2 * q + 1], 0.f));
       }
       tc::mbar_wait(&m->d2_full[1], p1);
       tc::tc_fence_after();
+      {
+        uint8_t *blk = sAH + cg * (128 * 128);
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        uint8_t *blk = sAH + (cc / 4) * (128 * 128);
-        const int ch = (cc % 4) * 2;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) =
-            make_uint4(hp[cc * 8 + 0], hp[cc * 8 + 1], hp[cc * 8 + 2], hp[cc * 8 + 3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) =
-            make_uint4(hp[cc * 8 + 4], hp[cc * 8 + 5], hp[cc * 8 + 6], hp[cc * 8 + 7]);
+        for (int cc = 0; cc < 4; ++cc) {
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) =
+              make_uint4(hp[cc * 8 + 0], hp[cc * 8 + 1], hp[cc * 8 + 2], hp[cc * 8 + 3]);
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) =
+              make_uint4(hp[cc * 8 + 4], hp[cc * 8 + 5], hp[cc * 8 + 6], hp[cc * 8 + 7]);
+        }
       }
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready[0]);
-#pragma unroll 1
-      for (int cc = 8; cc < 16; ++cc) {
-        const int c0 = cc * 16;
+      // kappa half 1 (TMEM columns 0..127): group cg takes kappa 128 + 64*cg..
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int k0 = 128 + cg * 64 + cc * 16;
         uint32_t x[16];
-        tc::tmem_ld16(r + c0 - 128, x);
+        tc::tmem_ld16(r + k0 - 128, x);
         tc::tmem_ld_wait();
         uint32_t pk[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + __ldg(b2 + c0 + 2 * q), 0.f),
-                                fmaxf(__uint_as_float(x[2 * q + 1]) + __ldg(b2 + c0 + 2 * q + 1), 0.f));
-        uint8_t *blk = sAH + (cc / 4) * (128 * 128);
-        const int ch = (cc % 4) * 2;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b2[k0 + 2 * q], 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + m->b2[k0 + 2 * q + 1], 0.f));
+        uint8_t *blk = sAH + (2 + cg) * (128 * 128);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready[1]);
-      tc::tc_fence_before();
       __syncwarp();
       if (warp == 4 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
@@ -382,7 +429,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&m->region_free[b]);
-      if (warp == 8 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+      if (warp == 12 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   }
   tc::tc_fence_before();

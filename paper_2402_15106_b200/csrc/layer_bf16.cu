@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256, 1)
                     __nv_bfloat16 *__restrict__ S, int64_t kp, const int32_t *__restrict__ col) {
   using C = EF<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space (LDS/STS)
   uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sV = sm + C::OFF_V, *sW1 = sm + C::OFF_W1,
           *sE = sm + C::OFF_E;
   EdgeMisc *m = reinterpret_cast<EdgeMisc *>(sm + C::OFF_MISC);
@@ -381,7 +381,7 @@ static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_FWD, s);
-  kern<<<grid, 384, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  kern<<<grid, 512, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256, 1)
                     __nv_bfloat16 *__restrict__ dZ2g, float *__restrict__ Ug, float *__restrict__ db2_part) {
   using C = EB<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space (LDS/STS)
   uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sDS = sm + C::OFF_DS, *sV = sm + C::OFF_V,
           *sW1 = sm + C::OFF_W1, *sE = sm + C::OFF_E;
   EdgeMisc *m = reinterpret_cast<EdgeMisc *>(sm + C::OFF_MISC);

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(192, 1)
                  int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
   using T = TG<BN, A_MN, B_MN>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t *sA = smem;
   uint8_t *sB = smem + T::STAGES * T::A_BYTES;
   float *scr = reinterpret_cast<float *>(sB + T::STAGES * T::B_BYTES);

@@ -416,13 +416,21 @@ __global__ void __launch_bounds__(512, 1)
             uint32_t x[16];
             tc::tmem_ld16(r + (h == 0 ? 128 : 0) + g * D + c0, x);
             tc::tmem_ld_wait();
-            uint32_t pk[8];
+            // S~_i layout [c][kappa] (kappa contiguous): lane pairs (kappa, kappa+1)
+            // swap halves so every 4-byte store of the warp covers 64
+            // contiguous bytes (two coalesced segments per instruction)
+            const bool odd = lane & 1;
+            const int cb = odd ? 8 : 0;  // columns this lane stores: c0+cb .. c0+cb+7
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              pk[q] = tc::pack_bf16(__uint_as_float(x[2 * q]) * inv, __uint_as_float(x[2 * q + 1]) * inv);
-            uint4 *dst = reinterpret_cast<uint4 *>(Si + (int64_t)kap * D + c0);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            for (int q = 0; q < 8; ++q) {
+              const float mine = __uint_as_float(x[cb + q]) * inv;
+              const float give = __uint_as_float(x[(8 - cb) + q]) * inv;   // partner's columns
+              const float other = __shfl_xor_sync(0xffffffffu, give, 1);
+              const uint32_t pair = odd ? tc::pack_bf16(other, mine) : tc::pack_bf16(mine, other);
+              asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(Si + (int64_t)(c0 + cb + q) * KH + (kap & ~1)),
+                           "r"(pair)
+                           : "memory");
+            }
           }
         }
       }

@@ -50,7 +50,10 @@ __global__ void pack_bf16_kernel(const float *__restrict__ W1, const float *__re
       else if (kap == k + 1 && root_dense) val = Wr[(int64_t)o * di + c];
       __nv_bfloat16 bv = __float2bfloat16_rn(val);
       p.Th[row * dout + o] = bv;
-      p.ThT[(int64_t)o * kp + row] = bv;
+      // the forward S~ rows store the kappa < k block as [c][kappa]: K index
+      // c*k + kappa (edge kernel EPI_B); the bias and root blocks keep k*d_in + c
+      const int64_t kk = kap < k ? (int64_t)c * k + kap : row;
+      p.ThT[(int64_t)o * kp + kk] = bv;
     }
   }
 }

@@ -49,9 +49,16 @@ __global__ void unpack_dtheta_aug_kernel(const float *__restrict__ dT, int k, in
                                          float *__restrict__ db3, float *__restrict__ dWr) {
   int64_t total = (int64_t)(k + 2) * D * D;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t row = t / D;
+    int64_t row = t / D;  // K index of the forward S~_aug layout
     int o = (int)(t - row * D);
-    int kap = (int)(row / D), c = (int)(row - (int64_t)kap * D);
+    int kap, c;
+    if (row < (int64_t)k * D) {  // [c][kappa] block
+      c = (int)(row / k);
+      kap = (int)(row - (int64_t)c * k);
+    } else {
+      kap = (int)(row / D);
+      c = (int)(row - (int64_t)kap * D);
+    }
     float x = dT[t];
     if (kap < k) { if (dW3) dW3[((int64_t)c * D + o) * k + kap] += x; }
     else if (kap == k) { if (db3) db3[(int64_t)c * D + o] += x; }

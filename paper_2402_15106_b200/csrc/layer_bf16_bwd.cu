@@ -423,7 +423,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.U = c.take<float>(E * D);
   b.part = c.take<float>((int64_t)kSplitsW * d.k * d.k);
   b.db2_part = c.take<float>((int64_t)kNumSMs * d.k);
-  b.db1_part = c.take<float>(((E + 127) / 128 + 1) * 4 * d.k);
+  b.db1_part = c.take<float>((int64_t)kColsumRows * d.k);
   b.dW1f = c.take<float>((int64_t)d.k * 16);
   b.de16 = c.take<float>(E * 16);
   return b;
@@ -561,9 +561,9 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     a.mask16 = b.A1 + eb * k;
     a.ldmask = k;
     a.colsum_part = b.db1_part;
+    DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
     DS_TRY(tgemm(a, s));
-    int rows = (int)(ceil_div(nE, 128) * 4);
-    DS_TRY(colsum(b.db1_part, rows, k, k, gr.b1, 1, s));
+    DS_TRY(colsum(b.db1_part, kColsumRows, k, k, gr.b1, 1, s));
   }
   // B6: dW1 += dz1^T e ;  de = dz1 W1
   if (gr.W1) {

@@ -8,6 +8,7 @@
 // 32x32b, one thread per output row) to fp32 global memory.  TMA zero-fills
 // out-of-range boxes, so ragged M/N/K tails need no special path.
 #include <cuda.h>
+#include <string.h>
 
 #include "tc.cuh"
 #include "tgemm.cuh"
@@ -58,39 +59,44 @@ dsmpnn_status make_tmap_bf16(CUtensorMap *m, const void *base, int64_t inner, in
   return DSMPNN_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool E16 = false>
 struct TG {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN >= 256 ? 4 : (BN >= 128 ? 5 : 6);
+  static constexpr int STAGES = BN >= 256 ? (E16 ? 3 : 4) : (BN >= 128 ? 5 : 6);
+  // bf16 epilogue staging per epilogue warp: 2 output buffers + 1 mask buffer (32 rows x 128 B each)
+  static constexpr int STG_BYTES = E16 ? 4 * 3 * 4096 : 0;
   static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
   static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
   static constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   static constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                 // double-buffered accumulator
   static constexpr int SCR_BYTES = 4 * 32 * 17 * 4;                  // colsum transpose scratch
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + SCR_BYTES + 512;
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STG_BYTES + SCR_BYTES + 512;
 };
 
 // Persistent: CTA c handles tiles c, c + G, ...  (tile = (m-block, n-block,
 // k-slice), m fastest).  Warp 0 = TMA producer, warp 1 = MMA issuer, warps
 // 2..5 = epilogue; the accumulator is double-buffered in TMEM so the epilogue
 // of tile i overlaps the mainloop of tile i+1.
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool E16>
 __global__ void __launch_bounds__(192, 1)
-    tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int64_t M, int64_t N,
-                 int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
-  using T = TG<BN, A_MN, B_MN>;
+    tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                 const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap tmask, int64_t M,
+                 int64_t N, int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
+  using T = TG<BN, A_MN, B_MN, E16>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t *sA = smem;
   uint8_t *sB = smem + T::STAGES * T::A_BYTES;
-  float *scr = reinterpret_cast<float *>(sB + T::STAGES * T::B_BYTES);
+  uint8_t *sStg = sB + T::STAGES * T::B_BYTES;  // E16 staging (1024-aligned)
+  float *scr = reinterpret_cast<float *>(sStg + T::STG_BYTES);
   uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(scr) + T::SCR_BYTES);
   uint64_t *empty = full + T::STAGES;
   uint64_t *tfull = empty + T::STAGES;   // [2]
   uint64_t *tempty = tfull + 2;          // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *mbar = tempty + 2;           // [4] mask loads, one per epilogue warp
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nm = (M + T::BM - 1) / T::BM, nn = (N + BN - 1) / BN;
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(192, 1)
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 4);
     }
+    for (int a = 0; a < 4; ++a) tc::mbar_init(&mbar[a], 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&ta);
     tc::tma_prefetch(&tb);
@@ -199,8 +206,8 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int g = warp & 3;  // TMEM lane group accessible to this warp
-    float *wscr = scr + g * (32 * 17);
-    uint32_t li = 0;
+    uint32_t li = 0, ocount = 0, mphase = 0;
+    float csum[BN / 64 > 0 ? BN / 64 : 1][2] = {};
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
       int64_t m0, n0, kb0;
       int nkb, z;
@@ -238,80 +245,108 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
         }
-      } else {
+      } else if constexpr (E16) {
+        // bf16 epilogue, 64 columns at a time: TMEM -> registers (scale,
+        // mask from a TMA-loaded tile) -> swizzled SMEM staging -> TMA store
         const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
+        uint8_t *mst = sStg + (g * 3 + 2) * 4096;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t v[16];
-          tc::tmem_ld16(dcol + (uint32_t)c0, v);
-          tc::tmem_ld_wait();
-          float x[16];
+        for (int c64 = 0; c64 < BN / 64; ++c64) {
+          const int64_t ncol = n0 + c64 * 64;
+          if (ncol >= N) break;
+          uint8_t *ost = sStg + (g * 3 + (ocount & 1)) * 4096;
+          if (ep.mask16 && lane == 0) {
+            tc::mbar_expect_tx(&mbar[g], 4096);
+            tc::tma_load_2d(mst, &tmask, &mbar[g], (int32_t)ncol, (int32_t)(m0 + g * 32));
+          }
+          uint32_t v[64];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
-          if (ep.mask16 && row < M) {
-            const __nv_bfloat16 *mk = ep.mask16 + row * ep.ldmask + n0 + c0;
-            if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(mk) & 15) == 0)) {
-              uint4 mv[2];
-              mv[0] = reinterpret_cast<const uint4 *>(mk)[0];
-              mv[1] = reinterpret_cast<const uint4 *>(mk)[1];
-              const __nv_bfloat16 *mb = reinterpret_cast<const __nv_bfloat16 *>(mv);
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[16];
+            tc::tmem_ld16(dcol + (uint32_t)(c64 * 64 + q * 16), w);
+            tc::tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (!(__bfloat162float(mb[j]) > 0.f)) x[j] = 0.f;
-            } else {
+            for (int j = 0; j < 16; ++j) v[q * 16 + j] = w[j];
+          }
+          float x[64];
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (n0 + c0 + j < N && !(__bfloat162float(mk[j]) > 0.f)) x[j] = 0.f;
+          for (int j = 0; j < 64; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
+          if (ep.mask16) {
+            tc::mbar_wait(&mbar[g], mphase & 1);
+            ++mphase;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 mv = *reinterpret_cast<const uint4 *>(mst + tc::sw128_off(lane, c));
+              const __nv_bfloat16 *mb = reinterpret_cast<const __nv_bfloat16 *>(&mv);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (!(__bfloat162float(mb[j]) > 0.f)) x[c * 8 + j] = 0.f;
             }
           }
-          __nv_bfloat16 xb[16];
+          if (lane == 0) tc::bulk_wait_read<1>();  // this staging buffer's previous store has read it
+          __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) xb[j] = __float2bfloat16_rn(x[j]);
-          if (row < M) {
-            __nv_bfloat16 *dst = ep.out16 + row * ep.ld16 + n0 + c0;
-            if (n0 + c0 + 16 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-              reinterpret_cast<uint4 *>(dst)[0] = *reinterpret_cast<uint4 *>(&xb[0]);
-              reinterpret_cast<uint4 *>(dst)[1] = *reinterpret_cast<uint4 *>(&xb[8]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (n0 + c0 + j < N) dst[j] = xb[j];
-            }
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4 *>(ost + tc::sw128_off(lane, c)) =
+                make_uint4(tc::pack_bf16(x[c * 8 + 0], x[c * 8 + 1]), tc::pack_bf16(x[c * 8 + 2], x[c * 8 + 3]),
+                           tc::pack_bf16(x[c * 8 + 4], x[c * 8 + 5]), tc::pack_bf16(x[c * 8 + 6], x[c * 8 + 7]));
+          tc::fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_2d(&tout, ost, (int32_t)ncol, (int32_t)(m0 + g * 32));
+            tc::bulk_commit();
           }
           if (ep.colsum_part) {
-            // column sums of the written (bf16-rounded) values over this warp's 32 rows
-#pragma unroll
-            for (int j = 0; j < 16; ++j) wscr[lane * 17 + j] = row < M ? __bfloat162float(xb[j]) : 0.f;
-            __syncwarp();
-            if (lane < 16) {
-              float y = 0.f;
+            // lane j sums columns 2j, 2j+1 of the written (bf16) tile over the 32 rows
+            float y0 = 0.f, y1 = 0.f;
+            const int c = (2 * lane) >> 3, e = (2 * lane) & 7;
 #pragma unroll 8
-              for (int q = 0; q < 32; ++q) y += wscr[q * 17 + lane];
-              if (n0 + c0 + lane < N) ep.colsum_part[((m0 / T::BM) * 4 + g) * N + n0 + c0 + lane] = y;
+            for (int r = 0; r < 32; ++r) {
+              const __nv_bfloat162 p = *reinterpret_cast<const __nv_bfloat162 *>(ost + tc::sw128_off(r, c) + e * 2);
+              y0 += __bfloat162float(p.x);
+              y1 += __bfloat162float(p.y);
             }
-            __syncwarp();
+            csum[c64][0] += y0;  // accumulated over this CTA's tiles (single N block)
+            csum[c64][1] += y1;
           }
+          ++ocount;
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
+    if (E16 && ep.colsum_part) {
+#pragma unroll
+      for (int c64 = 0; c64 < BN / 64; ++c64)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int col = c64 * 64 + 2 * lane + u;
+          if (col < N) ep.colsum_part[((int64_t)blockIdx.x * 4 + g) * N + col] = csum[c64][u];
+        }
+    }
   }
+  if (E16 && warp >= 2 && lane == 0) tc::bulk_wait<0>();  // TMA stores drained before exit
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<T::TMEM_COLS>(tmem);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool E16>
 static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
-  using T = TG<BN, A_MN, B_MN>;
-  CUtensorMap ta, tb;
+  using T = TG<BN, A_MN, B_MN, E16>;
+  CUtensorMap ta, tb, tout, tmask;
+  memset(&tout, 0, sizeof(tout));
+  memset(&tmask, 0, sizeof(tmask));
+  if (E16) {
+    DS_TRY(make_tmap_bf16(&tout, a.out16, a.N, a.M, a.ld16, 64, 32));
+    if (a.mask16) DS_TRY(make_tmap_bf16(&tmask, a.mask16, a.N, a.M, a.ldmask, 64, 32));
+  }
   if (!A_MN) DS_TRY(make_tmap_bf16(&ta, a.A, a.K, a.M, a.lda, 64, 128));
   else DS_TRY(make_tmap_bf16(&ta, a.A, a.M, a.K, a.lda, 64, 64));
   if (!B_MN) DS_TRY(make_tmap_bf16(&tb, a.B, a.K, a.N, a.ldb, 64, BN));
   else DS_TRY(make_tmap_bf16(&tb, a.B, a.N, a.K, a.ldb, T::B_INNER, 64));
-  auto kern = tgemm_kernel<BN, A_MN, B_MN>;
+  auto kern = tgemm_kernel<BN, A_MN, B_MN, E16>;
   static bool attr_set = false;
   if (!attr_set) {
     DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
@@ -328,18 +363,25 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (per_sm > 2) per_sm = 2;
   if (per_sm * T::TMEM_COLS > 512) per_sm = 512 / T::TMEM_COLS;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm));
-  kern<<<grid, 192, T::SMEM, s>>>(ta, tb, a.M, a.N, a.K, kbps, a, splits);
+  kern<<<grid, 192, T::SMEM, s>>>(ta, tb, tout, tmask, a.M, a.N, a.K, kbps, a, splits);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
 
 template <bool A_MN, bool B_MN>
 static dsmpnn_status dispatch_bn(const TgemmArgs &a, cudaStream_t s) {
-  if (a.N <= 16) return launch_tgemm<16, A_MN, B_MN>(a, s);
-  if (a.N <= 32) return launch_tgemm<32, A_MN, B_MN>(a, s);
-  if (a.N <= 64) return launch_tgemm<64, A_MN, B_MN>(a, s);
-  if (a.N <= 128) return launch_tgemm<128, A_MN, B_MN>(a, s);
-  return launch_tgemm<256, A_MN, B_MN>(a, s);
+  if (a.out16) {
+    DS_CHECK_ARG(a.N >= 64, DSMPNN_ERR_UNSUPPORTED, "tgemm: bf16 epilogue needs N >= 64");
+    DS_CHECK_ARG(!a.colsum_part || a.N <= 256, DSMPNN_ERR_UNSUPPORTED, "tgemm: column sums need N <= 256");
+    if (a.N <= 64) return launch_tgemm<64, A_MN, B_MN, true>(a, s);
+    if (a.N <= 128) return launch_tgemm<128, A_MN, B_MN, true>(a, s);
+    return launch_tgemm<256, A_MN, B_MN, true>(a, s);
+  }
+  if (a.N <= 16) return launch_tgemm<16, A_MN, B_MN, false>(a, s);
+  if (a.N <= 32) return launch_tgemm<32, A_MN, B_MN, false>(a, s);
+  if (a.N <= 64) return launch_tgemm<64, A_MN, B_MN, false>(a, s);
+  if (a.N <= 128) return launch_tgemm<128, A_MN, B_MN, false>(a, s);
+  return launch_tgemm<256, A_MN, B_MN, false>(a, s);
 }
 
 dsmpnn_status tgemm(const TgemmArgs &a, cudaStream_t s) {

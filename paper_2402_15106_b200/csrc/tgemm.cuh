@@ -11,6 +11,8 @@ namespace dsmpnn {
 //   A is M x K: K-major if stored [M][K] (a_mn_major = false) or M-major if
 //   stored [K][M] (a_mn_major = true).  B is K x N: K-major if stored [N][K],
 //   N-major if stored [K][N].  ld = elements between consecutive stored rows.
+constexpr int kColsumRows = 148 * 2 * 4;
+
 struct TgemmArgs {
   int64_t M, N, K;
   const void *A;
@@ -28,8 +30,9 @@ struct TgemmArgs {
   // as bf16 to out16[m*ld16 + n] instead of C, after
   //   x *= row_scale[m]             (row_scale != null)
   //   x  = mask16[m*ldmask + n] > 0 ? x : 0   (mask16 != null)
-  // and per-warp column sums of the written values go to
-  //   colsum_part[(blockIdx.y*4 + warp) * N + n]   (colsum_part != null)
+  // and column sums of the written values, per CTA and epilogue warp, go to
+  //   colsum_part[(cta*4 + warp) * N + n]   (colsum_part != null, N <= 256;
+  //   the caller zero-fills kColsumRows x N and sums all rows)
   __nv_bfloat16 *out16 = nullptr;
   int64_t ld16 = 0;
   const float *row_scale = nullptr;

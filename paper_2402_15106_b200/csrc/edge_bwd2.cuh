@@ -1,0 +1,487 @@
+// edge_bwd2.cuh - pipelined, warp-specialised fused edge kernel (backward,
+// step B3 of layer_bf16_bwd.cu).  Per tile of whole rows (edge_fwd2.cuh
+// tiling): recompute a1, h on tcgen05; per row i of the tile
+//   dH^T = dS_i V_seg^T   (M = kappa halves, N = the row's slots, K = c)
+//   U    = H dS_i         (M = 128 slots, N = D, K = kappa)
+// then  dz2 = dH * [h > 0]  -> dZ2 (global, bf16),  u_p = U + dS_i[k] -> U
+// (global, bf16), a1 -> A1 (global, bf16) and per-CTA db2 partial sums.
+//
+// Roles (16 warps):
+//   loader (warps 0,2)  : tile walker, e / v row gathers (register staged)
+//   TMA    (warp 3)     : lane 0 streams W2 K-blocks (2-slot ring), lane 16
+//                         streams dS_i tiles (2-slot ring)
+//   MMA    (warp 1)     : tcgen05 issue
+//   EPI_A  (warps 4-11) : a1, h epilogues (+ h > 0 bitmask)
+//   EPI_B  (warps 12-15): a1 copy-out (coalesced rows), U and dz2 epilogues
+// TMEM: columns 0..255 hold z1 / z2, then U (row g at g*D); columns 256..511
+// hold dH^T (kappa half h at 256 + h*128 + slot).  EPI_B releases the U
+// columns first, so MMA1/epi1 of the next tile overlap the dz2 epilogue.
+#pragma once
+#include "edge_fwd2.cuh"
+
+namespace dsmpnn {
+
+struct MiscB2 {
+  TileDesc2 desc[2];
+  uint64_t e_full[2], desc_free[2];
+  uint64_t e_empty, v_full, v_empty, d1_full, a1_ready, a1_copied, d2_full, h_ready, s_full, u_free, dh_free;
+  uint64_t ah_free, w2_full[2], w2_empty[2], ds_full[2], ds_empty[2];
+  int64_t cur_row, row_end;
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ void load16(const float *__restrict__ p, float (&o)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 t = __ldg(reinterpret_cast<const float4 *>(p) + q);
+    o[4 * q] = t.x;
+    o[4 * q + 1] = t.y;
+    o[4 * q + 2] = t.z;
+    o[4 * q + 3] = t.w;
+  }
+}
+
+template <int D>
+struct EB2 {
+  static constexpr int NMAX = D == 64 ? 2 : 4;
+  static constexpr int W2BLK = KH * 64 * 2;        // 32 KB
+  static constexpr int AH_BYTES = 128 * KH * 2;    // 64 KB
+  static constexpr int DS_BYTES = KH * D * 2;      // 32 / 16 KB
+  static constexpr int V_BYTES = 128 * D * 2;
+  static constexpr int W1_BYTES = KH * 32;
+  static constexpr int E_BYTES = 128 * 32;
+  static constexpr int MASK_BYTES = 128 * (KH / 32) * 4;  // [slot][kappa/32] bit words
+  static constexpr int OFF_W2 = 0;
+  static constexpr int OFF_AH = OFF_W2 + 2 * W2BLK;
+  static constexpr int OFF_DS = OFF_AH + AH_BYTES;
+  static constexpr int OFF_V = OFF_DS + 2 * DS_BYTES;
+  static constexpr int OFF_W1 = OFF_V + V_BYTES;
+  static constexpr int OFF_E = OFF_W1 + W1_BYTES;
+  static constexpr int OFF_MASK = OFF_E + E_BYTES;
+  static constexpr int OFF_MISC = OFF_MASK + MASK_BYTES;
+  static constexpr int SMEM = OFF_MISC + (int)sizeof(MiscB2) + 1024;
+  static_assert(SMEM <= 232448, "edge_bwd2: shared memory budget");
+  static constexpr uint32_t ROWB = D * 2;
+  static constexpr uint32_t SWZ = D == 64 ? tc::kSw128 : tc::kSw64;
+};
+
+template <int D>
+__global__ void __launch_bounds__(512, 1)
+    edge_bwd2_kernel(const __grid_constant__ CUtensorMap tW2, const __grid_constant__ CUtensorMap tDS,
+                     const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
+                     const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rb, int64_t re,
+                     int64_t eb, int64_t ee, Packed pw, const float *__restrict__ b1, const float *__restrict__ b2,
+                     const __nv_bfloat16 *__restrict__ dS, __nv_bfloat16 *__restrict__ A1g,
+                     __nv_bfloat16 *__restrict__ dZ2g, __nv_bfloat16 *__restrict__ Ug, float *__restrict__ db2_part) {
+  using C = EB2<D>;
+  constexpr int NMAX = C::NMAX;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sDS = sm + C::OFF_DS, *sV = sm + C::OFF_V,
+          *sW1 = sm + C::OFF_W1, *sE = sm + C::OFF_E;
+  uint32_t *sMask = reinterpret_cast<uint32_t *>(sm + C::OFF_MASK);
+  MiscB2 *m = reinterpret_cast<MiscB2 *>(sm + C::OFF_MISC);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---------------------------------------------------------------- setup
+  if (tid == 0) {
+    int64_t E = ee - eb;
+    int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
+    int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
+    auto lb = [&](int64_t t) {
+      int64_t lo = rb, hi = re;
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] < t) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
+    m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&m->e_full[b], 64);
+      tc::mbar_init(&m->desc_free[b], 1 + 8 + 4 + 2);  // MMA, every epilogue warp, TMA-W2, TMA-dS
+      tc::mbar_init(&m->w2_full[b], 1);
+      tc::mbar_init(&m->w2_empty[b], 1);
+      tc::mbar_init(&m->ds_full[b], 1);
+      tc::mbar_init(&m->ds_empty[b], 1);
+    }
+    tc::mbar_init(&m->e_empty, 1);
+    tc::mbar_init(&m->v_full, 64);
+    tc::mbar_init(&m->v_empty, 1);
+    tc::mbar_init(&m->d1_full, 1);
+    tc::mbar_init(&m->a1_ready, 256);
+    tc::mbar_init(&m->a1_copied, 128);
+    tc::mbar_init(&m->d2_full, 1);
+    tc::mbar_init(&m->h_ready, 256);
+    tc::mbar_init(&m->s_full, 1);
+    tc::mbar_init(&m->u_free, 128);
+    tc::mbar_init(&m->dh_free, 128);
+    tc::mbar_init(&m->ah_free, 1);
+    tc::fence_mbar_init();
+    tc::tma_prefetch(&tW2);
+    tc::tma_prefetch(&tDS);
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&m->tmem);
+  {
+    const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
+    for (int q = tid; q < KH * 2; q += 512) {
+      int r = q / 2, u = q % 2;
+      *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
+    }
+  }
+  tc::fence_async_shared();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = m->tmem;
+
+  if (warp == 0 || warp == 2) {
+    // ============================================================ loader
+    const int li = warp == 0 ? lane : 32 + lane;  // 0..63
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      TileDesc2 *dsc = &m->desc[b];
+      if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
+      if (warp == 0) walk_tile<NMAX>(m, dsc, row_ptr, lane);
+      tc::named_sync(1, 64);
+      const int nn = dsc->nnodes;
+      for (int s = li; s < 128; s += 64) {
+        int32_t pe = -1;
+        for (int g = 0; g < nn; ++g) {
+          int o = s - dsc->slot0[g];
+          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(dsc->ebase[g] + o);
+        }
+        dsc->slot_edge[s] = pe;
+      }
+      tc::named_sync(1, 64);
+      if (!dsc->more) {
+        tc::mbar_arrive(&m->e_full[b]);
+        break;
+      }
+      constexpr int CH = D / 8;
+      constexpr int NE = 256 / 64, NV = (128 * CH) / 64;
+      uint4 ev[NE], vv[NV];
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int q = li + 64 * k;
+        const int pe = dsc->slot_edge[q >> 1];
+        ev[k] = pe >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe * 16) + (q & 1))
+                        : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int q = li + 64 * k;
+        const int pe = dsc->slot_edge[q / CH];
+        vv[k] = pe >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)__ldg(col + pe) * D) + (q % CH))
+                        : make_uint4(0, 0, 0, 0);
+      }
+      if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int q = li + 64 * k;
+        *reinterpret_cast<uint4 *>(sE + il_off(q >> 1, q & 1)) = ev[k];
+      }
+      tc::fence_async_shared();
+      tc::mbar_arrive(&m->e_full[b]);
+      if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int q = li + 64 * k;
+        *reinterpret_cast<uint4 *>(sV + v_off<D>(q / CH, q % CH)) = vv[k];
+      }
+      tc::fence_async_shared();
+      tc::mbar_arrive(&m->v_full);
+    }
+  } else if (warp == 3) {
+    // ============================================================ TMA producers
+    if (lane == 0) {  // W2 K-blocks, 4 per tile, 2-slot ring
+      uint32_t q = 0;
+      for (uint32_t t = 0;; ++t) {
+        const int b = t & 1;
+        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+        if (!m->desc[b].more) break;
+        for (int j = 0; j < 4; ++j, ++q) {
+          const uint32_t s = q & 1, r = q >> 1;
+          if (r > 0) tc::mbar_wait(&m->w2_empty[s], (r - 1) & 1);
+          tc::mbar_expect_tx(&m->w2_full[s], C::W2BLK);
+          tc::tma_load_2d(sW2 + s * C::W2BLK, &tW2, &m->w2_full[s], j * 64, 0);
+        }
+        tc::mbar_arrive(&m->desc_free[b]);
+      }
+    } else if (lane == 16) {  // dS_i tiles, one per row, 2-slot ring
+      uint32_t q = 0;
+      for (uint32_t t = 0;; ++t) {
+        const int b = t & 1;
+        const TileDesc2 *dsc = &m->desc[b];
+        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+        if (!dsc->more) break;
+        for (int g = 0; g < dsc->nnodes; ++g, ++q) {
+          const uint32_t s = q & 1, r = q >> 1;
+          if (r > 0) tc::mbar_wait(&m->ds_empty[s], (r - 1) & 1);
+          tc::mbar_expect_tx(&m->ds_full[s], C::DS_BYTES);
+          tc::tma_load_2d(sDS + s * C::DS_BYTES, &tDS, &m->ds_full[s], 0, (int32_t)(dsc->node[g] * (KH + 1)));
+        }
+        tc::mbar_arrive(&m->desc_free[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // =============================================================== MMA
+    if (lane == 0) {
+      const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aDS = tc::smem_u32(sDS),
+                     aV = tc::smem_u32(sV), aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
+      constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
+      constexpr uint32_t IDESC_U = tc::idesc_bf16(128, D, false, true);
+      uint32_t w2q = 0, dsq = 0;
+      for (uint32_t t = 0;; ++t) {
+        const int b = t & 1;
+        const uint32_t p1 = t & 1;
+        const TileDesc2 *dsc = &m->desc[b];
+        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+        if (!dsc->more) break;
+        if (t >= 1) tc::mbar_wait(&m->u_free, (t - 1) & 1);  // columns 0..255 drained
+        tc::tc_fence_after();
+        // MMA1: z1 = E W1^T
+        tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone),
+                        IDESC_MLP, 0u);
+        tc::mma_commit(&m->d1_full);
+        tc::mma_commit(&m->e_empty);
+        // MMA2: z2 = a1 W2^T  (W2 streamed by K block)
+        tc::mbar_wait(&m->a1_ready, p1);
+        tc::tc_fence_after();
+        for (int j = 0; j < 4; ++j, ++w2q) {
+          const uint32_t s = w2q & 1;
+          tc::mbar_wait(&m->w2_full[s], (w2q >> 1) & 1);
+          tc::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            uint64_t ad = tc::sdesc(aAH + j * (128 * 128) + kk * 32, 16, 1024, tc::kSw128);
+            uint64_t bd = tc::sdesc(aW2 + s * C::W2BLK + kk * 32, 16, 1024, tc::kSw128);
+            tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc::mma_commit(&m->w2_empty[s]);
+        }
+        tc::mma_commit(&m->d2_full);
+        // per row: dH^T (columns 256 + h*128 + slot) and U (columns g*D)
+        tc::mbar_wait(&m->v_full, p1);
+        tc::mbar_wait(&m->h_ready, p1);
+        if (t >= 1) tc::mbar_wait(&m->dh_free, (t - 1) & 1);
+        tc::tc_fence_after();
+        const int nn = dsc->nnodes;
+        for (int g = 0; g < nn; ++g, ++dsq) {
+          const uint32_t s = dsq & 1;
+          tc::mbar_wait(&m->ds_full[s], (dsq >> 1) & 1);
+          tc::tc_fence_after();
+          const uint32_t ds = aDS + s * C::DS_BYTES;
+          const int s0 = dsc->slot0[g];
+          const int ns = (dsc->deg[g] + 15) & ~15;
+          const uint32_t idesc_h = tc::idesc_bf16(128, ns, false, false);
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              uint64_t ad = tc::sdesc(ds + h * 128 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
+              uint64_t bd = tc::sdesc(aV + (s0 / 8) * 8 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
+              tc::mma_bf16_ss(tmem + 256 + h * 128 + s0, ad, bd, idesc_h, kk > 0 ? 1u : 0u);
+            }
+          }
+#pragma unroll
+          for (int kk = 0; kk < KH / 16; ++kk) {
+            uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
+            uint64_t bd = tc::sdesc(ds + kk * 16 * C::ROWB, 64 * C::ROWB, 8 * C::ROWB, C::SWZ);
+            tc::mma_bf16_ss(tmem + g * D, ad, bd, IDESC_U, kk > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&m->ds_empty[s]);
+        }
+        tc::mma_commit(&m->s_full);
+        tc::mma_commit(&m->v_empty);
+        tc::mma_commit(&m->ah_free);
+        tc::mbar_arrive(&m->desc_free[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 12) {
+    // ============================================================= EPI_A
+    const int grp = warp & 3, cg = (warp - 4) >> 2;
+    const int erow = grp * 32 + lane;
+    const uint32_t r = tmem + ((uint32_t)(grp * 32) << 16);
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      const uint32_t p1 = t & 1;
+      tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+      if (!m->desc[b].more) break;
+      tc::mbar_wait(&m->d1_full, p1);
+      if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
+      tc::tc_fence_after();
+      // a1 = relu(z1 + b1) -> AH  (group cg: columns 128*cg ..)
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c0 = cg * 128 + cc * 16;
+        uint32_t x[16];
+        float bb[16];
+        tc::tmem_ld16(r + c0, x);
+        load16(b1 + c0, bb);  // warp-uniform address: one broadcast transaction per 16 B
+        tc::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + bb[2 * q], 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + bb[2 * q + 1], 0.f));
+        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
+        const int ch = (c0 % 64) / 8;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tc::fence_async_shared();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->a1_ready);
+      // h = relu(z2 + b2) -> AH (after MMA2 and the a1 copy-out), + [h > 0] bits
+      tc::mbar_wait(&m->d2_full, p1);
+      tc::mbar_wait(&m->a1_copied, p1);
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c0 = cg * 128 + cc * 16;
+        uint32_t x[16];
+        float bb[16];
+        tc::tmem_ld16(r + c0, x);
+        load16(b2 + c0, bb);
+        tc::tmem_ld_wait();
+        uint32_t pk[8], bits = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float h0 = fmaxf(__uint_as_float(x[2 * q]) + bb[2 * q], 0.f);
+          const float h1 = fmaxf(__uint_as_float(x[2 * q + 1]) + bb[2 * q + 1], 0.f);
+          pk[q] = tc::pack_bf16(h0, h1);
+          bits |= (h0 > 0.f ? 1u : 0u) << (2 * q);
+          bits |= (h1 > 0.f ? 1u : 0u) << (2 * q + 1);
+        }
+        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
+        const int ch = (c0 % 64) / 8;
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        // 16 bits per chunk -> half of word (c0 / 32) of this slot
+        reinterpret_cast<uint16_t *>(sMask)[erow * (KH / 16) + c0 / 16] = (uint16_t)bits;
+      }
+      tc::fence_async_shared();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->h_ready);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+    }
+  } else {
+    // ============================================================= EPI_B
+    const int grp = warp & 3;
+    const uint32_t lane_off = (uint32_t)(grp * 32) << 16;
+    float db2_lo = 0.f, db2_hi = 0.f;  // kappa = 32*grp + lane, and + 128
+    for (uint32_t t = 0;; ++t) {
+      const int b = t & 1;
+      const uint32_t p1 = t & 1;
+      const TileDesc2 *dsc = &m->desc[b];
+      tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+      if (!dsc->more) break;
+      // a1 rows -> A1 (one 512-byte row per warp instruction)
+      tc::mbar_wait(&m->a1_ready, p1);
+      for (int s = grp; s < 128; s += 4) {
+        const int p = dsc->slot_edge[s];
+        if (p < 0) continue;
+        const int j = lane >> 3, c = lane & 7;
+        const uint4 x = *reinterpret_cast<const uint4 *>(sAH + j * (128 * 128) + tc::sw128_off(s, c));
+        reinterpret_cast<uint4 *>(A1g + (int64_t)p * KH)[lane] = x;
+      }
+      tc::mbar_arrive(&m->a1_copied);
+      // dH / U ready (h_ready: the [h > 0] bits written by EPI_A are visible)
+      tc::mbar_wait(&m->h_ready, p1);
+      tc::mbar_wait(&m->s_full, p1);
+      tc::tc_fence_after();
+      const int nn = dsc->nnodes;
+      // U part (thread <-> slot row): u_p = U[slot] + dS_i[k]
+      {
+        const int s = grp * 32 + lane;
+        const int p = dsc->slot_edge[s];
+        for (int g = 0; g < nn; ++g) {
+          const bool mine = p >= 0 && s >= dsc->slot0[g] && s < dsc->slot0[g] + dsc->deg[g];
+          const __nv_bfloat16 *brow = dS + (dsc->node[g] * (KH + 1) + KH) * D;
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t x[16];
+            tc::tmem_ld16(tmem + lane_off + g * D + c0, x);
+            tc::tmem_ld_wait();
+            if (mine) {
+              const uint4 bb0 = __ldg(reinterpret_cast<const uint4 *>(brow + c0));
+              const uint4 bb1 = __ldg(reinterpret_cast<const uint4 *>(brow + c0 + 8));
+              const __nv_bfloat16 *bv0 = reinterpret_cast<const __nv_bfloat16 *>(&bb0);
+              const __nv_bfloat16 *bv1 = reinterpret_cast<const __nv_bfloat16 *>(&bb1);
+              uint32_t pk[8];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                pk[q] = tc::pack_bf16(__uint_as_float(x[2 * q]) + __bfloat162float(bv0[2 * q]),
+                                      __uint_as_float(x[2 * q + 1]) + __bfloat162float(bv0[2 * q + 1]));
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                pk[4 + q] = tc::pack_bf16(__uint_as_float(x[8 + 2 * q]) + __bfloat162float(bv1[2 * q]),
+                                          __uint_as_float(x[8 + 2 * q + 1]) + __bfloat162float(bv1[2 * q + 1]));
+              uint4 *dst = reinterpret_cast<uint4 *>(Ug + (int64_t)p * D + c0);
+              dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->u_free);
+      // dz2 part (thread <-> kappa): lane pairs exchange so every 4-byte store
+      // of the warp covers 64 contiguous bytes of two dZ2 rows
+      const bool odd = lane & 1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kap = 128 * h + grp * 32 + lane;
+        float acc = 0.f;
+        for (int g = 0; g < nn; ++g) {
+          const int s0 = dsc->slot0[g];
+          const int ns = (dsc->deg[g] + 15) & ~15;
+          for (int c0 = 0; c0 < ns; c0 += 16) {
+            uint32_t x[16];
+            tc::tmem_ld16(tmem + lane_off + 256 + h * 128 + s0 + c0, x);
+            tc::tmem_ld_wait();
+            float dz[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int s = s0 + c0 + j;
+              const uint32_t w = sMask[s * (KH / 32) + (kap >> 5)];
+              dz[j] = ((w >> (kap & 31)) & 1u) ? __uint_as_float(x[j]) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              // even lane stores slot (c0 + 2q) for kappa pair, odd lane slot (c0 + 2q + 1)
+              const float mine = odd ? dz[2 * q + 1] : dz[2 * q];
+              const float give = odd ? dz[2 * q] : dz[2 * q + 1];
+              const float other = __shfl_xor_sync(0xffffffffu, give, 1);
+              const int s = s0 + c0 + 2 * q + (odd ? 1 : 0);
+              const int p = dsc->slot_edge[s];
+              const __nv_bfloat162 pr = odd ? __floats2bfloat162_rn(other, mine) : __floats2bfloat162_rn(mine, other);
+              if (p >= 0)
+                asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(dZ2g + (int64_t)p * KH + (kap & ~1)),
+                             "r"(*reinterpret_cast<const uint32_t *>(&pr))
+                             : "memory");
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc += dz[j];  // pad slots hold dH = 0 (zero V rows)
+          }
+        }
+        if (h == 0) db2_lo += acc; else db2_hi += acc;
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&m->dh_free);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+    }
+    db2_part[(int64_t)blockIdx.x * KH + grp * 32 + lane] = db2_lo;
+    db2_part[(int64_t)blockIdx.x * KH + 128 + grp * 32 + lane] = db2_hi;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace dsmpnn

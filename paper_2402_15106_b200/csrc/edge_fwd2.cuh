@@ -59,8 +59,8 @@ struct EF2 {
 
 // walker: next tile of whole rows, executed by one full warp: the lanes fetch
 // 32 consecutive row_ptr entries in one round trip, lane 0 packs the rows.
-template <int NMAX>
-__device__ __forceinline__ void walk_tile(Misc2 *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr, int lane) {
+template <int NMAX, class MiscT>
+__device__ __forceinline__ void walk_tile(MiscT *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr, int lane) {
   int used = 0, nn = 0;
   int64_t cur = m->cur_row;
   const int64_t end = m->row_end;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(512, 1)
 
       tc::mbar_init(&m->d1_full[b], 1);
       tc::mbar_init(&m->region_free[b], 4);
-      tc::mbar_init(&m->desc_free[b], 3);
+      tc::mbar_init(&m->desc_free[b], 1 + 8 + 4);  // MMA + every epilogue warp
       tc::mbar_init(&m->d2_full[b], 1);
       tc::mbar_init(&m->h_ready[b], 256);
     }
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(512, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready[1]);
       __syncwarp();
-      if (warp == 4 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   } else {
     // ============================================================= EPI_B
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(512, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&m->region_free[b]);
-      if (warp == 12 && lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   }
   tc::tc_fence_before();

@@ -22,6 +22,7 @@
 #include "simt.cuh"
 #include "tc.cuh"
 #include "tgemm.cuh"
+#include "edge_bwd2.cuh"
 
 namespace dsmpnn {
 
@@ -79,315 +80,7 @@ __global__ void add_cols_kernel(const float *__restrict__ full, int64_t rows, in
 }
 
 // ---------------------------------------------------------- B3 edge kernel
-template <int D>
-struct EB {
-  static constexpr int W2BLK = KH * 64 * 2;       // one 64-wide K block of W2: 32 KB
-  static constexpr int AH_BYTES = 128 * KH * 2;   // 64 KB
-  static constexpr int V_BYTES = 128 * D * 2;
-  static constexpr int DS_BYTES = KH * D * 2;     // 32 KB / 16 KB
-  static constexpr int W1_BYTES = KH * 32;
-  static constexpr int E_BYTES = 128 * 32;
-  static constexpr int OFF_W2 = 0;                // 2-slot ring
-  static constexpr int OFF_AH = OFF_W2 + 2 * W2BLK;
-  static constexpr int OFF_DS = OFF_AH + AH_BYTES;
-  static constexpr int OFF_V = OFF_DS + DS_BYTES;
-  static constexpr int OFF_W1 = OFF_V + V_BYTES;
-  static constexpr int OFF_E = OFF_W1 + W1_BYTES;
-  static constexpr int OFF_MISC = OFF_E + E_BYTES;
-  static constexpr int SMEM = OFF_MISC + 2048 + 1024;
-  static constexpr uint32_t ROWB = D * 2;          // bytes per dS / V smem row
-  static constexpr uint32_t SWZ = D == 64 ? tc::kSw128 : tc::kSw64;
-};
-
-struct BwdMisc {
-  uint64_t w2_full[2], w2_empty[2], ds_full;
-  uint32_t w2_issued, w2_used;  // W2 block loads issued / consumed (thread 0 only)
-};
-
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    edge_bwd_kernel(const __grid_constant__ CUtensorMap tW2, const __grid_constant__ CUtensorMap tDS,
-                    const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
-                    const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rb, int64_t re,
-                    int64_t eb, int64_t ee, Packed pw, const float *__restrict__ b1, const float *__restrict__ b2,
-                    const __nv_bfloat16 *__restrict__ dS, __nv_bfloat16 *__restrict__ A1g,
-                    __nv_bfloat16 *__restrict__ dZ2g, float *__restrict__ Ug, float *__restrict__ db2_part) {
-  using C = EB<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space (LDS/STS)
-  uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sDS = sm + C::OFF_DS, *sV = sm + C::OFF_V,
-          *sW1 = sm + C::OFF_W1, *sE = sm + C::OFF_E;
-  EdgeMisc *m = reinterpret_cast<EdgeMisc *>(sm + C::OFF_MISC);
-  BwdMisc *bm = reinterpret_cast<BwdMisc *>(sm + C::OFF_MISC + 1536);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (tid == 0) {
-    int64_t E = ee - eb;
-    int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
-    int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
-    auto lb = [&](int64_t t) {
-      int64_t lo = rb, hi = re;
-      while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (row_ptr[mid] < t) lo = mid + 1; else hi = mid;
-      }
-      return lo;
-    };
-    m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
-    m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
-    m->cur_off = 0;
-    m->node_ctr = 0;
-    tc::mbar_init(&m->bar, 1);
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&bm->w2_full[s], 1);
-      tc::mbar_init(&bm->w2_empty[s], 1);
-    }
-    tc::mbar_init(&bm->ds_full, 1);
-    bm->w2_issued = 0;
-    bm->w2_used = 0;
-    tc::fence_mbar_init();
-    tc::tma_prefetch(&tW2);
-    tc::tma_prefetch(&tDS);
-  }
-  if (warp == 0) tc::tmem_alloc<512>(&m->tmem);
-  {
-    const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
-    for (int q = tid; q < KH * 2; q += 256) {
-      int r = q / 2, u = q % 2;
-      *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
-    }
-  }
-  tc::fence_async_shared();
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = m->tmem;
-  uint32_t phase = 0, ds_phase = 0;
-
-  const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aDS = tc::smem_u32(sDS), aV = tc::smem_u32(sV),
-                 aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
-  constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
-  constexpr uint32_t IDESC_U = tc::idesc_bf16(128, D, false, true);
-  const bool epi = warp >= 4;
-  const int erow = tid - 128;
-  const uint32_t lane_base = epi ? ((uint32_t)(32 * (warp - 4)) << 16) : 0u;
-  float db2_acc0 = 0.f, db2_acc1 = 0.f;  // kappa = erow, 128 + erow
-
-  auto wait_mma = [&]() {
-    tc::mbar_wait(&m->bar, phase & 1);
-    phase++;
-    tc::tc_fence_after();
-  };
-  // thread 0: issue the TMA of the next W2 K-block into the ring
-  auto w2_issue = [&]() {
-    uint32_t q = bm->w2_issued;
-    uint32_t s = q & 1, r = q >> 1;
-    if (r > 0) tc::mbar_wait(&bm->w2_empty[s], (r - 1) & 1);
-    tc::mbar_expect_tx(&bm->w2_full[s], C::W2BLK);
-    tc::tma_load_2d(sW2 + s * C::W2BLK, &tW2, &bm->w2_full[s], (int32_t)((q & 3) * 64), 0);
-    bm->w2_issued = q + 1;
-  };
-
-  for (;;) {
-    if (tid == 0) {
-      build_tile(m, row_ptr);
-      if (m->more) {  // prefetch W2 blocks 0 and 1 of this tile
-        w2_issue();
-        w2_issue();
-      }
-    }
-    __syncthreads();
-    if (!m->more) break;
-
-    {  // gather E and V rows of the slots
-      int s = tid >> 1, u = tid & 1;
-      int p = m->slot_edge[s];
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (p >= 0) val = reinterpret_cast<const uint4 *>(e16 + (int64_t)p * 16)[u];
-      *reinterpret_cast<uint4 *>(sE + il_off(s, u)) = val;
-      constexpr int CH = D / 8;
-      for (int q = tid; q < 128 * CH; q += 256) {
-        int sl = q / CH, c = q % CH;
-        int pe = m->slot_edge[sl];
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (pe >= 0) x = reinterpret_cast<const uint4 *>(v + (int64_t)col[pe] * D)[c];
-        *reinterpret_cast<uint4 *>(sV + v_off<D>(sl, c)) = x;
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- MMA1 + epilogue 1: a1 -> AH and -> A1 (global, for the dW2 / dz1 GEMMs)
-    if (tid == 0) {
-      tc::tc_fence_after();
-      tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC_MLP,
-                      0u);
-      tc::mma_commit(&m->bar);
-    }
-    wait_mma();
-    if (epi) {
-      const int p = m->slot_edge[erow];
-#pragma unroll 1
-      for (int c0 = 0; c0 < KH; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(tmem + lane_base + c0, r);
-        tc::tmem_ld_wait();
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b1 + c0 + 2 * j), 0.f),
-                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b1 + c0 + 2 * j + 1), 0.f));
-        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
-        int ch = (c0 % 64) / 8;
-        uint4 x0 = make_uint4(pk[0], pk[1], pk[2], pk[3]), x1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = x0;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = x1;
-        if (p >= 0) {
-          uint4 *g = reinterpret_cast<uint4 *>(A1g + (int64_t)p * KH + c0);
-          g[0] = x0;
-          g[1] = x1;
-        }
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- MMA2 with W2 streamed through the 2-slot ring
-    if (tid == 0) {
-      tc::tc_fence_after();
-      for (int j = 0; j < 4; ++j) {
-        uint32_t q = bm->w2_used;
-        uint32_t s = q & 1;
-        tc::mbar_wait(&bm->w2_full[s], (q >> 1) & 1);
-        tc::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          uint64_t ad = tc::sdesc(aAH + j * (128 * 128) + kk * 32, 16, 1024, tc::kSw128);
-          uint64_t bd = tc::sdesc(aW2 + s * C::W2BLK + kk * 32, 16, 1024, tc::kSw128);
-          tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(&bm->w2_empty[s]);
-        bm->w2_used = q + 1;
-        // blocks 2, 3 reuse the slots of 0, 1; issued one block late so the
-        // tensor pipe still holds queued MMAs while we wait for the slot
-        if (j == 1 || j == 2) w2_issue();
-      }
-      tc::mma_commit(&m->bar);
-    }
-    wait_mma();
-    if (epi) {  // h = relu(z2 + b2) -> AH
-#pragma unroll 1
-      for (int c0 = 0; c0 < KH; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(tmem + lane_base + c0, r);
-        tc::tmem_ld_wait();
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b2 + c0 + 2 * j), 0.f),
-                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b2 + c0 + 2 * j + 1), 0.f));
-        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
-        int ch = (c0 % 64) / 8;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- per row segment: dH^T = dS_i V_seg^T and U = H dS_i
-    const int nseg = m->nseg;
-    for (int g = 0; g < nseg; ++g) {
-      const Seg sg = m->seg[g];
-      if (tid == 0) {
-        tc::mbar_expect_tx(&bm->ds_full, C::DS_BYTES);
-        tc::tma_load_2d(sDS, &tDS, &bm->ds_full, 0, (int32_t)(sg.node * (KH + 1)));
-        tc::mbar_wait(&bm->ds_full, ds_phase & 1);
-        tc::tc_fence_after();
-        const uint32_t idesc_h = tc::idesc_bf16(128, sg.nslots, false, false);
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            uint64_t ad = tc::sdesc(aDS + h * 128 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
-            uint64_t bd = tc::sdesc(aV + (sg.slot0 / 8) * 8 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
-            tc::mma_bf16_ss(tmem + h * 128, ad, bd, idesc_h, kk > 0 ? 1u : 0u);
-          }
-        }
-#pragma unroll
-        for (int kk = 0; kk < KH / 16; ++kk) {
-          uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
-          uint64_t bd = tc::sdesc(aDS + kk * 16 * C::ROWB, 64 * C::ROWB, 8 * C::ROWB, C::SWZ);
-          tc::mma_bf16_ss(tmem + KH, ad, bd, IDESC_U, kk > 0 ? 1u : 0u);
-        }
-        tc::mma_commit(&m->bar);
-      }
-      ds_phase++;
-      wait_mma();
-      if (epi) {
-        // dz2[slot][kap] = dH^T[kap][slot] * [h[slot][kap] > 0]  (thread <-> kap)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kap = 128 * h + erow;
-          const uint8_t *hblk = sAH + (kap / 64) * (128 * 128);
-          const int hch = (kap % 64) / 8, hel = kap % 8;
-          float acc = 0.f;
-#pragma unroll 1
-          for (int c0 = 0; c0 < sg.nslots; c0 += 16) {
-            uint32_t r[16];
-            tc::tmem_ld16(tmem + lane_base + h * 128 + c0, r);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int s = sg.slot0 + c0 + j;
-              const int p = m->slot_edge[s];
-              const __nv_bfloat16 hv =
-                  *reinterpret_cast<const __nv_bfloat16 *>(hblk + tc::sw128_off(s, hch) + hel * 2);
-              float dz = __bfloat162float(hv) > 0.f ? __uint_as_float(r[j]) : 0.f;
-              __nv_bfloat16 dzb = __float2bfloat16_rn(dz);
-              if (p >= 0) {
-                dZ2g[(int64_t)p * KH + kap] = dzb;
-                acc += __bfloat162float(dzb);
-              }
-            }
-          }
-          if (h == 0) db2_acc0 += acc; else db2_acc1 += acc;
-        }
-        // u_p[c] = U[slot][c] + dS_i[k][c]  (thread <-> slot)
-        const int s = erow;
-        const int p = m->slot_edge[s];
-        const bool mine = s >= sg.slot0 && s < sg.slot0 + sg.nslots && p >= 0;
-        const __nv_bfloat16 *brow = dS + (sg.node * (KH + 1) + KH) * D;
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 16) {
-          uint32_t r[16];
-          tc::tmem_ld16(tmem + lane_base + KH + c0, r);  // warp-collective: executed by all lanes
-          tc::tmem_ld_wait();
-          if (mine) {
-            float4 *dst = reinterpret_cast<float4 *>(Ug + (int64_t)p * D + c0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(__uint_as_float(r[4 * j]) + __bfloat162float(brow[c0 + 4 * j]),
-                                   __uint_as_float(r[4 * j + 1]) + __bfloat162float(brow[c0 + 4 * j + 1]),
-                                   __uint_as_float(r[4 * j + 2]) + __bfloat162float(brow[c0 + 4 * j + 2]),
-                                   __uint_as_float(r[4 * j + 3]) + __bfloat162float(brow[c0 + 4 * j + 3]));
-          }
-        }
-      }
-      tc::tc_fence_before();
-      __syncthreads();
-    }
-  }
-  if (epi) {
-    db2_part[(int64_t)blockIdx.x * KH + erow] = db2_acc0;
-    db2_part[(int64_t)blockIdx.x * KH + 128 + erow] = db2_acc1;
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<512>(tmem);
-}
+// edge_bwd2.cuh (warp-specialised, pipelined)
 
 // ------------------------------------------------------------ workspace
 struct BBwd {
@@ -399,7 +92,7 @@ struct BBwd {
   __nv_bfloat16 *A1;       // [E x k]
   __nv_bfloat16 *dZ2;      // [E x k]
   __nv_bfloat16 *dZ1;      // [E x k]
-  float *U;                // [E x D]
+  __nv_bfloat16 *U;        // [E x D] (bf16)
   float *part;             // split-K partials (max over users)
   float *db2_part;         // [kNumSMs x k]
   float *db1_part;         // [ceil(E/128)*4 x k]
@@ -420,7 +113,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.A1 = c.take<__nv_bfloat16>(E * d.k);
   b.dZ2 = c.take<__nv_bfloat16>(E * d.k);
   b.dZ1 = c.take<__nv_bfloat16>(E * d.k);
-  b.U = c.take<float>(E * D);
+  b.U = c.take<__nv_bfloat16>(E * D);
   b.part = c.take<float>((int64_t)kSplitsW * d.k * d.k);
   b.db2_part = c.take<float>((int64_t)kNumSMs * d.k);
   b.db1_part = c.take<float>((int64_t)kColsumRows * d.k);
@@ -450,7 +143,7 @@ static BFwdView view_fwd(const dsmpnn_layer_desc &d, const void *ws, int64_t n_d
   return f;
 }
 
-__global__ void scatter_csc_f32_kernel(const float *__restrict__ U, const int32_t *__restrict__ perm,
+__global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, const int32_t *__restrict__ perm,
                                        const int64_t *__restrict__ cptr, int64_t n_loc, int di, int64_t eb,
                                        int64_t ee, float *__restrict__ dv) {
   int64_t total = n_loc * di;
@@ -461,7 +154,7 @@ __global__ void scatter_csc_f32_kernel(const float *__restrict__ U, const int32_
     bool any = false;
     for (int64_t q = cptr[j]; q < cptr[j + 1]; ++q) {
       int64_t p = perm[q];
-      if (p >= eb && p < ee) { s += U[p * di + c]; any = true; }
+      if (p >= eb && p < ee) { s += __bfloat162float(U[p * di + c]); any = true; }
     }
     if (any) dv[t] += s;
   }
@@ -479,17 +172,17 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
                                      const __nv_bfloat16 *v, const int64_t *row_ptr, const int32_t *col, int64_t n_dst,
                                      int64_t rb, int64_t re, int64_t eb, int64_t ee, const float *b1, const float *b2,
                                      const BBwd &b, int *grid_out, cudaStream_t s) {
-  using C = EB<D>;
+  using C = EB2<D>;
   CUtensorMap tW2, tDS;
   DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
   DS_TRY(make_tmap_bf16(&tDS, b.dS, D, n_dst * (int64_t)(KH + 1), D, D, KH));
-  auto kern = edge_bwd_kernel<D>;
+  auto kern = edge_bwd2_kernel<D>;
   DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   *grid_out = grid;
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_BWD, s);
-  kern<<<grid, 256, C::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS, b.A1, b.dZ2, b.U,
+  kern<<<grid, 512, C::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS, b.A1, b.dZ2, b.U,
                                   b.db2_part);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
@@ -585,7 +278,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   }
   // B7: dv[j] += sum of u_p over edges with source j (CSC order)
   if (dv) {
-    scatter_csc_f32_kernel<<<grid_of(n_loc * D), 256, 0, s>>>(b.U, perm, cptr, n_loc, D, eb, ee, dv);
+    scatter_csc_bf16_kernel<<<grid_of(n_loc * D), 256, 0, s>>>(b.U, perm, cptr, n_loc, D, eb, ee, dv);
     DS_LAUNCH_CHECK();
   }
   return DSMPNN_OK;

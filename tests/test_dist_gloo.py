@@ -1,0 +1,102 @@
+"""N>1 host-side logic on CPU (gloo, world_size 2): the cross-process halo
+refresh of Alg. 1 line 411 (pipeline.halo_exchange_mixed) and the gradient
+sum of line 418 (HotPath._allreduce_grads), checked against the oracle's
+halo_forward and a plain sum.  Sub-domains are mapped to processes in blocks
+(api.parts_of_process), as bench.py does for --gpus N."""
+import os
+import socket
+import types
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import halo as ohalo
+from oracle import partition as opart
+
+WORLD = 2
+NPARTS = 4
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _plan():
+    g = np.random.default_rng(5)
+    x = g.random((600, 2)).astype(np.float32)
+    gid = np.arange(600, dtype=np.int64) * 7 + 3
+    _, _, _, ranks = opart.plan(x, gid, NPARTS, 0.05, 0.04)
+    vals = []
+    for q, rk in enumerate(ranks):
+        n_loc = len(rk["local_rows"])
+        n_own = rk["n_deep"] + rk["n_near"]
+        v = g.normal(size=(n_loc, 5)).astype(np.float32)
+        v[n_own:] = np.nan  # halo rows: stale until the refresh
+        vals.append(v)
+    return ranks, vals
+
+
+def _worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_2402_15106_b200 import api, pipeline
+        ranks, vals = _plan()
+        mine = api.parts_of_process(NPARTS, WORLD, rank)
+        proc_of = [p // (NPARTS // WORLD) for p in range(NPARTS)]
+        subs = [types.SimpleNamespace(rank=p, nparts=NPARTS, halo_ptr=[int(t) for t in ranks[p]["halo_ptr"]],
+                                      send_ptr=[int(t) for t in ranks[p]["send_ptr"]],
+                                      send_idx=torch.from_numpy(ranks[p]["send_idx"].astype(np.int64)))
+                for p in mine]
+        tv = [torch.from_numpy(vals[p].copy()) for p in mine]
+
+        def gather(src, rows, out):  # test stand-in for the device gather kernel
+            out.copy_(src[rows.long()])
+
+        pipeline.halo_exchange_mixed(subs, tv, None, proc_of, rank, gather=gather)
+        want = ohalo.halo_forward(ranks, vals)
+        ok_halo = all(np.array_equal(t.numpy(), want[p]) for t, p in zip(tv, mine))
+
+        # gradient sum over processes
+        names = api.GNAMES
+        grads = {n: torch.full((3, 2), float(rank + 1) * (i + 1)) for i, n in enumerate(names)}
+        stub = types.SimpleNamespace(grads=grads, group=None)
+        api.HotPath._allreduce_grads(stub)
+        ok_red = all(torch.equal(grads[n], torch.full((3, 2), 3.0 * (i + 1))) for i, n in enumerate(names))
+        q.put((rank, ok_halo, ok_red))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_halo_and_allreduce_world2():
+    from paper_2402_15106_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(WORLD)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for rank, ok_halo, ok_red in sorted(res):
+        assert ok_halo, f"rank {rank}: halo refresh differs from oracle.halo.halo_forward"
+        assert ok_red, f"rank {rank}: gradient all-reduce wrong"
+
+
+def test_halo_plan_has_cross_process_traffic():
+    """The fixture actually exercises the NCCL/gloo leg: some send list crosses
+    the process boundary of the block mapping."""
+    ranks, _ = _plan()
+    per = NPARTS // WORLD
+    cross = sum(int(ranks[p]["send_ptr"][q + 1] - ranks[p]["send_ptr"][q])
+                for p in range(NPARTS) for q in range(NPARTS) if p // per != q // per)
+    assert cross > 0

@@ -7,12 +7,14 @@
 // (global, bf16), a1 -> A1 (global, bf16) and per-CTA db2 partial sums.
 //
 // Roles (16 warps):
-//   loader (warps 0,2)  : tile walker, e / v row gathers (register staged)
+//   loader (warps 0,2)  : tile walker, e / v row gathers (register staged),
+//                         dS_i[k] bias rows
 //   TMA    (warp 3)     : lane 0 streams W2 K-blocks (2-slot ring), lane 16
 //                         streams dS_i tiles (2-slot ring)
 //   MMA    (warp 1)     : tcgen05 issue
-//   EPI_A  (warps 4-11) : a1, h epilogues (+ h > 0 bitmask)
-//   EPI_B  (warps 12-15): a1 copy-out (coalesced rows), U and dz2 epilogues
+//   EPI_A  (warps 4-11) : a1 epilogue + coalesced a1 copy-out (overlaps MMA2),
+//                         h epilogue + [h > 0] bitmask
+//   EPI_B  (warps 12-15): U and dz2 epilogues
 // TMEM: columns 0..255 hold z1 / z2, then U (row g at g*D); columns 256..511
 // hold dH^T (kappa half h at 256 + h*128 + slot).  EPI_B releases the U
 // columns first, so MMA1/epi1 of the next tile overlap the dz2 epilogue.
@@ -21,24 +23,94 @@
 
 namespace dsmpnn {
 
-struct MiscB2 {
-  TileDesc2 desc[2];
-  uint64_t e_full[2], desc_free[2];
-  uint64_t e_empty, v_full, v_empty, d1_full, a1_ready, a1_copied, d2_full, h_ready, s_full, u_free, dh_free;
-  uint64_t ah_free, w2_full[2], w2_empty[2], ds_full[2], ds_empty[2];
-  int64_t cur_row, row_end;
-  uint32_t tmem;
+struct TileDescB {
+  int64_t node[4];
+  int64_t ebase[4];  // row_ptr[node]
+  int32_t slot0[4], deg[4];
+  int32_t nnodes, more;
 };
 
-__device__ __forceinline__ void load16(const float *__restrict__ p, float (&o)[16]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float4 t = __ldg(reinterpret_cast<const float4 *>(p) + q);
-    o[4 * q] = t.x;
-    o[4 * q + 1] = t.y;
-    o[4 * q + 2] = t.z;
-    o[4 * q + 3] = t.w;
+// edge held by tile slot s, or -1 for a padding slot
+__device__ __forceinline__ int32_t slot_edge_of(const TileDescB *d, int nn, int s) {
+  int32_t pe = -1;
+  for (int g = 0; g < nn; ++g) {
+    const int o = s - d->slot0[g];
+    if (o >= 0 && o < d->deg[g]) pe = (int32_t)(d->ebase[g] + o);
   }
+  return pe;
+}
+
+// register copy of a tile's rows (the desc fields are warp-uniform)
+template <int NMAX>
+struct TileRegs {
+  int nn;
+  int s0[NMAX], deg[NMAX];
+  int64_t eb[NMAX];
+  __device__ __forceinline__ void load(const TileDescB *d) {
+    nn = d->nnodes;
+#pragma unroll
+    for (int g = 0; g < NMAX; ++g) {
+      const bool ok = g < nn;
+      s0[g] = ok ? d->slot0[g] : 1 << 20;
+      deg[g] = ok ? d->deg[g] : 0;
+      eb[g] = ok ? d->ebase[g] : 0;
+    }
+  }
+  __device__ __forceinline__ int32_t edge(int s) const {
+    int32_t pe = -1;
+#pragma unroll
+    for (int g = 0; g < NMAX; ++g) {
+      const int o = s - s0[g];
+      if (o >= 0 && o < deg[g]) pe = (int32_t)(eb[g] + o);
+    }
+    return pe;
+  }
+};
+
+// dz2 for NS consecutive slots (one TMEM load, one wait): dz2 = dH * [h > 0];
+// lane pairs (kappa, kappa+1) exchange values so every 4-byte store of the
+// warp covers 64 contiguous bytes of two dZ2 rows.  Returns the lane's sum.
+// [h > 0] bits of slots s .. s+63 (bit j = slot s + j) from the 128 slot bits
+// w[0..3]; shifts and selects only (no register-array indexing)
+__device__ __forceinline__ uint64_t slot_bits(const uint32_t (&w)[4], int s) {
+  const uint64_t q0 = (uint64_t)w[0] | ((uint64_t)w[1] << 32), q1 = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+  if (s == 0) return q0;
+  if (s < 64) return (q0 >> s) | (q1 << (64 - s));
+  return s == 64 ? q1 : q1 >> (s - 64);
+}
+
+// dz2 for NS consecutive slots of one row (one wait): dz2 = dH * [h > 0].
+// Lane pairs (kappa, kappa+1) swap packed bf16 pairs so every 4-byte store
+// of the warp covers 64 contiguous bytes of two dZ2 rows.  Returns the sum
+// of the lane's fp32 dz2 values (db2 partial).
+template <int NS>
+__device__ __forceinline__ float dz2_chunk(uint32_t taddr, uint64_t bits, int kap, int c0, int deg,
+                                           __nv_bfloat16 *__restrict__ dz2_row0) {
+  uint32_t x[NS];
+  if constexpr (NS == 16) {
+    uint32_t (&y)[16] = *reinterpret_cast<uint32_t (*)[16]>(&x[0]);
+    tc::tmem_ld16(taddr, y);
+  } else {
+#pragma unroll
+    for (int u = 0; u < NS / 32; ++u) tc::tmem_ld32(taddr + 32 * u, *reinterpret_cast<uint32_t (*)[32]>(&x[32 * u]));
+  }
+  tc::tmem_ld_wait();
+  const bool odd = kap & 1;
+  const uint32_t sel = odd ? 0x3276u : 0x5410u;  // odd: (partner.hi, own.hi); even: (own.lo, partner.lo)
+  __nv_bfloat16 *dst = dz2_row0 + (int64_t)(c0 + (odd ? 1 : 0)) * KH + (kap & ~1);
+  float acc = 0.f;
+#pragma unroll
+  for (int q = 0; q < NS / 2; ++q) {
+    const uint32_t m0 = 0u - (uint32_t)((bits >> (2 * q)) & 1u), m1 = 0u - (uint32_t)((bits >> (2 * q + 1)) & 1u);
+    const float d0 = __uint_as_float(x[2 * q] & m0), d1 = __uint_as_float(x[2 * q + 1] & m1);
+    acc += d0 + d1;  // padding slots hold dH = 0 (zero V rows)
+    const uint32_t own = tc::pack_bf16(d0, d1);  // (slot 2q, slot 2q+1) of this kappa
+    const uint32_t oth = __shfl_xor_sync(0xffffffffu, own, 1);
+    const uint32_t pr = __byte_perm(own, oth, sel);
+    if (c0 + 2 * q + (odd ? 1 : 0) < deg)
+      asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(dst + (int64_t)(2 * q) * KH), "r"(pr) : "memory");
+  }
+  return acc;
 }
 
 template <int D>
@@ -50,7 +122,7 @@ struct EB2 {
   static constexpr int V_BYTES = 128 * D * 2;
   static constexpr int W1_BYTES = KH * 32;
   static constexpr int E_BYTES = 128 * 32;
-  static constexpr int MASK_BYTES = 128 * (KH / 32) * 4;  // [slot][kappa/32] bit words
+  static constexpr int MASK_BYTES = 4 * KH * 4;  // [slot/32][kappa] words, bit = slot % 32
   static constexpr int OFF_W2 = 0;
   static constexpr int OFF_AH = OFF_W2 + 2 * W2BLK;
   static constexpr int OFF_DS = OFF_AH + AH_BYTES;
@@ -58,8 +130,18 @@ struct EB2 {
   static constexpr int OFF_W1 = OFF_V + V_BYTES;
   static constexpr int OFF_E = OFF_W1 + W1_BYTES;
   static constexpr int OFF_MASK = OFF_E + E_BYTES;
-  static constexpr int OFF_MISC = OFF_MASK + MASK_BYTES;
-  static constexpr int SMEM = OFF_MISC + (int)sizeof(MiscB2) + 1024;
+  static constexpr int OFF_BIAS = OFF_MASK + MASK_BYTES;   // b1[KH], b2[KH] (fp32)
+  static constexpr int OFF_MISC = OFF_BIAS + 2 * KH * 4;
+  struct Misc {
+    TileDescB desc[2];
+    __nv_bfloat16 brow[2][NMAX][D];  // dS_i[k] of the rows of desc[b]
+    uint64_t e_full[2], desc_free[2], w2_full[2], w2_empty[2], ds_full[2], ds_empty[2];
+    uint64_t e_empty, v_full, v_empty, d1_full, a1_ready, d2_full, h_ready, s_full, u_free, dh_free, ah_free;
+    uint64_t mask_read;
+    int64_t cur_row, row_end;
+    uint32_t tmem;
+  };
+  static constexpr int SMEM = OFF_MISC + (int)sizeof(Misc);
   static_assert(SMEM <= 232448, "edge_bwd2: shared memory budget");
   static constexpr uint32_t ROWB = D * 2;
   static constexpr uint32_t SWZ = D == 64 ? tc::kSw128 : tc::kSw64;
@@ -74,17 +156,21 @@ __global__ void __launch_bounds__(512, 1)
                      const __nv_bfloat16 *__restrict__ dS, __nv_bfloat16 *__restrict__ A1g,
                      __nv_bfloat16 *__restrict__ dZ2g, __nv_bfloat16 *__restrict__ Ug, float *__restrict__ db2_part) {
   using C = EB2<D>;
+  using Misc = typename C::Misc;
   constexpr int NMAX = C::NMAX;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  // 1024-byte aligned (SW128 operands); no slack is reserved, so check it
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sm = smem_raw;
   uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sDS = sm + C::OFF_DS, *sV = sm + C::OFF_V,
           *sW1 = sm + C::OFF_W1, *sE = sm + C::OFF_E;
   uint32_t *sMask = reinterpret_cast<uint32_t *>(sm + C::OFF_MASK);
-  MiscB2 *m = reinterpret_cast<MiscB2 *>(sm + C::OFF_MISC);
+  float *sB1 = reinterpret_cast<float *>(sm + C::OFF_BIAS), *sB2 = sB1 + KH;
+  Misc *m = reinterpret_cast<Misc *>(sm + C::OFF_MISC);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---------------------------------------------------------------- setup
   if (tid == 0) {
+    if (tc::smem_u32(smem_raw) & 1023u) __trap();
     int64_t E = ee - eb;
     int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
     int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
@@ -111,9 +197,9 @@ __global__ void __launch_bounds__(512, 1)
     tc::mbar_init(&m->v_empty, 1);
     tc::mbar_init(&m->d1_full, 1);
     tc::mbar_init(&m->a1_ready, 256);
-    tc::mbar_init(&m->a1_copied, 128);
     tc::mbar_init(&m->d2_full, 1);
     tc::mbar_init(&m->h_ready, 256);
+    tc::mbar_init(&m->mask_read, 128);
     tc::mbar_init(&m->s_full, 1);
     tc::mbar_init(&m->u_free, 128);
     tc::mbar_init(&m->dh_free, 128);
@@ -129,6 +215,10 @@ __global__ void __launch_bounds__(512, 1)
       int r = q / 2, u = q % 2;
       *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
     }
+    for (int q = tid; q < KH; q += 512) {
+      sB1[q] = b1[q];
+      sB2[q] = b2[q];
+    }
   }
   tc::fence_async_shared();
   tc::tc_fence_before();
@@ -141,54 +231,56 @@ __global__ void __launch_bounds__(512, 1)
     const int li = warp == 0 ? lane : 32 + lane;  // 0..63
     for (uint32_t t = 0;; ++t) {
       const int b = t & 1;
-      TileDesc2 *dsc = &m->desc[b];
+      TileDescB *dsc = &m->desc[b];
       if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
       if (warp == 0) walk_tile<NMAX>(m, dsc, row_ptr, lane);
       tc::named_sync(1, 64);
       const int nn = dsc->nnodes;
-      for (int s = li; s < 128; s += 64) {
-        int32_t pe = -1;
-        for (int g = 0; g < nn; ++g) {
-          int o = s - dsc->slot0[g];
-          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(dsc->ebase[g] + o);
-        }
-        dsc->slot_edge[s] = pe;
-      }
-      tc::named_sync(1, 64);
       if (!dsc->more) {
         tc::mbar_arrive(&m->e_full[b]);
         break;
       }
       constexpr int CH = D / 8;
-      constexpr int NE = 256 / 64, NV = (128 * CH) / 64;
-      uint4 ev[NE], vv[NV];
+      TileRegs<NMAX> tr;
+      tr.load(dsc);
+      // thread li gathers whole rows of slots li and li + 64: two index loads,
+      // then all row loads in flight at once
+      int32_t pe[2], cj[2];
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int q = li + 64 * k;
-        const int pe = dsc->slot_edge[q >> 1];
-        ev[k] = pe >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe * 16) + (q & 1))
-                        : make_uint4(0, 0, 0, 0);
+      for (int u = 0; u < 2; ++u) pe[u] = tr.edge(li + 64 * u);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) cj[u] = pe[u] >= 0 ? __ldg(col + pe[u]) : -1;
+      uint4 ev[2][2], vv[2][CH];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          ev[u][c] = pe[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe[u] * 16) + c)
+                                : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+          vv[u][c] = cj[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)cj[u] * D) + c)
+                                : make_uint4(0, 0, 0, 0);
       }
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int q = li + 64 * k;
-        const int pe = dsc->slot_edge[q / CH];
-        vv[k] = pe >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)__ldg(col + pe) * D) + (q % CH))
-                        : make_uint4(0, 0, 0, 0);
+      // dS_i[k] rows (the constant term of u_p) for EPI_B
+      for (int q = li; q < nn * CH; q += 64) {
+        const int g = q / CH, c = q % CH;
+        reinterpret_cast<uint4 *>(&m->brow[b][g][0])[c] =
+            __ldg(reinterpret_cast<const uint4 *>(dS + (dsc->node[g] * (KH + 1) + KH) * D) + c);
       }
       if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int q = li + 64 * k;
-        *reinterpret_cast<uint4 *>(sE + il_off(q >> 1, q & 1)) = ev[k];
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) *reinterpret_cast<uint4 *>(sE + il_off(li + 64 * u, c)) = ev[u][c];
       }
       tc::fence_async_shared();
       tc::mbar_arrive(&m->e_full[b]);
       if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int q = li + 64 * k;
-        *reinterpret_cast<uint4 *>(sV + v_off<D>(q / CH, q % CH)) = vv[k];
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) *reinterpret_cast<uint4 *>(sV + v_off<D>(li + 64 * u, c)) = vv[u][c];
       }
       tc::fence_async_shared();
       tc::mbar_arrive(&m->v_full);
@@ -213,7 +305,7 @@ __global__ void __launch_bounds__(512, 1)
       uint32_t q = 0;
       for (uint32_t t = 0;; ++t) {
         const int b = t & 1;
-        const TileDesc2 *dsc = &m->desc[b];
+        const TileDescB *dsc = &m->desc[b];
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!dsc->more) break;
         for (int g = 0; g < dsc->nnodes; ++g, ++q) {
@@ -237,7 +329,7 @@ __global__ void __launch_bounds__(512, 1)
       for (uint32_t t = 0;; ++t) {
         const int b = t & 1;
         const uint32_t p1 = t & 1;
-        const TileDesc2 *dsc = &m->desc[b];
+        const TileDescB *dsc = &m->desc[b];
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!dsc->more) break;
         if (t >= 1) tc::mbar_wait(&m->u_free, (t - 1) & 1);  // columns 0..255 drained
@@ -302,66 +394,91 @@ __global__ void __launch_bounds__(512, 1)
     __syncwarp();
   } else if (warp < 12) {
     // ============================================================= EPI_A
-    const int grp = warp & 3, cg = (warp - 4) >> 2;
+    const int grp = warp & 3, cg = (warp - 4) >> 2, wi = warp - 4;
     const int erow = grp * 32 + lane;
     const uint32_t r = tmem + ((uint32_t)(grp * 32) << 16);
     for (uint32_t t = 0;; ++t) {
       const int b = t & 1;
       const uint32_t p1 = t & 1;
+      const TileDescB *dsc = &m->desc[b];
       tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
-      if (!m->desc[b].more) break;
+      if (!dsc->more) break;
       tc::mbar_wait(&m->d1_full, p1);
       if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
       tc::tc_fence_after();
       // a1 = relu(z1 + b1) -> AH  (group cg: columns 128*cg ..)
 #pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c0 = cg * 128 + cc * 16;
-        uint32_t x[16];
-        float bb[16];
-        tc::tmem_ld16(r + c0, x);
-        load16(b1 + c0, bb);  // warp-uniform address: one broadcast transaction per 16 B
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c0 = cg * 128 + cc * 32;
+        uint32_t x[32];
+        tc::tmem_ld32(r + c0, x);
         tc::tmem_ld_wait();
-        uint32_t pk[8];
+        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + bb[2 * q], 0.f),
-                                fmaxf(__uint_as_float(x[2 * q + 1]) + bb[2 * q + 1], 0.f));
+        for (int q = 0; q < 16; ++q)
+          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + sB1[c0 + 2 * q], 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + sB1[c0 + 2 * q + 1], 0.f));
         uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
         const int ch = (c0 % 64) / 8;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + u)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->a1_ready);
+      // a1 rows -> A1 (one 512-byte row per warp instruction), overlapping MMA2
+      tc::named_sync(2, 256);
+      {
+        TileRegs<NMAX> tr;
+        tr.load(dsc);
+        const int j = lane >> 3, c = lane & 7;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint4 xs[8];
+          int32_t ps[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int s = wi + 8 * (8 * h + k);
+            ps[k] = tr.edge(s);
+            xs[k] = *reinterpret_cast<const uint4 *>(sAH + j * (128 * 128) + tc::sw128_off(s, c));
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (ps[k] >= 0) reinterpret_cast<uint4 *>(A1g + (int64_t)ps[k] * KH)[lane] = xs[k];
+        }
+      }
       // h = relu(z2 + b2) -> AH (after MMA2 and the a1 copy-out), + [h > 0] bits
       tc::mbar_wait(&m->d2_full, p1);
-      tc::mbar_wait(&m->a1_copied, p1);
+      if (t >= 1) tc::mbar_wait(&m->mask_read, (t - 1) & 1);
+      tc::named_sync(2, 256);
       tc::tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c0 = cg * 128 + cc * 16;
-        uint32_t x[16];
-        float bb[16];
-        tc::tmem_ld16(r + c0, x);
-        load16(b2 + c0, bb);
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c0 = cg * 128 + cc * 32;
+        uint32_t x[32];
+        tc::tmem_ld32(r + c0, x);
         tc::tmem_ld_wait();
-        uint32_t pk[8], bits = 0;
+        uint32_t pk[16], bits = 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float h0 = fmaxf(__uint_as_float(x[2 * q]) + bb[2 * q], 0.f);
-          const float h1 = fmaxf(__uint_as_float(x[2 * q + 1]) + bb[2 * q + 1], 0.f);
+        for (int q = 0; q < 16; ++q) {
+          const float h0 = fmaxf(__uint_as_float(x[2 * q]) + sB2[c0 + 2 * q], 0.f);
+          const float h1 = fmaxf(__uint_as_float(x[2 * q + 1]) + sB2[c0 + 2 * q + 1], 0.f);
           pk[q] = tc::pack_bf16(h0, h1);
-          bits |= (h0 > 0.f ? 1u : 0u) << (2 * q);
-          bits |= (h1 > 0.f ? 1u : 0u) << (2 * q + 1);
+          // word for kappa = c0 + j over this warp's 32 slots; lane j keeps it
+          const uint32_t w0 = __ballot_sync(0xffffffffu, h0 > 0.f);
+          const uint32_t w1 = __ballot_sync(0xffffffffu, h1 > 0.f);
+          if (lane == 2 * q) bits = w0;
+          if (lane == 2 * q + 1) bits = w1;
         }
         uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
         const int ch = (c0 % 64) / 8;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        // 16 bits per chunk -> half of word (c0 / 32) of this slot
-        reinterpret_cast<uint16_t *>(sMask)[erow * (KH / 16) + c0 / 16] = (uint16_t)bits;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + u)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        sMask[grp * KH + c0 + lane] = bits;
       }
       tc::fence_async_shared();
       tc::tc_fence_before();
@@ -377,97 +494,81 @@ __global__ void __launch_bounds__(512, 1)
     for (uint32_t t = 0;; ++t) {
       const int b = t & 1;
       const uint32_t p1 = t & 1;
-      const TileDesc2 *dsc = &m->desc[b];
+      const TileDescB *dsc = &m->desc[b];
       tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
       if (!dsc->more) break;
-      // a1 rows -> A1 (one 512-byte row per warp instruction)
-      tc::mbar_wait(&m->a1_ready, p1);
-      for (int s = grp; s < 128; s += 4) {
-        const int p = dsc->slot_edge[s];
-        if (p < 0) continue;
-        const int j = lane >> 3, c = lane & 7;
-        const uint4 x = *reinterpret_cast<const uint4 *>(sAH + j * (128 * 128) + tc::sw128_off(s, c));
-        reinterpret_cast<uint4 *>(A1g + (int64_t)p * KH)[lane] = x;
-      }
-      tc::mbar_arrive(&m->a1_copied);
       // dH / U ready (h_ready: the [h > 0] bits written by EPI_A are visible)
       tc::mbar_wait(&m->h_ready, p1);
+      uint32_t mw0[4], mw1[4];  // [h > 0] over the 128 slots for kappa and kappa + 128
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mw0[u] = sMask[u * KH + grp * 32 + lane];
+        mw1[u] = sMask[u * KH + 128 + grp * 32 + lane];
+      }
+      tc::mbar_arrive(&m->mask_read);
       tc::mbar_wait(&m->s_full, p1);
       tc::tc_fence_after();
       const int nn = dsc->nnodes;
       // U part (thread <-> slot row): u_p = U[slot] + dS_i[k]
       {
         const int s = grp * 32 + lane;
-        const int p = dsc->slot_edge[s];
+        const int p = slot_edge_of(dsc, nn, s);
         for (int g = 0; g < nn; ++g) {
-          const bool mine = p >= 0 && s >= dsc->slot0[g] && s < dsc->slot0[g] + dsc->deg[g];
-          const __nv_bfloat16 *brow = dS + (dsc->node[g] * (KH + 1) + KH) * D;
+          const int g0 = dsc->slot0[g], gd = dsc->deg[g];
+          if (g0 >= grp * 32 + 32 || g0 + gd <= grp * 32) continue;  // row not in this warp's slots
+          const bool mine = p >= 0 && s >= g0 && s < g0 + gd;
+          const __nv_bfloat16 *brow = &m->brow[b][g][0];
+          uint32_t xx[D];
 #pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 16) {
-            uint32_t x[16];
-            tc::tmem_ld16(tmem + lane_off + g * D + c0, x);
-            tc::tmem_ld_wait();
+          for (int c0 = 0; c0 < D; c0 += 32)
+            tc::tmem_ld32(tmem + lane_off + g * D + c0, *reinterpret_cast<uint32_t (*)[32]>(&xx[c0]));
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            const uint32_t *x = &xx[c0];
             if (mine) {
-              const uint4 bb0 = __ldg(reinterpret_cast<const uint4 *>(brow + c0));
-              const uint4 bb1 = __ldg(reinterpret_cast<const uint4 *>(brow + c0 + 8));
-              const __nv_bfloat16 *bv0 = reinterpret_cast<const __nv_bfloat16 *>(&bb0);
-              const __nv_bfloat16 *bv1 = reinterpret_cast<const __nv_bfloat16 *>(&bb1);
-              uint32_t pk[8];
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                pk[q] = tc::pack_bf16(__uint_as_float(x[2 * q]) + __bfloat162float(bv0[2 * q]),
-                                      __uint_as_float(x[2 * q + 1]) + __bfloat162float(bv0[2 * q + 1]));
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                pk[4 + q] = tc::pack_bf16(__uint_as_float(x[8 + 2 * q]) + __bfloat162float(bv1[2 * q]),
-                                          __uint_as_float(x[8 + 2 * q + 1]) + __bfloat162float(bv1[2 * q + 1]));
               uint4 *dst = reinterpret_cast<uint4 *>(Ug + (int64_t)p * D + c0);
-              dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const uint4 bb = *reinterpret_cast<const uint4 *>(brow + c0 + 8 * u);
+                const __nv_bfloat162 *bv = reinterpret_cast<const __nv_bfloat162 *>(&bb);
+                uint32_t pk[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float2 bf = __bfloat1622float2(bv[q]);
+                  pk[q] = tc::pack_bf16(__uint_as_float(x[8 * u + 2 * q]) + bf.x,
+                                        __uint_as_float(x[8 * u + 2 * q + 1]) + bf.y);
+                }
+                dst[u] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              }
             }
           }
         }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&m->u_free);
-      // dz2 part (thread <-> kappa): lane pairs exchange so every 4-byte store
-      // of the warp covers 64 contiguous bytes of two dZ2 rows
-      const bool odd = lane & 1;
+      // dz2 part (thread <-> kappa)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int kap = 128 * h + grp * 32 + lane;
+        uint32_t mwh[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mwh[u] = h ? mw1[u] : mw0[u];
         float acc = 0.f;
         for (int g = 0; g < nn; ++g) {
           const int s0 = dsc->slot0[g];
           const int ns = (dsc->deg[g] + 15) & ~15;
-          for (int c0 = 0; c0 < ns; c0 += 16) {
-            uint32_t x[16];
-            tc::tmem_ld16(tmem + lane_off + 256 + h * 128 + s0 + c0, x);
-            tc::tmem_ld_wait();
-            float dz[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int s = s0 + c0 + j;
-              const uint32_t w = sMask[s * (KH / 32) + (kap >> 5)];
-              dz[j] = ((w >> (kap & 31)) & 1u) ? __uint_as_float(x[j]) : 0.f;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              // even lane stores slot (c0 + 2q) for kappa pair, odd lane slot (c0 + 2q + 1)
-              const float mine = odd ? dz[2 * q + 1] : dz[2 * q];
-              const float give = odd ? dz[2 * q] : dz[2 * q + 1];
-              const float other = __shfl_xor_sync(0xffffffffu, give, 1);
-              const int s = s0 + c0 + 2 * q + (odd ? 1 : 0);
-              const int p = dsc->slot_edge[s];
-              const __nv_bfloat162 pr = odd ? __floats2bfloat162_rn(other, mine) : __floats2bfloat162_rn(mine, other);
-              if (p >= 0)
-                asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(dZ2g + (int64_t)p * KH + (kap & ~1)),
-                             "r"(*reinterpret_cast<const uint32_t *>(&pr))
-                             : "memory");
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc += dz[j];  // pad slots hold dH = 0 (zero V rows)
+          const int64_t ebase = dsc->ebase[g];
+          const int deg = dsc->deg[g];
+          __nv_bfloat16 *row0 = dZ2g + ebase * KH;
+          const uint32_t ta = tmem + lane_off + 256 + h * 128 + s0;
+          int c0 = 0;
+          for (; c0 + 64 <= ns; c0 += 64) acc += dz2_chunk<64>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);
+          if (c0 + 32 <= ns) {
+            acc += dz2_chunk<32>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);
+            c0 += 32;
           }
+          if (c0 < ns) acc += dz2_chunk<16>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);
         }
         if (h == 0) db2_lo += acc; else db2_hi += acc;
       }

@@ -59,8 +59,8 @@ struct EF2 {
 
 // walker: next tile of whole rows, executed by one full warp: the lanes fetch
 // 32 consecutive row_ptr entries in one round trip, lane 0 packs the rows.
-template <int NMAX, class MiscT>
-__device__ __forceinline__ void walk_tile(MiscT *m, TileDesc2 *d, const int64_t *__restrict__ row_ptr, int lane) {
+template <int NMAX, class MiscT, class DescT>
+__device__ __forceinline__ void walk_tile(MiscT *m, DescT *d, const int64_t *__restrict__ row_ptr, int lane) {
   int used = 0, nn = 0;
   int64_t cur = m->cur_row;
   const int64_t end = m->row_end;

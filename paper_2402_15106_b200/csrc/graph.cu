@@ -2,14 +2,23 @@
 // Alg. 1 :395-396; readings R7, R8, R10, R11).
 //
 // Cell list: points are binned into cells of edge h >= r(1+2^-8) over the
-// local bounding box and sorted by cell (stable radix sort).  One warp owns one
+// local bounding box and sorted by cell (stable radix sort); coordinates, the
+// local index and gid are then stored in cell order (xs, gs) so a candidate
+// scan is one coalesced 16-byte load per point.  One warp owns one
 // destination row and scans the 3^dim neighbouring cells (32 candidates per
-// step, ballot-compacted).  Pass 1 counts candidates; the CSR offsets are an
-// exclusive scan of min(count, n_e); pass 2 either keeps all candidates or
-// selects the n_e smallest (key_edge, gid) by a most-significant-digit radix
-// select (8-bit digits, early exit once the boundary bucket is taken whole),
-// then orders the kept row by gid with a rank sort and writes it.
+// step, ballot-compacted).
+//  pass 1 (count2): candidate count and a 2^10-bin histogram of the top key
+//          bits; for a capped row the bin holding the n_e-th smallest key and
+//          how many to take from it;
+//  CSR offsets = exclusive scan of min(count, n_e);
+//  pass 2 (select2): keeps the candidates below the boundary bin, selects the
+//          remaining ones from the boundary bin by full (key_edge, gid) rank,
+//          orders the kept row by gid (rank sort) and writes it.
+// A row whose boundary bin overflows the per-warp buffer (not expected for
+// hash keys) is finished by the general most-significant-digit radix select
+// (select_kernel, 8-bit digits over the full 128-bit (key, gid) composite).
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "hash.cuh"
@@ -147,26 +156,6 @@ __device__ __forceinline__ void scan_candidates(int64_t i, const float *__restri
     }
 }
 
-__global__ void count_kernel(const float *__restrict__ x, int64_t n_dst, int dim, float r,
-                             const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
-                             const int32_t *__restrict__ sorted_idx, int32_t *__restrict__ counts,
-                             int64_t *__restrict__ deg, int32_t n_e) {
-  GridParams p = *gp;
-  float r2 = __fmul_rn(r, r);
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n_dst; i += nwarps) {
-    int cnt = 0;
-    scan_candidates(i, x, dim, r2, p, start, sorted_idx, [&](int, bool ok) {
-      cnt += __popc(__ballot_sync(0xffffffffu, ok));
-    });
-    if ((threadIdx.x & 31) == 0) {
-      if (counts) counts[i] = cnt;
-      if (deg) deg[i] = cnt < n_e ? cnt : n_e;
-    }
-  }
-}
-
 constexpr int kMaxNe = 128;
 constexpr int kSelWarps = 4;
 
@@ -199,7 +188,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(
     const float *__restrict__ x, const int64_t *__restrict__ gid, int64_t n_dst, int dim, float r, int32_t n_e,
     uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
     const int32_t *__restrict__ sorted_idx, const int32_t *__restrict__ counts, const int64_t *__restrict__ row_ptr,
-    int32_t *__restrict__ col) {
+    int32_t *__restrict__ col, const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows) {
   __shared__ uint32_t hist[kSelWarps][256];
   __shared__ int32_t lidx[kSelWarps][kMaxNe];
   __shared__ int64_t lgid[kSelWarps][kMaxNe];
@@ -208,7 +197,9 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(
   int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n_dst; i += nwarps) {
+  const int64_t nr = rows ? (int64_t)*nrows : n_dst;
+  for (int64_t ii = warp; ii < nr; ii += nwarps) {
+    const int64_t i = rows ? (int64_t)rows[ii] : ii;
     int cnt = counts[i];
     uint64_t gi = (uint64_t)gid[i];
     uint64_t si = smx(s0 ^ gi);
@@ -287,6 +278,203 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(
   }
 }
 
+
+// ----------------------------------------------------------- fast path --
+constexpr int kHB = 10, kHBins = 1 << kHB;  // top key bits of the pass-1 histogram
+constexpr int kCapB = 384;                  // boundary-bin buffer per warp
+constexpr int kGWarps = 8;
+
+__global__ void permute_points_kernel(const float *__restrict__ x, const int64_t *__restrict__ gid, int64_t n,
+                                      int dim, const int32_t *__restrict__ sorted_idx, float4 *__restrict__ xs,
+                                      int64_t *__restrict__ gs) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = sorted_idx[t];
+    float4 p;
+    p.x = x[(int64_t)j * dim];
+    p.y = x[(int64_t)j * dim + 1];
+    p.z = dim == 3 ? x[(int64_t)j * dim + 2] : 0.f;
+    p.w = __int_as_float(j);
+    xs[t] = p;
+    if (gs) gs[t] = gid[j];
+  }
+}
+
+// Visit the candidates of row i in cell order; F(t, j, ok) per 32-wide step
+// (warp-uniform call), t = cell-order position, j = local index.
+template <typename F>
+__device__ __forceinline__ void scan_sorted(int64_t i, const float *__restrict__ x, int dim, float r2,
+                                            const GridParams &p, const int32_t *__restrict__ start,
+                                            const float4 *__restrict__ xs, F &&f) {
+  const int lane = threadIdx.x & 31;
+  float xi[3] = {0.f, 0.f, 0.f};
+  for (int d = 0; d < dim; ++d) xi[d] = x[i * dim + d];
+  int c[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) c[d] = cell_coord(xi[d], p.lo[d], p.inv_h, p.n[d]);
+  const int z0 = dim == 3 ? max(c[2] - 1, 0) : 0, z1 = dim == 3 ? min(c[2] + 1, p.n[2] - 1) : 0;
+  const int y0 = max(c[1] - 1, 0), y1 = min(c[1] + 1, p.n[1] - 1);
+  const int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, p.n[0] - 1);
+  for (int cz = z0; cz <= z1; ++cz)
+    for (int cy = y0; cy <= y1; ++cy) {
+      const int base = (cz * p.n[1] + cy) * p.n[0];
+      const int a = start[base + x0], b = start[base + x1 + 1];
+      for (int t0 = a; t0 < b; t0 += 64) {  // two loads in flight per lane
+        const int ta = t0 + lane, tb = t0 + 32 + lane;
+        const float4 pa = ta < b ? xs[ta] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        const float4 pb = tb < b ? xs[tb] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        {
+          const int j = __float_as_int(pa.w);
+          const float xj[3] = {pa.x, pa.y, pa.z};
+          f(ta, j, ta < b && j != i && within(xi, xj, dim, r2));
+        }
+        if (t0 + 32 < b) {
+          const int j = __float_as_int(pb.w);
+          const float xj[3] = {pb.x, pb.y, pb.z};
+          f(tb, j, tb < b && j != i && within(xi, xj, dim, r2));
+        }
+      }
+    }
+}
+
+// pass 1: counts, deg = min(count, n_e), and for capped rows the boundary
+// bin b* of the top-kHB key bits and the number `take` kept from it
+template <bool HIST>
+__global__ void __launch_bounds__(kGWarps * 32) count2_kernel(
+    const float *__restrict__ x, const int64_t *__restrict__ gs, const int64_t *__restrict__ gid, int64_t n_dst,
+    int dim, float r, int32_t n_e, uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
+    const float4 *__restrict__ xs, int32_t *__restrict__ counts, int64_t *__restrict__ deg, int2 *__restrict__ bnd) {
+  __shared__ uint32_t hist_all[HIST ? kGWarps : 1][HIST ? kHBins : 1];
+  const GridParams p = *gp;
+  const float r2 = __fmul_rn(r, r);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *hist = hist_all[HIST ? w : 0];
+  if (HIST)
+    for (int q = lane; q < kHBins; q += 32) hist[q] = 0;
+  __syncwarp();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_dst; i += nwarps) {
+    const uint64_t si = HIST ? smx(s0 ^ (uint64_t)gid[i]) : 0;
+    int cnt = 0;
+    scan_sorted(i, x, dim, r2, p, start, xs, [&](int t, int, bool ok) {
+      if (HIST && ok) atomicAdd(&hist[key_edge(si, (uint64_t)gs[t]) >> (64 - kHB)], 1u);
+      cnt += __popc(__ballot_sync(0xffffffffu, ok));
+    });
+    if (lane == 0) {
+      if (counts) counts[i] = cnt;
+      if (deg) deg[i] = cnt < n_e ? cnt : n_e;
+    }
+    if (HIST) {
+      __syncwarp();
+      constexpr int PER = kHBins / 32;
+      if (cnt > n_e) {
+        uint32_t sum = 0;
+        for (int q = 0; q < PER; ++q) sum += hist[lane * PER + q];
+        uint32_t incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const uint32_t excl = incl - sum;
+        if ((int)excl < n_e && n_e <= (int)incl) {
+          uint32_t c0 = excl;
+          for (int q = 0; q < PER; ++q) {
+            const uint32_t hq = hist[lane * PER + q];
+            if ((int)(c0 + hq) >= n_e) {
+              bnd[i] = make_int2(lane * PER + q, n_e - (int)c0);
+              break;
+            }
+            c0 += hq;
+          }
+        }
+      }
+      __syncwarp();
+      for (int q = lane; q < kHBins; q += 32) hist[q] = 0;
+      __syncwarp();
+    }
+  }
+}
+
+// pass 2 (capped rows select from the boundary bin; uncapped rows keep all)
+__global__ void __launch_bounds__(kGWarps * 32) select2_kernel(
+    const float *__restrict__ x, const int64_t *__restrict__ gs, const int64_t *__restrict__ gid, int64_t n_dst,
+    int dim, float r, int32_t n_e, uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
+    const float4 *__restrict__ xs, const int32_t *__restrict__ counts, const int2 *__restrict__ bnd,
+    const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col, int32_t *__restrict__ fl_rows,
+    int32_t *__restrict__ fl_n, int force_fallback) {
+  __shared__ int32_t Lt[kGWarps][kMaxNe];
+  __shared__ int64_t Lg[kGWarps][kMaxNe];
+  __shared__ uint64_t Bk[kGWarps][kCapB];
+  __shared__ int32_t Bt[kGWarps][kCapB];
+  const GridParams p = *gp;
+  const float r2 = __fmul_rn(r, r);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_dst; i += nwarps) {
+    const int cnt = counts[i];
+    const bool capped = cnt > n_e;
+    const int2 bt = capped ? bnd[i] : make_int2(kHBins, 0);
+    const uint64_t si = smx(s0 ^ (uint64_t)gid[i]);
+    int nl = 0, nb = 0;
+    scan_sorted(i, x, dim, r2, p, start, xs, [&](int t, int, bool ok) {
+      uint32_t top = 0;
+      uint64_t key = 0;
+      if (ok && capped) {
+        key = key_edge(si, (uint64_t)gs[t]);
+        top = (uint32_t)(key >> (64 - kHB));
+      }
+      const bool inL = ok && (!capped || (int)top < bt.x);
+      const bool inB = ok && capped && (int)top == bt.x;
+      const uint32_t mL = __ballot_sync(0xffffffffu, inL), mB = __ballot_sync(0xffffffffu, inB);
+      if (inL) Lt[w][nl + __popc(mL & lt)] = t;
+      if (inB) {
+        const int q = nb + __popc(mB & lt);
+        if (q < kCapB) {
+          Bk[w][q] = key;
+          Bt[w][q] = t;
+        }
+      }
+      nl += __popc(mL);
+      nb += __popc(mB);
+    });
+    if (nb > kCapB || (force_fallback && capped)) {  // finish this row with the general select
+      if (lane == 0) fl_rows[atomicAdd(fl_n, 1)] = (int32_t)i;
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // the `take` smallest (key, gid) of the boundary bin
+    for (int a0 = 0; a0 < nb; a0 += 32) {
+      const int a = a0 + lane;
+      bool keep = false;
+      if (a < nb) {
+        const uint64_t ka = Bk[w][a];
+        int rank = 0;
+        for (int b = 0; b < nb; ++b) {
+          const uint64_t kb = Bk[w][b];
+          rank += kb < ka || (kb == ka && gs[Bt[w][b]] < gs[Bt[w][a]]);
+        }
+        keep = rank < bt.y;
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) Lt[w][nl + __popc(m & lt)] = Bt[w][a];
+      nl += __popc(m);
+    }
+    __syncwarp();
+    for (int q = lane; q < nl; q += 32) Lg[w][q] = gs[Lt[w][q]];
+    __syncwarp();
+    const int64_t off = row_ptr[i];
+    for (int a = lane; a < nl; a += 32) {
+      const int64_t g = Lg[w][a];
+      int rank = 0;
+      for (int b = 0; b < nl; ++b) rank += Lg[w][b] < g;
+      col[off + rank] = __float_as_int(xs[Lt[w][a]].w);
+    }
+    __syncwarp();
+  }
+}
+
 static int64_t max_cells_for(int64_t n_loc) { return std::max<int64_t>(4 * n_loc, 4096); }
 
 static size_t graph_ws(int64_t n_loc, int64_t n_dst, size_t *sort_tmp, size_t *scan_tmp) {
@@ -300,6 +488,10 @@ static size_t graph_ws(int64_t n_loc, int64_t n_dst, size_t *sort_tmp, size_t *s
   c.take<int32_t>(max_cells_for(n_loc) + 1);
   c.take<int32_t>(n_dst);
   c.take<int64_t>(n_dst + 1);
+  c.take<float4>(n_loc);
+  c.take<int64_t>(n_loc);
+  c.take<int2>(n_dst);
+  c.take<int32_t>(n_dst + 1);
   c.take<char>(*sort_tmp);
   c.take<char>(*scan_tmp);
   return c.used();
@@ -309,12 +501,16 @@ struct GraphState {
   GridParams *gp;
   int32_t *sorted_idx, *start, *counts;
   int64_t *deg;
+  float4 *xs;
+  int64_t *gs;
+  int2 *bnd;
+  int32_t *fl;  // [0] = count, [1..] = rows
   void *scan_tmp;
   size_t scan_bytes;
 };
 
-static dsmpnn_status build_cells(const float *coords, int64_t n_loc, int64_t n_dst, int dim, float r, void *ws,
-                                 size_t ws_bytes, cudaStream_t s, GraphState &st) {
+static dsmpnn_status build_cells(const float *coords, const int64_t *gid, int64_t n_loc, int64_t n_dst, int dim,
+                                 float r, void *ws, size_t ws_bytes, cudaStream_t s, GraphState &st) {
   size_t sort_tmp, scan_tmp;
   size_t need = graph_ws(n_loc, n_dst, &sort_tmp, &scan_tmp);
   DS_CHECK_ARG(ws_bytes >= need, DSMPNN_ERR_CAPACITY, "radius_graph: workspace %zu < %zu", ws_bytes, need);
@@ -328,6 +524,10 @@ static dsmpnn_status build_cells(const float *coords, int64_t n_loc, int64_t n_d
   st.start = c.take<int32_t>(maxc + 1);
   st.counts = c.take<int32_t>(n_dst);
   st.deg = c.take<int64_t>(n_dst + 1);
+  st.xs = c.take<float4>(n_loc);
+  st.gs = c.take<int64_t>(n_loc);
+  st.bnd = c.take<int2>(n_dst);
+  st.fl = c.take<int32_t>(n_dst + 1);
   void *t1 = c.take<char>(sort_tmp);
   st.scan_tmp = c.take<char>(scan_tmp);
   st.scan_bytes = scan_tmp;
@@ -343,6 +543,8 @@ static dsmpnn_status build_cells(const float *coords, int64_t n_loc, int64_t n_d
                                           end_bit, s));
   cell_start_kernel<<<(int)std::min<int64_t>(ceil_div(maxc + 1, 256), 148 * 8), 256, 0, s>>>(cell_sorted, n_loc,
                                                                                             st.gp, st.start, maxc);
+  DS_LAUNCH_CHECK();
+  permute_points_kernel<<<g, 256, 0, s>>>(coords, gid, n_loc, dim, st.sorted_idx, st.xs, gid ? st.gs : nullptr);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -368,9 +570,10 @@ dsmpnn_status dsmpnn_radius_counts(const float *coords, int64_t n_loc, int64_t n
   if (n_dst == 0) return DSMPNN_OK;
   cudaStream_t s = as_stream(stream);
   GraphState st;
-  DS_TRY(build_cells(coords, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
-  int blocks = (int)std::min<int64_t>(ceil_div(n_dst * 32, 256), 148 * 16);
-  count_kernel<<<blocks, 256, 0, s>>>(coords, n_dst, dim, r, st.gp, st.start, st.sorted_idx, counts, nullptr, 1);
+  DS_TRY(build_cells(coords, nullptr, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
+  int blocks = (int)std::min<int64_t>(ceil_div(n_dst, kGWarps), 148 * 16);
+  count2_kernel<false><<<blocks, kGWarps * 32, 0, s>>>(coords, nullptr, nullptr, n_dst, dim, r, 1, 0, st.gp, st.start,
+                                                       st.xs, counts, nullptr, nullptr);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -394,10 +597,13 @@ dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64
     DS_CHECK_ARG(col_capacity >= n_dst * (int64_t)n_e, DSMPNN_ERR_CAPACITY,
                  "radius_graph: without n_edges, col_capacity must be >= n_dst*n_e");
   GraphState st;
-  DS_TRY(build_cells(coords, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
-  int blocks = (int)std::min<int64_t>(ceil_div(n_dst * 32, 256), 148 * 16);
-  count_kernel<<<blocks, 256, 0, s>>>(coords, n_dst, dim, r, st.gp, st.start, st.sorted_idx, st.counts, st.deg, n_e);
+  DS_TRY(build_cells(coords, gid, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
+  const uint64_t s0 = smx(seed);
+  int blocks = (int)std::min<int64_t>(ceil_div(n_dst, kGWarps), 148 * 16);
+  count2_kernel<true><<<blocks, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start,
+                                                      st.xs, st.counts, st.deg, st.bnd);
   DS_LAUNCH_CHECK();
+  DS_CUDA(cudaMemsetAsync(st.fl, 0, sizeof(int32_t), s));
   DS_CUDA(cudaMemsetAsync(st.deg + n_dst, 0, sizeof(int64_t), s));
   size_t sb = st.scan_bytes;
   DS_CUDA(cub::DeviceScan::ExclusiveSum(st.scan_tmp, sb, st.deg, row_ptr, (int)(n_dst + 1), s));
@@ -409,9 +615,13 @@ dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64
       return DSMPNN_ERR_CAPACITY;
     }
   }
-  int sblocks = (int)std::min<int64_t>(ceil_div(n_dst, kSelWarps), 148 * 16);
-  select_kernel<<<sblocks, kSelWarps * 32, 0, s>>>(coords, gid, n_dst, dim, r, n_e, smx(seed), st.gp, st.start,
-                                                  st.sorted_idx, st.counts, row_ptr, col_idx);
+  select2_kernel<<<blocks, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start, st.xs,
+                                                st.counts, st.bnd, row_ptr, col_idx, st.fl + 1, st.fl,
+                                                getenv("DSMPNN_TEST_GRAPH_FALLBACK") != nullptr);
+  DS_LAUNCH_CHECK();
+  // rows whose boundary bin overflowed (row list on the device; usually empty)
+  select_kernel<<<148, kSelWarps * 32, 0, s>>>(coords, gid, n_dst, dim, r, n_e, s0, st.gp, st.start, st.sorted_idx,
+                                               st.counts, row_ptr, col_idx, st.fl + 1, st.fl);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

@@ -45,25 +45,29 @@ __global__ void ghat_bf16_kernel(const float *__restrict__ G, const float *__res
   }
 }
 
-// dW3[c*D+o, kap] += dT[kap*D+c, o]; db3[c*D+o] += dT[k*D+c, o]; dW_root[o, c] += dT[(k+1)*D+c, o]
-__global__ void unpack_dtheta_aug_kernel(const float *__restrict__ dT, int k, int D, float *__restrict__ dW3,
-                                         float *__restrict__ db3, float *__restrict__ dWr) {
-  int64_t total = (int64_t)(k + 2) * D * D;
+// dW3[c*D+o, kap] += dT[c*k+kap, o]  (the [c][kappa] block of S~_aug's K
+// order): 32 x 32 tiles transposed through shared memory so both the dT reads
+// and the dW3 read-modify-writes are coalesced.  grid = (k/32, D/32, D)
+__global__ void unpack_dw3_kernel(const float *__restrict__ dT, int k, int D, float *__restrict__ dW3) {
+  __shared__ float t[32][33];
+  const int kap0 = blockIdx.x * 32, o0 = blockIdx.y * 32, c = blockIdx.z;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  for (int r = ty; r < 32; r += 8) t[r][tx] = dT[((int64_t)c * k + kap0 + r) * D + o0 + tx];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    float *w = dW3 + ((int64_t)c * D + o0 + r) * k + kap0 + tx;
+    *w += t[tx][r];
+  }
+}
+
+// db3[c*D+o] += dT[k*D+c, o]; dW_root[o, c] += dT[(k+1)*D+c, o]
+__global__ void unpack_bias_root_kernel(const float *__restrict__ dT, int k, int D, float *__restrict__ db3,
+                                        float *__restrict__ dWr) {
+  const int64_t total = (int64_t)D * D;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t row = t / D;  // K index of the forward S~_aug layout
-    int o = (int)(t - row * D);
-    int kap, c;
-    if (row < (int64_t)k * D) {  // [c][kappa] block
-      c = (int)(row / k);
-      kap = (int)(row - (int64_t)c * k);
-    } else {
-      kap = (int)(row / D);
-      c = (int)(row - (int64_t)kap * D);
-    }
-    float x = dT[t];
-    if (kap < k) { if (dW3) dW3[((int64_t)c * D + o) * k + kap] += x; }
-    else if (kap == k) { if (db3) db3[(int64_t)c * D + o] += x; }
-    else if (dWr) dWr[(int64_t)o * D + c] += x;
+    const int a = (int)(t / D), b = (int)(t - (int64_t)a * D);
+    if (db3) db3[t] += dT[((int64_t)k * D) * D + t];                       // c = a, o = b
+    if (dWr) dWr[(int64_t)b * D + a] += dT[((int64_t)(k + 1) * D) * D + t];  // c = a, o = b
   }
 }
 
@@ -95,7 +99,8 @@ struct BBwd {
   __nv_bfloat16 *U;        // [E x D] (bf16)
   float *part;             // split-K partials (max over users)
   float *db2_part;         // [kNumSMs x k]
-  float *db1_part;         // [ceil(E/128)*4 x k]
+  float *db1_part;         // [kColsumRows x k]
+  float *cs_ws;            // colsum partials [kColsumChunks x max(D, k)]
   float *dW1f;             // [k x 16]
   float *de16;             // [E x 16]
 };
@@ -117,6 +122,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.part = c.take<float>((int64_t)kSplitsW * d.k * d.k);
   b.db2_part = c.take<float>((int64_t)kNumSMs * d.k);
   b.db1_part = c.take<float>((int64_t)kColsumRows * d.k);
+  b.cs_ws = c.take<float>((int64_t)kColsumChunks * std::max(d.k, d.d_in));
   b.dW1f = c.take<float>((int64_t)d.k * 16);
   b.de16 = c.take<float>(E * 16);
   return b;
@@ -143,20 +149,61 @@ static BFwdView view_fwd(const dsmpnn_layer_desc &d, const void *ws, int64_t n_d
   return f;
 }
 
+// dv[j] += sum over the CSC list of j of u_p (p in [eb, ee)).  One warp per
+// node: lane = (channel group of 8, sub-list); sub-lists interleave the list
+// and are combined by a butterfly, so the summation order is fixed.
+template <int D>
 __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, const int32_t *__restrict__ perm,
-                                       const int64_t *__restrict__ cptr, int64_t n_loc, int di, int64_t eb,
-                                       int64_t ee, float *__restrict__ dv) {
-  int64_t total = n_loc * di;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t j = t / di;
-    int c = (int)(t - j * di);
-    float s = 0.f;
+                                        const int64_t *__restrict__ cptr, int64_t n_loc, int64_t eb, int64_t ee,
+                                        float *__restrict__ dv) {
+  constexpr int CG = D / 8, SL = 32 / CG, UNR = 4;
+  const int lane = threadIdx.x & 31, cg = lane % CG, sub = lane / CG;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_loc; j += nw) {
+    const int64_t q0 = cptr[j], q1 = cptr[j + 1];
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
     bool any = false;
-    for (int64_t q = cptr[j]; q < cptr[j + 1]; ++q) {
-      int64_t p = perm[q];
-      if (p >= eb && p < ee) { s += __bfloat162float(U[p * di + c]); any = true; }
+    for (int64_t q = q0 + sub; q < q1; q += SL * UNR) {
+      int64_t p[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t qq = q + u * SL;
+        p[u] = qq < q1 ? (int64_t)__ldg(perm + qq) : -1;
+      }
+      uint4 x[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const bool ok = p[u] >= eb && p[u] < ee;
+        any |= ok;
+        x[u] = ok ? __ldg(reinterpret_cast<const uint4 *>(U + p[u] * D) + cg) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&x[u]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
     }
-    if (any) dv[t] += s;
+#pragma unroll
+    for (int off = CG; off < 32; off <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (any && sub == 0) {
+      float4 *o = reinterpret_cast<float4 *>(dv + j * D + cg * 8);
+      float4 a0 = o[0], a1 = o[1];
+      a0.x += acc[0]; a0.y += acc[1]; a0.z += acc[2]; a0.w += acc[3];
+      a1.x += acc[4]; a1.y += acc[5]; a1.z += acc[6]; a1.w += acc[7];
+      o[0] = a0;
+      o[1] = a1;
+    }
   }
 }
 
@@ -206,7 +253,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   // B0
   ghat_bf16_kernel<<<grid_of(nR * D), 256, 0, s>>>(G, f.pre, row_ptr, rb, re, D, d.act, b.gh, b.gh16, b.inv_deg);
   DS_LAUNCH_CHECK();
-  DS_TRY(colsum(b.gh + rb * D, nR, D, D, gr.b, 1, s));
+  DS_TRY(colsum_ws(b.gh + rb * D, nR, D, D, gr.b, 1, b.cs_ws, s));
   if (d.root == DSMPNN_ROOT_DENSE && dv) {
     SgemmArgs g{nR, D, D, b.gh + rb * D, D, 1, w.W_root, D, 1, dv + rb * D, D, nullptr, 0, 1, 1.f};
     DS_TRY(sgemm(g, 1, nullptr, s));
@@ -218,8 +265,12 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   if (gr.W3 || gr.b3 || gr.W_root) {
     TgemmArgs a{kp, D, nR, f.S + rb * kp, kp, true, b.gh16 + rb * D, D, true, b.dT, D, 1, 0, 0};
     DS_TRY(tgemm(a, s));
-    unpack_dtheta_aug_kernel<<<grid_of((int64_t)(k + 2) * D * D), 256, 0, s>>>(
-        b.dT, k, D, gr.W3, gr.b3, d.root == DSMPNN_ROOT_DENSE ? gr.W_root : nullptr);
+    if (gr.W3) {
+      unpack_dw3_kernel<<<dim3(k / 32, D / 32, D), 256, 0, s>>>(b.dT, k, D, gr.W3);
+      DS_LAUNCH_CHECK();
+    }
+    unpack_bias_root_kernel<<<grid_of((int64_t)D * D), 256, 0, s>>>(
+        b.dT, k, D, gr.b3, d.root == DSMPNN_ROOT_DENSE ? gr.W_root : nullptr);
     DS_LAUNCH_CHECK();
   }
   if (nE <= 0) return DSMPNN_OK;
@@ -256,7 +307,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     a.colsum_part = b.db1_part;
     DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
     DS_TRY(tgemm(a, s));
-    DS_TRY(colsum(b.db1_part, kColsumRows, k, k, gr.b1, 1, s));
+    DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, gr.b1, 1, b.cs_ws, s));
   }
   // B6: dW1 += dz1^T e ;  de = dz1 W1
   if (gr.W1) {
@@ -278,7 +329,9 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   }
   // B7: dv[j] += sum of u_p over edges with source j (CSC order)
   if (dv) {
-    scatter_csc_bf16_kernel<<<grid_of(n_loc * D), 256, 0, s>>>(b.U, perm, cptr, n_loc, D, eb, ee, dv);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 8), 148 * 16));
+    if (D == 64) scatter_csc_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
+    else scatter_csc_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
     DS_LAUNCH_CHECK();
   }
   return DSMPNN_OK;

@@ -109,9 +109,17 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ 
   __shared__ float red[32][33];
   int c = threadIdx.x & 31, r = threadIdx.x >> 5;
   int64_t n = (int64_t)blockIdx.x * 32 + c;
-  float s = 0.f;
-  if (n < N)
-    for (int64_t m = r; m < M; m += 32) s += A[m * lda + n];
+  // 8 independent accumulators (loads in flight), combined in a fixed order
+  float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (n < N) {
+    int64_t m = r;
+    for (; m + 7 * 32 < M; m += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) p[u] += A[(m + u * 32) * lda + n];
+    }
+    for (; m < M; m += 32) p[0] += A[m * lda + n];
+  }
+  const float s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
   red[r][c] = s;
   __syncthreads();
   if (r == 0 && n < N) {
@@ -121,11 +129,41 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ 
   }
 }
 
+__global__ void __launch_bounds__(1024) colsum_chunk_kernel(const float *__restrict__ A, int64_t M, int64_t N,
+                                                            int64_t lda, int64_t chunk, float *__restrict__ ws) {
+  __shared__ float red[32][33];
+  const int c = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int64_t n = (int64_t)blockIdx.x * 32 + c;
+  const int64_t m0 = (int64_t)blockIdx.y * chunk, m1 = m0 + chunk < M ? m0 + chunk : M;
+  float s = 0.f;
+  if (n < N)
+    for (int64_t m = m0 + r; m < m1; m += 32) s += A[m * lda + n];
+  red[r][c] = s;
+  __syncthreads();
+  if (r == 0 && n < N) {
+    float t = 0.f;
+    for (int k = 0; k < 32; ++k) t += red[k][c];
+    ws[(int64_t)blockIdx.y * N + n] = t;
+  }
+}
+
 dsmpnn_status colsum(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, cudaStream_t s) {
   if (N <= 0 || !out) return DSMPNN_OK;
   colsum_kernel<<<(unsigned)ceil_div(N, 32), 1024, 0, s>>>(A, M, N, lda, out, accumulate);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
+}
+
+dsmpnn_status colsum_ws(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, float *ws,
+                        cudaStream_t s) {
+  if (N <= 0 || !out) return DSMPNN_OK;
+  if (!ws || M <= 2048) return colsum(A, M, N, lda, out, accumulate, s);
+  const int64_t chunk = ceil_div(M, (int64_t)kColsumChunks);
+  const int R = (int)ceil_div(M, chunk);
+  // level 1: chunk r of rows -> ws[r, :]   (grid.y = chunk)
+  colsum_chunk_kernel<<<dim3((unsigned)ceil_div(N, 32), R), 1024, 0, s>>>(A, M, N, lda, chunk, ws);
+  DS_LAUNCH_CHECK();
+  return colsum(ws, R, N, N, out, accumulate, s);
 }
 
 }  // namespace dsmpnn

@@ -26,5 +26,10 @@ dsmpnn_status sgemm(const SgemmArgs &a, int splits, float *partial, cudaStream_t
 
 // out[n] (+)= sum_{m<M} A[m*lda + n] in a fixed order (deterministic)
 dsmpnn_status colsum(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, cudaStream_t s);
+// same result semantics, two-level (row chunks -> partials -> sum in chunk
+// order) when M is large; ws must hold kColsumChunks * N floats
+constexpr int kColsumChunks = 128;
+dsmpnn_status colsum_ws(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, float *ws,
+                        cudaStream_t s);
 
 }  // namespace dsmpnn

@@ -400,8 +400,15 @@ __global__ void splitk_sum_kernel(const float *__restrict__ p, int splits, int64
   int64_t total = M * N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t m = t / N, n = t - m * N;
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += p[z * stride + m * ld + n];
+    float q[4] = {0.f, 0.f, 0.f, 0.f};  // 4 loads in flight, fixed combination order
+    const float *src = p + m * ld + n;
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] += src[(int64_t)(z + u) * stride];
+    }
+    for (; z < splits; ++z) q[0] += src[(int64_t)z * stride];
+    const float s = (q[0] + q[1]) + (q[2] + q[3]);
     float *c = C + m * ldc + n;
     *c = accumulate ? *c + s : s;
   }

@@ -70,6 +70,21 @@ def test_radius_graph_bit_exact(L, name, gen, r, n_e, frac):
     assert np.array_equal(col, ocol)
 
 
+@pytest.mark.parametrize("name,gen,r,n_e,frac", [CASES[0], CASES[3], CASES[5]], ids=["uniform2d", "grid3d", "dense"])
+def test_radius_graph_general_select_path(L, name, gen, r, n_e, frac, monkeypatch):
+    """Rows whose boundary histogram bin overflows are finished by the general
+    128-bit radix select; the test hook sends every capped row there."""
+    monkeypatch.setenv("DSMPNN_TEST_GRAPH_FALLBACK", "1")
+    g = np.random.default_rng(zlib.crc32(name.encode()) % 1000)
+    x = gen(g).astype(np.float32)
+    n = len(x)
+    gid = g.permutation(10 * n)[:n].astype(np.int64)
+    rp, col, E = _graph_gpu(L, x, gid, n, r, n_e, 91)
+    orp, ocol = graph.radius_graph(x, gid, n, r, n_e, 91)
+    assert np.array_equal(rp, orp)
+    assert np.array_equal(col, ocol)
+
+
 def test_radius_graph_empty_and_errors(L):
     x = np.random.default_rng(0).random((10, 2)).astype(np.float32)
     rp, col, E = _graph_gpu(L, x, np.arange(10), 0, 0.1, 8, 1)

@@ -132,6 +132,18 @@ def count_our_launches(fn):
     return ours, other
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed `ncu --set full` summary (profiles/ncu_traffic.json),
+    or None when no capture of the current kernel is recorded."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f).get(kernel)
+        return rec["bytes_per_launch"] if rec else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -260,7 +272,14 @@ def main():
     torch.cuda.synchronize()
     E_local = hp.n_edges
     launches, lib_other = count_our_launches(lambda: step(devin))
-    probe_id = L.PROBE_BF16_EDGE_FWD if sc.dtype == L.BF16 else L.PROBE_F32_MLP2
+    # dominant kernel of the step: the fused edge backward (BF16), the kappa-MLP
+    # second-layer GEMM (F32)
+    probe_id = L.PROBE_BF16_EDGE_BWD if sc.dtype == L.BF16 else L.PROBE_F32_MLP2
+    # algorithmic HBM bytes of one step's edge-backward launches (DESIGN.md
+    # "Rooflines"): per edge e (32 B, bf16 padded to 16) + v_j (2d) + col (4)
+    # + a1, dz2 (2k each) + u_p (2d); per destination row dS_i (2(k+1)d)
+    bwd_bytes_step = sum(sd.n_edges * (32 + 4 + 4 * sc.d + 4 * sc.k) + sd.n_own * 2 * (sc.k + 1) * sc.d
+                         for sd in hp.subs) * sc.L
 
     # ---- device-resident timed region
     clocks = ClockSampler(local)
@@ -300,6 +319,16 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1) / args.steps
 
+    # ---- graph build alone (sample + partition + radius graph + attributes + CSC), for reference
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(st)
+    for _ in range(args.steps):
+        hp.build(devin["coords"], devin["attr"])
+    g1.record(st)
+    torch.cuda.synchronize()
+    graph_ms = g0.elapsed_time(g1) / args.steps
+
     stats = torch.tensor([ms, e2e_ms, float(E_local)], dtype=torch.float64, device=dev)
     if world > 1:
         mx = stats.clone()
@@ -314,10 +343,10 @@ def main():
     if rank == 0:
         peaks, src = measured_peaks()
         k, d = sc.k, sc.d
+        bwd_flops_edge = 2 * (16 * k + k * k) + 2 * 2 * k * d  # recomputed MLP + dH^T + U
         if sc.dtype == L.BF16:
-            # dominant kernel: fused edge MLP + S formation; algorithmic flops per edge
-            flops_edge = 2 * (16 * k + k * k) + 2 * (k + 1) * d
-            unit, bound, peak = "TFLOP/s", "tensor", float(peaks["bf16_tflops_sustained"])
+            # fused edge backward: HBM-bound (its byte floor exceeds its tensor floor)
+            unit, bound, peak = "GB/s", "hbm", float(peaks["hbm_gbs"])
         else:
             # F32: the kappa-MLP second layer (fp32 SIMT FFMA); peak from unit counts
             flops_edge = 2 * k * k
@@ -325,7 +354,14 @@ def main():
             peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         per_launch_ms = probe_ms / max(1, probe_n)
         units_per_launch = E_local * args.steps * sc.L / max(1, probe_n)
-        achieved = flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
+        if sc.dtype == L.BF16:
+            bytes_per_launch = bwd_bytes_step * args.steps / max(1, probe_n)
+            achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9 if probe_n else 0.0
+            tensor_tflops = bwd_flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
+            traffic = ncu_traffic("edge_bwd2")
+        else:
+            achieved = flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
+            bytes_per_launch, tensor_tflops, traffic = None, None, None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -339,12 +375,18 @@ def main():
                        "l2": "256 MB buffer zeroed at the start of every step, inside the timed region",
                        "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd"},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                         "frac": achieved / peak if peak else None, "traffic": None,
-                         "kernel": {1: "F32 mlp2 sgemm", 3: "bf16 fused edge fwd"}.get(probe_id, str(probe_id)),
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel": {1: "F32 mlp2 sgemm", 5: "bf16 fused edge bwd (edge_bwd2)"}.get(probe_id,
+                                                                                               str(probe_id)),
+                         "algorithmic_bytes_per_launch": bytes_per_launch,
+                         "tensor_tflops_same_launches": tensor_tflops,
+                         "tensor_frac": (tensor_tflops / float(peaks["bf16_tflops_sustained"])
+                                         if tensor_tflops else None),
                          "per_launch_ms": per_launch_ms, "launches": probe_n,
                          "share_of_step": probe_ms / (ms * args.steps), "peak_source": src},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
+            "graph_ms": graph_ms,
             "gpu_launches": launches * args.steps,
             "gpu_launches_cub": lib_other * args.steps,
             "clocks": clk,

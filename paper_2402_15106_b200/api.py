@@ -79,9 +79,8 @@ class HotPath:
         a = torch.empty((ids.numel(), c.n_attr), dtype=torch.float32, device=self.dev)
         L.gather_rows(attr, ids64, a)
         self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts)
-        for sd in self.subs:
-            pipeline.build_graph(sd, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
-                                 want_bf16=(c.dtype == L.BF16))
+        pipeline.build_graphs(self.subs, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
+                              want_bf16=(c.dtype == L.BF16))
         return self
 
     @property

@@ -40,36 +40,6 @@ __device__ __forceinline__ int32_t slot_edge_of(const TileDescB *d, int nn, int 
   return pe;
 }
 
-// register copy of a tile's rows (the desc fields are warp-uniform)
-template <int NMAX>
-struct TileRegs {
-  int nn;
-  int s0[NMAX], deg[NMAX];
-  int64_t eb[NMAX];
-  __device__ __forceinline__ void load(const TileDescB *d) {
-    nn = d->nnodes;
-#pragma unroll
-    for (int g = 0; g < NMAX; ++g) {
-      const bool ok = g < nn;
-      s0[g] = ok ? d->slot0[g] : 1 << 20;
-      deg[g] = ok ? d->deg[g] : 0;
-      eb[g] = ok ? d->ebase[g] : 0;
-    }
-  }
-  __device__ __forceinline__ int32_t edge(int s) const {
-    int32_t pe = -1;
-#pragma unroll
-    for (int g = 0; g < NMAX; ++g) {
-      const int o = s - s0[g];
-      if (o >= 0 && o < deg[g]) pe = (int32_t)(eb[g] + o);
-    }
-    return pe;
-  }
-};
-
-// dz2 for NS consecutive slots (one TMEM load, one wait): dz2 = dH * [h > 0];
-// lane pairs (kappa, kappa+1) exchange values so every 4-byte store of the
-// warp covers 64 contiguous bytes of two dZ2 rows.  Returns the lane's sum.
 // [h > 0] bits of slots s .. s+63 (bit j = slot s + j) from the 128 slot bits
 // w[0..3]; shifts and selects only (no register-array indexing)
 __device__ __forceinline__ uint64_t slot_bits(const uint32_t (&w)[4], int s) {

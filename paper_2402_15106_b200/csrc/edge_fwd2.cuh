@@ -57,6 +57,37 @@ struct EF2 {
   static constexpr uint32_t ROWB = D * 2;
 };
 
+// register copy of a tile's rows (the desc fields are warp-uniform)
+template <int NMAX>
+struct TileRegs {
+  int nn;
+  int s0[NMAX], deg[NMAX];
+  int64_t eb[NMAX];
+  template <class DescT>
+  __device__ __forceinline__ void load(const DescT *d) {
+    nn = d->nnodes;
+#pragma unroll
+    for (int g = 0; g < NMAX; ++g) {
+      const bool ok = g < nn;
+      s0[g] = ok ? d->slot0[g] : 1 << 20;
+      deg[g] = ok ? d->deg[g] : 0;
+      eb[g] = ok ? d->ebase[g] : 0;
+    }
+  }
+  __device__ __forceinline__ int32_t edge(int s) const {
+    int32_t pe = -1;
+#pragma unroll
+    for (int g = 0; g < NMAX; ++g) {
+      const int o = s - s0[g];
+      if (o >= 0 && o < deg[g]) pe = (int32_t)(eb[g] + o);
+    }
+    return pe;
+  }
+};
+
+// dz2 for NS consecutive slots (one TMEM load, one wait): dz2 = dH * [h > 0];
+// lane pairs (kappa, kappa+1) exchange values so every 4-byte store of the
+// warp covers 64 contiguous bytes of two dZ2 rows.  Returns the lane's sum.
 // walker: next tile of whole rows, executed by one full warp: the lanes fetch
 // 32 consecutive row_ptr entries in one round trip, lane 0 packs the rows.
 template <int NMAX, class MiscT, class DescT>
@@ -176,57 +207,47 @@ __global__ void __launch_bounds__(512, 1)
       if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
       if (warp == 0) walk_tile<NMAX>(m, dsc, row_ptr, lane);
       tc::named_sync(1, 96);
-      const int nn = dsc->nnodes;
-      for (int s = li; s < 128; s += 96) {
-        int32_t pe = -1;
-        for (int g = 0; g < nn; ++g) {
-          int o = s - dsc->slot0[g];
-          if (o >= 0 && o < dsc->deg[g]) pe = (int32_t)(dsc->ebase[g] + o);
-        }
-        dsc->slot_edge[s] = pe;
-      }
-      tc::named_sync(1, 96);
       if (!dsc->more) {
         tc::mbar_arrive(&m->e_full[b]);
         break;
       }
-      // issue every global load of the tile first (registers), store to SMEM
-      // only once the consumers have released the buffers
-      constexpr int CH = D / 8;                        // 16-byte chunks per v row
-      constexpr int NE = (256 + 95) / 96, NV = (128 * CH + 95) / 96;
-      uint4 ev[NE], vv[NV];
+      // thread li gathers whole rows li and li + 96 (< 128): index loads first,
+      // then every row load in flight; SMEM stores once the buffers are free
+      constexpr int CH = D / 8;  // 16-byte chunks per v row
+      TileRegs<NMAX> tr;
+      tr.load(dsc);
+      int32_t pe[2], cj[2];
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int q = li + 96 * k;
-        ev[k] = make_uint4(0, 0, 0, 0);
-        if (q < 256) {
-          const int pe = dsc->slot_edge[q >> 1];
-          if (pe >= 0) ev[k] = __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe * 16) + (q & 1));
-        }
-      }
+      for (int u = 0; u < 2; ++u) pe[u] = (li + 96 * u < 128) ? tr.edge(li + 96 * u) : -1;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int q = li + 96 * k;
-        vv[k] = make_uint4(0, 0, 0, 0);
-        if (q < 128 * CH) {
-          const int pe = dsc->slot_edge[q / CH];
-          if (pe >= 0) vv[k] = __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)__ldg(col + pe) * D) + (q % CH));
-        }
+      for (int u = 0; u < 2; ++u) cj[u] = pe[u] >= 0 ? __ldg(col + pe[u]) : -1;
+      uint4 ev[2][2], vv[2][CH];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          ev[u][c] = pe[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe[u] * 16) + c)
+                                : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+          vv[u][c] = cj[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)cj[u] * D) + c)
+                                : make_uint4(0, 0, 0, 0);
       }
       if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
-      uint8_t *eb_s = sE;
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int q = li + 96 * k;
-        if (q < 256) *reinterpret_cast<uint4 *>(eb_s + il_off(q >> 1, q & 1)) = ev[k];
+      for (int u = 0; u < 2; ++u) {
+        if (li + 96 * u >= 128) continue;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) *reinterpret_cast<uint4 *>(sE + il_off(li + 96 * u, c)) = ev[u][c];
       }
       tc::fence_async_shared();
       tc::mbar_arrive(&m->e_full[b]);
       if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int q = li + 96 * k;
-        if (q < 128 * CH) *reinterpret_cast<uint4 *>(sV + v_off<D>(q / CH, q % CH)) = vv[k];
+      for (int u = 0; u < 2; ++u) {
+        if (li + 96 * u >= 128) continue;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) *reinterpret_cast<uint4 *>(sV + v_off<D>(li + 96 * u, c)) = vv[u][c];
       }
       tc::fence_async_shared();
       tc::mbar_arrive(&m->v_full);

@@ -65,8 +65,8 @@ struct TG {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGES = BN >= 256 ? (E16 ? 3 : 4) : (BN >= 128 ? 5 : 6);
-  // bf16 epilogue staging per epilogue warp: 2 output buffers + 1 mask buffer (32 rows x 128 B each)
-  static constexpr int STG_BYTES = E16 ? 4 * 3 * 4096 : 0;
+  // bf16 epilogue staging per epilogue warp: 2 output buffers + 2 mask buffers (32 rows x 128 B each)
+  static constexpr int STG_BYTES = E16 ? 4 * 4 * 4096 : 0;
   static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
   static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
   static constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t *empty = full + T::STAGES;
   uint64_t *tfull = empty + T::STAGES;   // [2]
   uint64_t *tempty = tfull + 2;          // [2]
-  uint64_t *mbar = tempty + 2;           // [4] mask loads, one per epilogue warp
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 4);
+  uint64_t *mbar = tempty + 2;           // [4][2] mask loads, two buffers per epilogue warp
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nm = (M + T::BM - 1) / T::BM, nn = (N + BN - 1) / BN;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(192, 1)
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 4);
     }
-    for (int a = 0; a < 4; ++a) tc::mbar_init(&mbar[a], 1);
+    for (int a = 0; a < 8; ++a) tc::mbar_init(&mbar[a], 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&ta);
     tc::tma_prefetch(&tb);
@@ -206,8 +206,20 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int g = warp & 3;  // TMEM lane group accessible to this warp
-    uint32_t li = 0, ocount = 0, mphase = 0;
+    uint32_t li = 0, ocount = 0;
     float csum[BN / 64 > 0 ? BN / 64 : 1][2] = {};
+    // mask tiles are prefetched one 64-column chunk ahead (two buffers)
+    auto mask_load = [&](int64_t t, int c64, uint32_t q) {
+      if (!E16 || !ep.mask16 || lane != 0 || t >= ntiles) return;
+      int64_t m0, n0, kb0;
+      int nkb_, z_;
+      tile_coords(t, m0, n0, kb0, nkb_, z_);
+      if (n0 + c64 * 64 >= N) return;
+      tc::mbar_expect_tx(&mbar[g * 2 + (q & 1)], 4096);
+      tc::tma_load_2d(sStg + (g * 4 + 2 + (q & 1)) * 4096, &tmask, &mbar[g * 2 + (q & 1)],
+                      (int32_t)(n0 + c64 * 64), (int32_t)(m0 + g * 32));
+    };
+    mask_load(blockIdx.x, 0, 0);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
       int64_t m0, n0, kb0;
       int nkb, z;
@@ -249,31 +261,24 @@ __global__ void __launch_bounds__(192, 1)
         // bf16 epilogue, 64 columns at a time: TMEM -> registers (scale,
         // mask from a TMA-loaded tile) -> swizzled SMEM staging -> TMA store
         const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
-        uint8_t *mst = sStg + (g * 3 + 2) * 4096;
+        const int nch = (int)((N - n0 + 63) / 64) < BN / 64 ? (int)((N - n0 + 63) / 64) : BN / 64;
 #pragma unroll 1
-        for (int c64 = 0; c64 < BN / 64; ++c64) {
+        for (int c64 = 0; c64 < nch; ++c64) {
           const int64_t ncol = n0 + c64 * 64;
-          if (ncol >= N) break;
-          uint8_t *ost = sStg + (g * 3 + (ocount & 1)) * 4096;
-          if (ep.mask16 && lane == 0) {
-            tc::mbar_expect_tx(&mbar[g], 4096);
-            tc::tma_load_2d(mst, &tmask, &mbar[g], (int32_t)ncol, (int32_t)(m0 + g * 32));
-          }
+          uint8_t *ost = sStg + (g * 4 + (ocount & 1)) * 4096;
+          uint8_t *mst = sStg + (g * 4 + 2 + (ocount & 1)) * 4096;
+          // prefetch the next chunk's mask (this tile's next chunk, else the next tile's first)
+          if (c64 + 1 < nch) mask_load(t, c64 + 1, ocount + 1);
+          else mask_load(t + gridDim.x, 0, ocount + 1);
           uint32_t v[64];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w[16];
-            tc::tmem_ld16(dcol + (uint32_t)(c64 * 64 + q * 16), w);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[q * 16 + j] = w[j];
-          }
+          tc::tmem_ld32(dcol + (uint32_t)(c64 * 64), *reinterpret_cast<uint32_t (*)[32]>(&v[0]));
+          tc::tmem_ld32(dcol + (uint32_t)(c64 * 64 + 32), *reinterpret_cast<uint32_t (*)[32]>(&v[32]));
+          tc::tmem_ld_wait();
           float x[64];
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
           if (ep.mask16) {
-            tc::mbar_wait(&mbar[g], mphase & 1);
-            ++mphase;
+            tc::mbar_wait(&mbar[g * 2 + (ocount & 1)], (ocount >> 1) & 1);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const uint4 mv = *reinterpret_cast<const uint4 *>(mst + tc::sw128_off(lane, c));

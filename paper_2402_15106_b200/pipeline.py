@@ -53,52 +53,84 @@ def sample_nodes(n_points, s, seed, device):
 
 
 def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks):
-    """Partition the sampled set and build the local arrays of the given ranks."""
+    """Partition the sampled set and build the local arrays of the given ranks.
+    All ranks' plans are enqueued first and their sizes read back with one
+    host synchronisation."""
     dev = coords_s.device
     n, dim = coords_s.shape
     owner = torch.empty(n, dtype=torch.int32, device=dev)
     boxes = torch.empty(nparts * 2 * dim, dtype=torch.float32, device=dev)
     internal = torch.empty(nparts * 2 * dim, dtype=torch.uint8, device=dev)
-    counts = torch.empty(4 + 2 * (nparts + 1), dtype=torch.int64, device=dev)
-    out = []
-    for q in ranks:
+    nc = 4 + 2 * (nparts + 1)
+    ranks = list(ranks)
+    counts = torch.empty((len(ranks), nc), dtype=torch.int64, device=dev)
+    bufs = []
+    for t, q in enumerate(ranks):
         local_rows = torch.empty(n, dtype=torch.int64, device=dev)
         send_idx = torch.empty(max(1, n * max(1, nparts - 1)), dtype=torch.int32, device=dev)
-        h = L.partition(coords_s, gid_s, nparts, overlap_l, radius, q, owner, boxes, internal, local_rows, counts,
-                        send_idx, sync=True)
+        L.partition(coords_s, gid_s, nparts, overlap_l, radius, q, owner, boxes, internal, local_rows, counts[t],
+                    send_idx, sync=False)
+        bufs.append((local_rows, send_idx))
+    hcounts = counts.cpu().tolist()  # the one synchronisation
+    out = []
+    for t, q in enumerate(ranks):
+        h = hcounts[t]
+        local_rows, send_idx = bufs[t]
         nd, nn, nh, ns = h[0], h[1], h[2], h[3]
         halo_ptr = h[4:4 + nparts + 1]
         send_ptr = h[4 + nparts + 1:4 + 2 * (nparts + 1)]
         n_loc = nd + nn + nh
-        lr = local_rows[:n_loc].clone()
+        lr = local_rows[:n_loc]
         c = torch.empty((n_loc, dim), dtype=torch.float32, device=dev)
         L.gather_rows(coords_s, lr, c)
         g = torch.empty(n_loc, dtype=torch.int64, device=dev)
         L.gather_rows(gid_s, lr, g)
         a = torch.empty((n_loc, attr_s.shape[1]), dtype=torch.float32, device=dev)
         L.gather_rows(attr_s, lr, a)
-        out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[:max(ns, 0)].clone(), c, g, a))
+        out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[:max(ns, 0)], c, g, a))
     return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
 
 
-def build_graph(sd: Subdomain, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
+def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
+    """build_graph for several sub-domains with one host synchronisation: all
+    radius graphs are enqueued (capacity n_own * n_e), then the edge counts and
+    the host copies of row_ptr are read back together, then edge attributes
+    and CSC views are enqueued."""
+    if not subs:
+        return subs
+    dev = subs[0].coords.device
+    cols = []
+    for sd in subs:
+        sd.row_ptr = torch.empty(sd.n_own + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(max(1, sd.n_own * n_e), dtype=torch.int32, device=dev)
+        L.radius_graph(sd.coords, sd.gid, sd.n_own, r, n_e, seed, sd.row_ptr, col, want_count=False)
+        cols.append(col)
+    host = torch.cat([sd.row_ptr for sd in subs]).cpu()  # the one synchronisation
+    off = 0
+    for sd, col in zip(subs, cols):
+        sd.row_ptr_host = host[off:off + sd.n_own + 1]
+        off += sd.n_own + 1
+        E = int(sd.row_ptr_host[-1])
+        sd.col_idx = col[:E]
+        sd.n_edges = E
+        _edge_arrays(sd, edge_mode, want_f32, want_bf16)
+    return subs
+
+
+def _edge_arrays(sd, edge_mode, want_f32, want_bf16):
     dev = sd.coords.device
-    n_own = sd.n_own
-    sd.row_ptr = torch.empty(n_own + 1, dtype=torch.int64, device=dev)
-    cap = max(1, n_own * n_e)
-    col = torch.empty(cap, dtype=torch.int32, device=dev)
-    E = L.radius_graph(sd.coords, sd.gid, n_own, r, n_e, seed, sd.row_ptr, col)
-    sd.col_idx = col[:E]
-    sd.n_edges = E
-    sd.row_ptr_host = sd.row_ptr.cpu()
+    E = sd.n_edges
     de = (sd.coords.shape[1] + sd.attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
     sd.e32 = torch.empty((max(E, 1), de), dtype=torch.float32, device=dev) if want_f32 else None
     sd.e16 = torch.zeros((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None
-    L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, n_own, sd.e32, sd.e16)
+    L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, sd.n_own, sd.e32, sd.e16)
     sd.csc_perm = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)
     L.csc(sd.col_idx, sd.n_loc, sd.csc_perm, sd.csc_ptr)
-    return sd
+
+
+def build_graph(sd: Subdomain, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
+    return build_graphs([sd], r, n_e, seed, edge_mode, want_f32, want_bf16)[0]
 
 
 def halo_exchange_loopback(subs, values, dtype):

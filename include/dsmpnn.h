@@ -228,6 +228,17 @@ dsmpnn_status dsmpnn_halo_exchange_loopback(int32_t nparts, void *const *values,
                                             const int64_t *const *send_ptr, const int32_t *const *send_idx,
                                             int32_t width, int32_t dtype, void *stream);
 
+/* Loopback REVERSE_ADD among P virtual ranks on ONE device (SURVEY §8(f) f2,
+ * reading R16): the transpose of dsmpnn_halo_exchange_loopback for fp32
+ * gradients.  For p = 0..P-1 and q ascending (q != p):
+ *   values[p][send_idx_p[send_ptr_p[q] + t]] += values[q][halo_ptr_q[p] + t]
+ * so a halo row's gradient reaches the row it was copied from.  Halo rows are
+ * only read; the order of the additions is fixed (deterministic).  Same
+ * argument layout as dsmpnn_halo_exchange_loopback; values are float32. */
+dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *values, const int64_t *const *halo_ptr,
+                                               const int64_t *const *send_ptr, const int32_t *const *send_idx,
+                                               int32_t width, void *stream);
+
 /* --------------------------------------------------------------- GEMM --- */
 /* Dense bf16 GEMM on the tcgen05 tensor cores, fp32 accumulate:
  *   C[M x N] (+)= A[M x K] . B[K x N]

@@ -44,3 +44,70 @@ def ds_forward(desc, W, ranks, v_global_rows, n_layers):
             new_vals.append(nv)
         vals = halo.halo_forward(ranks, new_vals)
     return outs
+
+
+DETACH, REVERSE_ADD = 0, 1
+
+
+def ds_forward_backward(desc, W, ranks, v_global_rows, G_global_rows, n_layers, mode=DETACH):
+    """Decomposed forward (as ds_forward) then backward over n_layers, with the
+    halo gradient handled per reading R16 / SURVEY §8(f) f2:
+
+      DETACH       received halo values are constants: the gradient reaching a
+                   halo row is dropped (Alg. 1 :417 local backprop);
+      REVERSE_ADD  after each layer's backward the halo rows' gradients are
+                   added to their owners' rows (halo_reverse_add, q ascending),
+                   the transpose of the forward halo copy, so the decomposed
+                   gradient equals the undecomposed one.
+
+    G_global_rows(rows) -> dL/dout of the last layer for those sampled rows
+    (owned rows are used).  Returns the weight gradients summed over ranks
+    (Alg. 1 :418)."""
+    vals = [np.asarray(v_global_rows(q["local_rows"]), dtype=np.float64) for q in ranks]
+    acts = [vals]
+    for _ in range(n_layers):
+        outs = [layer.layer_fwd(desc, W, v, q["e"], q["row_ptr"], q["col_idx"])[0] for q, v in zip(ranks, vals)]
+        new_vals = []
+        for v, o in zip(vals, outs):
+            nv = v.copy()
+            nv[: len(o)] = o
+            new_vals.append(nv)
+        vals = halo.halo_forward(ranks, new_vals)
+        acts.append(vals)
+    grads = None
+    gouts = [np.asarray(G_global_rows(q["local_rows"][: len(q["row_ptr"]) - 1]), dtype=np.float64) for q in ranks]
+    for layer_i in reversed(range(n_layers)):
+        dvs = []
+        for q, v, g_out in zip(ranks, acts[layer_i], gouts):
+            dv, _, g = layer.layer_bwd(desc, W, v, q["e"], q["row_ptr"], q["col_idx"], g_out, want_de=False)
+            dvs.append(dv)
+            if grads is None:
+                grads = {n: np.zeros_like(x) for n, x in g.items()}
+            for n in grads:
+                grads[n] += g[n]
+        if mode == REVERSE_ADD:
+            dvs = halo.halo_reverse_add(ranks, dvs)
+        gouts = [dv[: len(q["row_ptr"]) - 1] for q, dv in zip(ranks, dvs)]
+    return grads
+
+
+def undecomposed_forward_backward(desc, W, coords, gid, attr, r, n_e, seed, edge_mode, v, G, n_layers):
+    """The same L-layer chain on the whole sampled set as one domain (S-MPNN):
+    summed weight gradients of sum_i G_i . out_i^(L)."""
+    x = np.asarray(coords, np.float32)
+    n = len(x)
+    rp, ci = graph.radius_graph(x, np.asarray(gid, np.int64), n, r, n_e, seed)
+    e = features.edge_features(edge_mode, x, np.asarray(attr, np.float32), features.dst_of_edges(rp), ci)
+    acts = [np.asarray(v, np.float64)]
+    for _ in range(n_layers):
+        acts.append(layer.layer_fwd(desc, W, acts[-1], e, rp, ci)[0])
+    g_out = np.asarray(G, np.float64)
+    grads = None
+    for layer_i in reversed(range(n_layers)):
+        dv, _, g = layer.layer_bwd(desc, W, acts[layer_i], e, rp, ci, g_out, want_de=False)
+        if grads is None:
+            grads = {k: np.zeros_like(x_) for k, x_ in g.items()}
+        for k in grads:
+            grads[k] += g[k]
+        g_out = dv
+    return grads

@@ -89,6 +89,8 @@ _f = {
     "halo_scatter_add": _sig("halo_scatter_add", P, P, I64, I32, P, P),
     "halo_exchange_loopback": _sig("halo_exchange_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
                                    C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, P),
+    "halo_reverse_add_loopback": _sig("halo_reverse_add_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
+                                      C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, P),
     "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
     "probe_begin": _sig("probe_begin", I32, I32),
     "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
@@ -267,6 +269,19 @@ def halo_exchange_loopback(values_list, halo_ptr_list, send_ptr_list, send_idx_l
     spp = (C.POINTER(I64) * P_)(*[C.cast(s, C.POINTER(I64)) for s in sp])
     sidx = (P * P_)(*[s.data_ptr() for s in send_idx_list])
     _call("halo_exchange_loopback", P_, vals, hpp, spp, sidx, width, dtype, _stream(stream))
+
+
+def halo_reverse_add_loopback(values_list, halo_ptr_list, send_ptr_list, send_idx_list, stream=None):
+    """fp32 gradients: values[p][send rows to q] += values[q][halo slice from p], q ascending."""
+    P_ = len(values_list)
+    width = values_list[0].shape[1]
+    vals = (P * P_)(*[v.data_ptr() for v in values_list])
+    hp = [(I64 * (P_ + 1))(*[int(x) for x in h]) for h in halo_ptr_list]
+    sp = [(I64 * (P_ + 1))(*[int(x) for x in s]) for s in send_ptr_list]
+    hpp = (C.POINTER(I64) * P_)(*[C.cast(h, C.POINTER(I64)) for h in hp])
+    spp = (C.POINTER(I64) * P_)(*[C.cast(s, C.POINTER(I64)) for s in sp])
+    sidx = (P * P_)(*[s.data_ptr() for s in send_idx_list])
+    _call("halo_reverse_add_loopback", P_, vals, hpp, spp, sidx, width, _stream(stream))
 
 
 def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=None, accumulate=False,

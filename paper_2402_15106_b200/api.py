@@ -8,8 +8,11 @@ encoder/decoder and the optimiser are outside the hot path.
 
 A process owns one or more sub-domains ("virtual ranks"); halos between
 sub-domains on the same device are device copies, halos between processes go
-through torch.distributed (NCCL) point-to-point.  Received halo values are
-detached (reading R16): the backward drops gradients of halo rows.
+through torch.distributed (NCCL) point-to-point.  Gradients through halo
+rows (reading R16): DETACH (default, the paper's local backprop) drops them;
+REVERSE_ADD adds them to the owning rows after every
+layer's backward, which makes the decomposed gradient equal the
+undecomposed one.
 """
 from dataclasses import dataclass
 
@@ -20,6 +23,7 @@ from . import _lib as L
 from . import pipeline
 
 GNAMES = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
+DETACH, REVERSE_ADD = 0, 1
 
 
 @dataclass
@@ -41,6 +45,7 @@ class StepConfig:
     act: int = L.ACT_RELU
     seed_sampling: int = 0
     seed_capping: int = 0
+    grad_mode: int = DETACH
 
 
 def parts_of_process(nparts, world, rank):
@@ -102,6 +107,13 @@ class HotPath:
         else:
             pipeline.halo_exchange_mixed(self.subs, vals, dtype, self.proc_of, self.rank, self.group)
 
+    def halo_reverse(self, grads):
+        """REVERSE_ADD of fp32 gradients (f2) for every local sub-domain."""
+        if self.world == 1:
+            pipeline.halo_reverse_loopback(self.subs, grads)
+        else:
+            pipeline.halo_reverse_mixed(self.subs, grads, self.proc_of, self.rank, self.group)
+
     def forward_backward(self, v0, G):
         """v0: [s x d] initial latent of the sampled nodes (sampled order);
         G: [s x d] dL/d(last layer output) (rows of owned nodes are used).
@@ -132,7 +144,7 @@ class HotPath:
                 nxt.append(nv)
             self.halo(nxt, L.BF16 if lowp else L.F32)
             acts.append(nxt)
-        # backward: DETACH halo rows (R16)
+        # backward: DETACH or REVERSE_ADD halo rows (R16, f2)
         gouts = []
         for sd in self.subs:
             g = torch.empty((sd.n_own, c.d), dtype=torch.float32, device=self.dev)
@@ -145,11 +157,14 @@ class HotPath:
                 bws = self._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
                 gv = torch.zeros((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
                 e = sd.e16 if lowp else sd.e32
+                # the input gradient of the first layer is not needed (no scatter / root term)
                 L.layer_bwd(desc, self.W, self.packed, acts[layer][q], e, sd.row_ptr, sd.col_idx, sd.csc_perm,
-                            sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, gouts[q], gv, None, self.grads, ws, bws,
-                            row_ptr_host=sd.row_ptr_host)
-                new_g.append(gv[: sd.n_own])
-            gouts = new_g
+                            sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, gouts[q], gv if layer > 0 else None, None,
+                            self.grads, ws, bws, row_ptr_host=sd.row_ptr_host)
+                new_g.append(gv)
+            if c.grad_mode == REVERSE_ADD:
+                self.halo_reverse(new_g)
+            gouts = [gv[: sd.n_own] for gv, sd in zip(new_g, self.subs)]
         if self.world > 1:
             self._allreduce_grads()
         return self.grads

@@ -242,6 +242,22 @@ dsmpnn_status dsmpnn_halo_exchange_loopback(int32_t nparts, void *const *values,
   return DSMPNN_OK;
 }
 
+dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *values, const int64_t *const *halo_ptr,
+                                               const int64_t *const *send_ptr, const int32_t *const *send_idx,
+                                               int32_t width, void *stream) {
+  DS_CHECK_ARG(nparts >= 1 && width > 0, DSMPNN_ERR_INVALID_ARG, "halo_reverse_add_loopback: nparts / width");
+  for (int p = 0; p < nparts; ++p)
+    for (int q = 0; q < nparts; ++q) {
+      if (q == p) continue;
+      int64_t s0 = send_ptr[p][q], s1 = send_ptr[p][q + 1];
+      int64_t a = halo_ptr[q][p], b = halo_ptr[q][p + 1];
+      DS_CHECK_ARG(b - a == s1 - s0, DSMPNN_ERR_SHAPE, "halo_reverse_add_loopback: %d<-%d sizes differ", p, q);
+      if (b == a) continue;
+      DS_TRY(dsmpnn_halo_scatter_add(values[q] + a * width, send_idx[p] + s0, b - a, width, values[p], stream));
+    }
+  return DSMPNN_OK;
+}
+
 dsmpnn_status dsmpnn_csc_workspace_size(int64_t n_edges, int64_t n_loc, size_t *bytes) {
   size_t tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int32_t *)nullptr, (int32_t *)nullptr,

@@ -139,6 +139,64 @@ def halo_exchange_loopback(subs, values, dtype):
                              [s.send_idx for s in subs], dtype)
 
 
+def halo_reverse_loopback(subs, grads):
+    """REVERSE_ADD among virtual ranks on this device:
+    fp32 gradients of halo rows are added to the rows they were copied from."""
+    L.halo_reverse_add_loopback(grads, [s.halo_ptr for s in subs], [s.send_ptr for s in subs],
+                                [s.send_idx for s in subs])
+
+
+def halo_reverse_mixed(subs, grads, proc_of, my_proc, group=None, scatter_add=None):
+    """REVERSE_ADD when sub-domains are spread over processes: the halo slice
+    of q received from p is sent back to p's process (NCCL send/recv, issued in
+    (destination, source) order on both sides), then every owner adds the
+    slices into its send rows with q ascending (the oracle's order).  fp32.
+    `scatter_add(inp, rows, values)` defaults to the library kernel."""
+    import torch.distributed as dist
+    if scatter_add is None:
+        scatter_add = L.halo_scatter_add
+    local = {sd.rank: (sd, g) for sd, g in zip(subs, grads)}
+    nparts = subs[0].nparts
+    ops, recv = [], {}
+    for p_id in range(nparts):          # owner of the rows
+        for q_id in range(nparts):      # holder of the halo copy
+            if p_id == q_id:
+                continue
+            own_local, halo_local = p_id in local, q_id in local
+            if own_local and not halo_local:
+                psd, _ = local[p_id]
+                s0, s1 = psd.send_ptr[q_id], psd.send_ptr[q_id + 1]
+                if s1 > s0:
+                    buf = torch.empty((s1 - s0, grads[0].shape[1]), dtype=torch.float32, device=grads[0].device)
+                    recv[(p_id, q_id)] = buf
+                    ops.append(dist.P2POp(dist.irecv, buf, proc_of[q_id], group))
+            elif halo_local and not own_local:
+                qsd, qg = local[q_id]
+                a, b = qsd.halo_ptr[p_id], qsd.halo_ptr[p_id + 1]
+                if b > a:
+                    ops.append(dist.P2POp(dist.isend, qg[a:b].contiguous(), proc_of[p_id], group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for p_id in range(nparts):
+        if p_id not in local:
+            continue
+        psd, pg = local[p_id]
+        for q_id in range(nparts):
+            if q_id == p_id:
+                continue
+            s0, s1 = psd.send_ptr[q_id], psd.send_ptr[q_id + 1]
+            if s1 <= s0:
+                continue
+            if q_id in local:
+                qsd, qg = local[q_id]
+                a, b = qsd.halo_ptr[p_id], qsd.halo_ptr[p_id + 1]
+                src = qg[a:b]
+            else:
+                src = recv[(p_id, q_id)]
+            scatter_add(src, psd.send_idx[s0:s1], pg)
+
+
 def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gather=None):
     """FORWARD halo refresh when sub-domains are spread over processes.
 

@@ -62,13 +62,23 @@ def _worker(rank, port, q):
         want = ohalo.halo_forward(ranks, vals)
         ok_halo = all(np.array_equal(t.numpy(), want[p]) for t, p in zip(tv, mine))
 
+        # REVERSE_ADD (f2): halo slices go back to their owners, added in q order
+        gv = [torch.from_numpy(np.nan_to_num(vals[p]).astype(np.float32)) for p in mine]
+        want_r = ohalo.halo_reverse_add(ranks, [np.nan_to_num(v).astype(np.float64) for v in vals])
+
+        def scatter_add(inp, rows, values):  # test stand-in for the device kernel
+            values.index_add_(0, rows.long(), inp)
+
+        pipeline.halo_reverse_mixed(subs, gv, proc_of, rank, scatter_add=scatter_add)
+        ok_rev = all(np.allclose(t.numpy(), want_r[p], rtol=1e-6, atol=1e-6) for t, p in zip(gv, mine))
+
         # gradient sum over processes
         names = api.GNAMES
         grads = {n: torch.full((3, 2), float(rank + 1) * (i + 1)) for i, n in enumerate(names)}
         stub = types.SimpleNamespace(grads=grads, group=None)
         api.HotPath._allreduce_grads(stub)
         ok_red = all(torch.equal(grads[n], torch.full((3, 2), 3.0 * (i + 1))) for i, n in enumerate(names))
-        q.put((rank, ok_halo, ok_red))
+        q.put((rank, ok_halo and ok_rev, ok_red))
     finally:
         dist.destroy_process_group()
 
@@ -88,7 +98,7 @@ def test_halo_and_allreduce_world2():
         p.join(60)
         assert p.exitcode == 0
     for rank, ok_halo, ok_red in sorted(res):
-        assert ok_halo, f"rank {rank}: halo refresh differs from oracle.halo.halo_forward"
+        assert ok_halo, f"rank {rank}: halo refresh / reverse add differs from oracle.halo"
         assert ok_red, f"rank {rank}: gradient all-reduce wrong"
 
 

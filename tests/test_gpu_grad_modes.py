@@ -1,0 +1,78 @@
+"""SURVEY §8(f) f2 (exact-gradient DS) and reading R16 on the GPU path: the
+full hot-path step (HotPath: sample, partition, graphs, L layers forward with
+halo refresh, L layers backward) on 4 virtual ranks of one device, weight
+gradients compared with the fp64 oracle's decomposed backward in both modes
+(DETACH, REVERSE_ADD) and, for REVERSE_ADD, with the undecomposed chain."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import decomp, sample
+from oracle.layer import LayerDesc
+from paper_2402_15106_b200 import synth
+from gpu_util import cuda, nerr
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
+
+
+def _case(seed=61, n=600, dim=2, d=16, k=32, L=3, P=4, r=0.11, n_e=16):
+    g = np.random.default_rng(seed)
+    x = g.random((n, dim)).astype(np.float32)
+    a = g.normal(size=(n, 1)).astype(np.float32)
+    W = synth.weights(dim + 1, d, d, k, salt=seed)
+    v0 = g.normal(size=(n, d)).astype(np.float32)
+    G = g.normal(size=(n, d)).astype(np.float32)
+    return dict(x=x, a=a, W=W, v0=v0, G=G, n=n, dim=dim, d=d, k=k, L=L, P=P, r=r, n_e=n_e)
+
+
+def _gpu(c, mode, dtype):
+    from paper_2402_15106_b200 import _lib as Lib
+    from paper_2402_15106_b200.api import HotPath, StepConfig
+    l = c["r"] * (1 + 2 ** -12)
+    sc = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
+                    n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
+                    seed_sampling=3, seed_capping=5, grad_mode=mode)
+    dev = cuda()
+    hp = HotPath(sc, c["W"], dev)
+    ids = sample.sample(c["n"], c["n"], 3)  # identity sample (s = N), sampled order = id order
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    grads = hp.step(T(c["x"]), T(c["a"]), T(c["v0"][ids]), T(c["G"][ids]))
+    torch.cuda.synchronize()
+    return {n: grads[n].cpu().numpy() for n in NAMES}
+
+
+def _oracle(c, mode, P=None):
+    ids = sample.sample(c["n"], c["n"], 3)
+    x, a = c["x"][ids], c["a"][ids]
+    l = c["r"] * (1 + 2 ** -12)
+    _, _, _, ranks = decomp.build_local(x, ids.astype(np.int64), a, P or c["P"], l, c["r"], c["n_e"], 5, "diff")
+    desc = LayerDesc(c["dim"] + 1, c["d"], c["d"], c["k"], 2, 1)
+    v0, G = c["v0"][ids], c["G"][ids]
+    return decomp.ds_forward_backward(desc, c["W"], ranks, lambda rows: v0[rows], lambda rows: G[rows], c["L"], mode)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2402_15106_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("mode", [decomp.DETACH, decomp.REVERSE_ADD], ids=["detach", "reverse_add"])
+def test_step_gradients_match_oracle_f32(lib, mode):
+    c = _case()
+    got = _gpu(c, mode, 0)
+    want = _oracle(c, mode)
+    for n in NAMES:
+        assert nerr(got[n], want[n]) <= 1e-5, n
+
+
+def test_reverse_add_equals_undecomposed_and_detach_does_not(lib):
+    c = _case(seed=62)
+    got = _gpu(c, decomp.REVERSE_ADD, 0)
+    single = _oracle(c, decomp.REVERSE_ADD, P=1)
+    for n in NAMES:
+        assert nerr(got[n], single[n]) <= 1e-5, n
+    det = _gpu(c, decomp.DETACH, 0)
+    assert max(nerr(det[n], single[n]) for n in NAMES) > 1e-3

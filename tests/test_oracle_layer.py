@@ -321,3 +321,40 @@ def test_act_round_only_changes_activations():
     desc.act_round = "bf16"
     b = layer.layer_fwd(desc, W, v, e, rp, ci)[0]
     assert np.array_equal(a, b)
+
+
+def _ds_grads(P, L, mode, seed=51, dim=2):
+    x, gid, attr, r, desc, W, vg = _decomp_case(seed, P, 1, dim)
+    G = np.random.default_rng(seed + 1).normal(size=vg.shape)
+    l = r * (1 + 2 ** -12)
+    _, _, _, ranks = decomp.build_local(x, gid, attr, P, l, r, 8, 5, "diff")
+    return decomp.ds_forward_backward(desc, W, ranks, lambda rows: vg[rows], lambda rows: G[rows], L, mode), \
+        (x, gid, attr, r, desc, W, vg, G)
+
+
+def _close(a, b, tol=1e-10):
+    return all(np.allclose(a[n], b[n], rtol=tol, atol=tol * max(1.0, np.abs(b[n]).max())) for n in a)
+
+
+@pytest.mark.parametrize("P,L", [(2, 2), (4, 3)])
+def test_ds_reverse_add_gradients_equal_undecomposed(P, L):
+    # with REVERSE_ADD (the transpose of the forward halo copy)
+    # the decomposed weight gradients equal the single-domain ones for any depth
+    g_ds, case = _ds_grads(P, L, decomp.REVERSE_ADD)
+    g_1, _ = _ds_grads(1, L, decomp.REVERSE_ADD)
+    assert _close(g_ds, g_1)
+    # and the single-domain chain written out directly (no partition machinery)
+    x, gid, attr, r, desc, W, vg, G = case
+    g_plain = decomp.undecomposed_forward_backward(desc, W, x, gid, attr, r, 8, 5, "diff", vg, G, L)
+    assert _close(g_plain, g_1)
+
+
+def test_ds_detach_exact_at_one_layer_only():
+    # R16: DETACH drops the halo rows' gradient; it is exact for one layer
+    # (Alg. 1 :417 local backprop) and generically not for two
+    g1_ds, _ = _ds_grads(4, 1, decomp.DETACH)
+    g1_ref, _ = _ds_grads(1, 1, decomp.DETACH)
+    assert _close(g1_ds, g1_ref)
+    g2_ds, _ = _ds_grads(4, 2, decomp.DETACH)
+    g2_ref, _ = _ds_grads(1, 2, decomp.DETACH)
+    assert not _close(g2_ds, g2_ref, 1e-6)

@@ -260,20 +260,25 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t IDESC1 = tc::idesc_bf16(128, KH, false, false);
       constexpr uint32_t IDESC2 = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t IDESC_S = tc::idesc_bf16(128, D, true, true);
-      for (uint32_t t = 0;; ++t) {
+      // MMA1 of tile t: z1 = E W1^T (one K=16 step) into TMEM region t & 1
+      auto mma1 = [&](uint32_t t) -> bool {
         const int b = t & 1;
-        const uint32_t ph = (t >> 1) & 1, p1 = t & 1;
-        const TileDesc2 *dsc = &m->desc[b];
-        tc::mbar_wait(&m->e_full[b], ph);
-        if (!dsc->more) break;
+        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+        if (!m->desc[b].more) return false;
         if (t >= 2) tc::mbar_wait(&m->region_free[b], ((t >> 1) - 1) & 1);
         tc::tc_fence_after();
-        const uint32_t r = tmem + b * 256;
-        // MMA1: z1 = E W1^T (one K=16 step)
-        tc::mma_bf16_ss(r, tc::sdesc(aE, 128, 256, tc::kSwNone),
+        tc::mma_bf16_ss(tmem + b * 256, tc::sdesc(aE, 128, 256, tc::kSwNone),
                         tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC1, 0u);
         tc::mma_commit(&m->d1_full[b]);
         tc::mma_commit(&m->e_empty);
+        return true;
+      };
+      bool more = mma1(0);
+      for (uint32_t t = 0; more; ++t) {
+        const int b = t & 1;
+        const uint32_t p1 = t & 1;
+        const TileDesc2 *dsc = &m->desc[b];
+        const uint32_t r = tmem + b * 256;
         // MMA2: z2 = a1 W2^T in two N halves.  Half 0 (kappa 0..127) goes to
         // columns 128..255, whose z1 the epilogue drains first (a1 blocks 2, 3),
         // and consumes a1 K-blocks in the order they arrive (2, 3, 0, 1); half 1
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(512, 1)
         tc::mma_commit(&m->v_empty);
         tc::mma_commit(&m->ah_free);
         tc::mbar_arrive(&m->desc_free[b]);
+        more = mma1(t + 1);
       }
     }
     __syncwarp();
@@ -332,28 +338,27 @@ __global__ void __launch_bounds__(512, 1)
       if (!m->desc[b].more) break;
       const uint32_t r = tmem + b * 256 + lane_off;
       tc::mbar_wait(&m->d1_full[b], ph);
-      if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
       tc::tc_fence_after();
       // a1 = relu(z1 + b1) -> AH; group 1 drains blocks 3, 2 (columns MMA2
-      // half 0 overwrites first), group 0 blocks 0, 1
+      // half 0 overwrites first), group 0 blocks 0, 1.  The first block is
+      // computed into registers while the previous tile's S MMAs still read AH.
 #pragma unroll 1
       for (int jj = 0; jj < 2; ++jj) {
         const int j = cg == 1 ? 3 - jj : jj;
         uint8_t *blk = sAH + j * (128 * 128);
+        uint32_t x[64], pk[32];
+        tc::tmem_ld32(r + j * 64, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
+        tc::tmem_ld32(r + j * 64 + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
+        tc::tmem_ld_wait();
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c0 = j * 64 + cc * 16;
-          uint32_t x[16];
-          tc::tmem_ld16(r + c0, x);
-          tc::tmem_ld_wait();
-          uint32_t pk[8];
+        for (int q = 0; q < 32; ++q)
+          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b1[j * 64 + 2 * q], 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + m->b1[j * 64 + 2 * q + 1], 0.f));
+        if (jj == 0 && t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b1[c0 + 2 * q], 0.f),
-                                  fmaxf(__uint_as_float(x[2 * q + 1]) + m->b1[c0 + 2 * q + 1], 0.f));
-          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        }
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, c)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         tc::fence_async_shared();
         tc::tc_fence_before();
         tc::mbar_arrive(&m->a1_ready[j]);
@@ -364,16 +369,16 @@ __global__ void __launch_bounds__(512, 1)
       tc::mbar_wait(&m->d2_full[0], p1);
       tc::tc_fence_after();
       uint32_t hp[32];
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int k0 = cg * 64 + cc * 16;  // kappa
-        uint32_t x[16];
-        tc::tmem_ld16(r + 128 + k0, x);
+      {
+        const int k0 = cg * 64;  // kappa
+        uint32_t x[64];
+        tc::tmem_ld32(r + 128 + k0, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
+        tc::tmem_ld32(r + 128 + k0 + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          hp[cc * 8 + q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b2[k0 + 2 * q], 0.f),
-                                         fmaxf(__uint_as_float(x[2 * q + 1]) + m->b2[k0 + 2 * q + 1], 0.f));
+        for (int q = 0; q < 32; ++q)
+          hp[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b2[k0 + 2 * q], 0.f),
+                                fmaxf(__uint_as_float(x[2 * q + 1]) + m->b2[k0 + 2 * q + 1], 0.f));
       }
       tc::mbar_wait(&m->d2_full[1], p1);
       tc::tc_fence_after();
@@ -391,20 +396,21 @@ __global__ void __launch_bounds__(512, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready[0]);
       // kappa half 1 (TMEM columns 0..127): group cg takes kappa 128 + 64*cg..
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        const int k0 = 128 + cg * 64 + cc * 16;
-        uint32_t x[16];
-        tc::tmem_ld16(r + k0 - 128, x);
+      {
+        const int k0 = 128 + cg * 64;
+        uint32_t x[64], pk[32];
+        tc::tmem_ld32(r + k0 - 128, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
+        tc::tmem_ld32(r + k0 - 128 + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
         tc::tmem_ld_wait();
-        uint32_t pk[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < 32; ++q)
           pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + m->b2[k0 + 2 * q], 0.f),
                                 fmaxf(__uint_as_float(x[2 * q + 1]) + m->b2[k0 + 2 * q + 1], 0.f));
         uint8_t *blk = sAH + (2 + cg) * (128 * 128);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, cc * 2 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, c)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       tc::fence_async_shared();
       tc::tc_fence_before();

@@ -15,9 +15,10 @@
 //   EPI_A  (warps 4-11) : a1 epilogue + coalesced a1 copy-out (overlaps MMA2),
 //                         h epilogue + [h > 0] bitmask
 //   EPI_B  (warps 12-15): U and dz2 epilogues
-// TMEM: columns 0..255 hold z1 / z2, then U (row g at g*D); columns 256..511
-// hold dH^T (kappa half h at 256 + h*128 + slot).  EPI_B releases the U
-// columns first, so MMA1/epi1 of the next tile overlap the dz2 epilogue.
+// TMEM: columns 0..255 z1 / z2; 256..383 U (row g at 256 + slot(g)*D), then,
+// once EPI_B has drained U, dH^T kappa half 1 (slot s at 256 + s); 384..511
+// dH^T kappa half 0.  z is free once the h epilogue has drained it, so MMA1 of
+// the next tile is issued before this tile's U / dH products.
 #pragma once
 #include "edge_fwd2.cuh"
 
@@ -96,7 +97,8 @@ struct EB2 {
   static constexpr int OFF_W2 = 0;
   static constexpr int OFF_AH = OFF_W2 + 2 * W2BLK;
   static constexpr int OFF_DS = OFF_AH + AH_BYTES;
-  static constexpr int OFF_V = OFF_DS + 2 * DS_BYTES;
+  static constexpr int NDS = NMAX;                 // dS ring slots: every row of a tile resident
+  static constexpr int OFF_V = OFF_DS + NDS * DS_BYTES;
   static constexpr int OFF_W1 = OFF_V + V_BYTES;
   static constexpr int OFF_E = OFF_W1 + W1_BYTES;
   static constexpr int OFF_MASK = OFF_E + E_BYTES;
@@ -105,9 +107,9 @@ struct EB2 {
   struct Misc {
     TileDescB desc[2];
     __nv_bfloat16 brow[2][NMAX][D];  // dS_i[k] of the rows of desc[b]
-    uint64_t e_full[2], desc_free[2], w2_full[2], w2_empty[2], ds_full[2], ds_empty[2];
-    uint64_t e_empty, v_full, v_empty, d1_full, a1_ready, d2_full, h_ready, s_full, u_free, dh_free, ah_free;
-    uint64_t mask_read;
+    uint64_t e_full[2], desc_free[2], w2_full[2], w2_empty[2], ds_full[NMAX], ds_empty[NMAX];
+    uint64_t e_empty, v_full, v_empty, d1_full, a1_ready, d2_full, h_ready, ah_free, mask_read;
+    uint64_t u_full, u_free, dh0_full, dh0_free, dh1_full, dh_free;
     int64_t cur_row, row_end;
     uint32_t tmem;
   };
@@ -155,23 +157,28 @@ __global__ void __launch_bounds__(512, 1)
     m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
     m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&m->e_full[b], 64);
-      tc::mbar_init(&m->desc_free[b], 1 + 8 + 4 + 2);  // MMA, every epilogue warp, TMA-W2, TMA-dS
+      tc::mbar_init(&m->e_full[b], 32);
+      tc::mbar_init(&m->desc_free[b], 1 + 8 + 4 + 2 + 1);  // MMA, epilogue warps, TMA-W2, TMA-dS, v loader
       tc::mbar_init(&m->w2_full[b], 1);
       tc::mbar_init(&m->w2_empty[b], 1);
+    }
+    for (int b = 0; b < NMAX; ++b) {
       tc::mbar_init(&m->ds_full[b], 1);
       tc::mbar_init(&m->ds_empty[b], 1);
     }
     tc::mbar_init(&m->e_empty, 1);
-    tc::mbar_init(&m->v_full, 64);
+    tc::mbar_init(&m->v_full, 32);
     tc::mbar_init(&m->v_empty, 1);
     tc::mbar_init(&m->d1_full, 1);
     tc::mbar_init(&m->a1_ready, 256);
     tc::mbar_init(&m->d2_full, 1);
     tc::mbar_init(&m->h_ready, 256);
     tc::mbar_init(&m->mask_read, 128);
-    tc::mbar_init(&m->s_full, 1);
+    tc::mbar_init(&m->u_full, 1);
     tc::mbar_init(&m->u_free, 128);
+    tc::mbar_init(&m->dh0_full, 1);
+    tc::mbar_init(&m->dh0_free, 128);
+    tc::mbar_init(&m->dh1_full, 1);
     tc::mbar_init(&m->dh_free, 128);
     tc::mbar_init(&m->ah_free, 1);
     tc::fence_mbar_init();
@@ -197,63 +204,79 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t tmem = m->tmem;
 
   if (warp == 0 || warp == 2) {
-    // ============================================================ loader
-    const int li = warp == 0 ? lane : 32 + lane;  // 0..63
+    // ============================================================ loaders
+    // warp 0: tile walker + e rows + dS_i[k] rows; warp 2: v_j rows.  The two
+    // progress independently, so e (and MMA1) of the next tile never wait
+    // for the v buffer, which is released only after the second dH half.
+    constexpr int CH = D / 8;
     for (uint32_t t = 0;; ++t) {
       const int b = t & 1;
       TileDescB *dsc = &m->desc[b];
-      if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
-      if (warp == 0) walk_tile<NMAX>(m, dsc, row_ptr, lane);
-      tc::named_sync(1, 64);
-      const int nn = dsc->nnodes;
-      if (!dsc->more) {
+      if (warp == 0) {
+        if (t >= 2) tc::mbar_wait(&m->desc_free[b], ((t >> 1) - 1) & 1);
+        walk_tile<NMAX>(m, dsc, row_ptr, lane);
+        if (!dsc->more) {
+          tc::mbar_arrive(&m->e_full[b]);
+          break;
+        }
+        TileRegs<NMAX> tr;
+        tr.load(dsc);
+        int32_t pe[4];
+        uint4 ev[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pe[u] = tr.edge(lane + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            ev[u][c] = pe[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe[u] * 16) + c)
+                                  : make_uint4(0, 0, 0, 0);
+        // dS_i[k] rows (the constant term of u_p) for EPI_B
+        for (int q = lane; q < tr.nn * CH; q += 32) {
+          const int g = q / CH, c = q % CH;
+          reinterpret_cast<uint4 *>(&m->brow[b][g][0])[c] =
+              __ldg(reinterpret_cast<const uint4 *>(dS + (dsc->node[g] * (KH + 1) + KH) * D) + c);
+        }
+        if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) *reinterpret_cast<uint4 *>(sE + il_off(lane + 32 * u, c)) = ev[u][c];
+        tc::fence_async_shared();
         tc::mbar_arrive(&m->e_full[b]);
-        break;
+      } else {
+        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
+        if (!dsc->more) break;
+        TileRegs<NMAX> tr;
+        tr.load(dsc);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+        // two rows per lane per batch: index loads, then every row load in flight
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          int32_t cj[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int32_t pe = tr.edge(lane + 32 * (2 * h + u));
+            cj[u] = pe >= 0 ? __ldg(col + pe) : -1;
+          }
+          uint4 vv[2][CH];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              vv[u][c] = cj[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)cj[u] * D) + c)
+                                    : make_uint4(0, 0, 0, 0);
+          if (h == 0 && t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              *reinterpret_cast<uint4 *>(sV + v_off<D>(lane + 32 * (2 * h + u), c)) = vv[u][c];
+        }
+        tc::fence_async_shared();
+        tc::mbar_arrive(&m->v_full);
       }
-      constexpr int CH = D / 8;
-      TileRegs<NMAX> tr;
-      tr.load(dsc);
-      // thread li gathers whole rows of slots li and li + 64: two index loads,
-      // then all row loads in flight at once
-      int32_t pe[2], cj[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) pe[u] = tr.edge(li + 64 * u);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) cj[u] = pe[u] >= 0 ? __ldg(col + pe[u]) : -1;
-      uint4 ev[2][2], vv[2][CH];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          ev[u][c] = pe[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(e16 + (int64_t)pe[u] * 16) + c)
-                                : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int c = 0; c < CH; ++c)
-          vv[u][c] = cj[u] >= 0 ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)cj[u] * D) + c)
-                                : make_uint4(0, 0, 0, 0);
-      }
-      // dS_i[k] rows (the constant term of u_p) for EPI_B
-      for (int q = li; q < nn * CH; q += 64) {
-        const int g = q / CH, c = q % CH;
-        reinterpret_cast<uint4 *>(&m->brow[b][g][0])[c] =
-            __ldg(reinterpret_cast<const uint4 *>(dS + (dsc->node[g] * (KH + 1) + KH) * D) + c);
-      }
-      if (t >= 1) tc::mbar_wait(&m->e_empty, (t - 1) & 1);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) *reinterpret_cast<uint4 *>(sE + il_off(li + 64 * u, c)) = ev[u][c];
-      }
-      tc::fence_async_shared();
-      tc::mbar_arrive(&m->e_full[b]);
-      if (t >= 1) tc::mbar_wait(&m->v_empty, (t - 1) & 1);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) *reinterpret_cast<uint4 *>(sV + v_off<D>(li + 64 * u, c)) = vv[u][c];
-      }
-      tc::fence_async_shared();
-      tc::mbar_arrive(&m->v_full);
     }
   } else if (warp == 3) {
     // ============================================================ TMA producers
@@ -263,28 +286,35 @@ __global__ void __launch_bounds__(512, 1)
         const int b = t & 1;
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!m->desc[b].more) break;
+        tc::mbar_arrive(&m->desc_free[b]);
         for (int j = 0; j < 4; ++j, ++q) {
           const uint32_t s = q & 1, r = q >> 1;
           if (r > 0) tc::mbar_wait(&m->w2_empty[s], (r - 1) & 1);
           tc::mbar_expect_tx(&m->w2_full[s], C::W2BLK);
           tc::tma_load_2d(sW2 + s * C::W2BLK, &tW2, &m->w2_full[s], j * 64, 0);
         }
-        tc::mbar_arrive(&m->desc_free[b]);
       }
-    } else if (lane == 16) {  // dS_i tiles, one per row, 2-slot ring
+    } else if (lane == 16) {  // dS_i tiles, one per row, NMAX-slot ring
       uint32_t q = 0;
       for (uint32_t t = 0;; ++t) {
         const int b = t & 1;
         const TileDescB *dsc = &m->desc[b];
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!dsc->more) break;
-        for (int g = 0; g < dsc->nnodes; ++g, ++q) {
-          const uint32_t s = q & 1, r = q >> 1;
+        const int nn = dsc->nnodes;
+        int64_t node[NMAX];
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) node[g] = g < nn ? dsc->node[g] : 0;
+        tc::mbar_arrive(&m->desc_free[b]);
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) {
+          if (g >= nn) break;
+          const uint32_t s = q % C::NDS, r = q / C::NDS;
           if (r > 0) tc::mbar_wait(&m->ds_empty[s], (r - 1) & 1);
           tc::mbar_expect_tx(&m->ds_full[s], C::DS_BYTES);
-          tc::tma_load_2d(sDS + s * C::DS_BYTES, &tDS, &m->ds_full[s], 0, (int32_t)(dsc->node[g] * (KH + 1)));
+          tc::tma_load_2d(sDS + s * C::DS_BYTES, &tDS, &m->ds_full[s], 0, (int32_t)(node[g] * (KH + 1)));
+          ++q;
         }
-        tc::mbar_arrive(&m->desc_free[b]);
       }
     }
     __syncwarp();
@@ -294,23 +324,16 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aDS = tc::smem_u32(sDS),
                      aV = tc::smem_u32(sV), aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
       constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
-      constexpr uint32_t IDESC_U = tc::idesc_bf16(128, D, false, true);
+      constexpr uint32_t IDESC_U = tc::idesc_bf16(128, C::NDS * D, false, true);
       uint32_t w2q = 0, dsq = 0;
-      for (uint32_t t = 0;; ++t) {
-        const int b = t & 1;
-        const uint32_t p1 = t & 1;
-        const TileDescB *dsc = &m->desc[b];
-        tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
-        if (!dsc->more) break;
-        if (t >= 1) tc::mbar_wait(&m->u_free, (t - 1) & 1);  // columns 0..255 drained
-        tc::tc_fence_after();
-        // MMA1: z1 = E W1^T
+      auto mma1 = [&]() {  // z1 = E W1^T into columns 0..255
         tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone),
                         IDESC_MLP, 0u);
         tc::mma_commit(&m->d1_full);
         tc::mma_commit(&m->e_empty);
-        // MMA2: z2 = a1 W2^T  (W2 streamed by K block)
-        tc::mbar_wait(&m->a1_ready, p1);
+      };
+      auto mma2 = [&](uint32_t t) {  // z2 = a1 W2^T (W2 streamed by K block)
+        tc::mbar_wait(&m->a1_ready, t & 1);
         tc::tc_fence_after();
         for (int j = 0; j < 4; ++j, ++w2q) {
           const uint32_t s = w2q & 1;
@@ -325,40 +348,94 @@ __global__ void __launch_bounds__(512, 1)
           tc::mma_commit(&m->w2_empty[s]);
         }
         tc::mma_commit(&m->d2_full);
-        // per row: dH^T (columns 256 + h*128 + slot) and U (columns g*D)
-        tc::mbar_wait(&m->v_full, p1);
-        tc::mbar_wait(&m->h_ready, p1);
-        if (t >= 1) tc::mbar_wait(&m->dh_free, (t - 1) & 1);
+      };
+      tc::mbar_wait(&m->e_full[0], 0);
+      bool more = m->desc[0].more;
+      if (more) {
         tc::tc_fence_after();
-        const int nn = dsc->nnodes;
-        for (int g = 0; g < nn; ++g, ++dsq) {
-          const uint32_t s = dsq & 1;
-          tc::mbar_wait(&m->ds_full[s], (dsq >> 1) & 1);
-          tc::tc_fence_after();
-          const uint32_t ds = aDS + s * C::DS_BYTES;
-          const int s0 = dsc->slot0[g];
-          const int ns = (dsc->deg[g] + 15) & ~15;
-          const uint32_t idesc_h = tc::idesc_bf16(128, ns, false, false);
-          for (int h = 0; h < 2; ++h) {
+        mma1();
+        mma2(0);
+      }
+      for (uint32_t t = 0; more; ++t) {
+        const int b = t & 1, nb = (t + 1) & 1;
+        const uint32_t p1 = t & 1;
+        TileRegs<NMAX> tr;
+        tr.load(&m->desc[b]);
+        tc::mbar_arrive(&m->desc_free[b]);
+        tc::mbar_wait(&m->v_full, p1);
+        tc::mbar_wait(&m->h_ready, p1);  // z2 drained: z is free for the next tile
+        tc::tc_fence_after();
+        // next tile's MMA1 now if its edge tile is already loaded (never blocks here)
+        bool next_known = false, next_more = false;
+        if (tc::mbar_test(&m->e_full[nb], ((t + 1) >> 1) & 1)) {
+          next_known = true;
+          next_more = m->desc[nb].more;
+          if (next_more) {
+            tc::tc_fence_after();
+            mma1();
+          }
+        }
+        // U = H [dS_slot0 | dS_slot1 | ..] in one product (N = NDS * D): row g's
+        // block sits at columns 256 + slot(g) * D (slots not holding a row of
+        // this tile give unused columns)
+        if (t >= 1) tc::mbar_wait(&m->dh_free, (t - 1) & 1);  // U region: dz2 half 1 of t-1 drained
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) {
+          if (g >= tr.nn) break;
+          const uint32_t q = dsq + g;
+          tc::mbar_wait(&m->ds_full[q % C::NDS], (q / C::NDS) & 1);
+        }
+        tc::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < KH / 16; ++kk) {
+          uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
+          uint64_t bd = tc::sdesc(aDS + kk * 16 * C::ROWB, C::DS_BYTES, 8 * C::ROWB, C::SWZ);
+          tc::mma_bf16_ss(tmem + 256, ad, bd, IDESC_U, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&m->u_full);
+        tc::mma_commit(&m->ah_free);
+        // dH^T = dS_i V_seg^T, kappa half h (columns 384 + slot)
+        auto dh_half = [&](int h) {  // half 0 -> columns 384.., half 1 -> 256..
+#pragma unroll
+          for (int g = 0; g < NMAX; ++g) {
+            if (g >= tr.nn) break;
+            const uint32_t ds = aDS + ((dsq + g) % C::NDS) * C::DS_BYTES;
+            const int s0 = tr.s0[g];
+            const uint32_t idesc_h = tc::idesc_bf16(128, (tr.deg[g] + 15) & ~15, false, false);
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
               uint64_t ad = tc::sdesc(ds + h * 128 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
               uint64_t bd = tc::sdesc(aV + (s0 / 8) * 8 * C::ROWB + kk * 32, 16, 8 * C::ROWB, C::SWZ);
-              tc::mma_bf16_ss(tmem + 256 + h * 128 + s0, ad, bd, idesc_h, kk > 0 ? 1u : 0u);
+              tc::mma_bf16_ss(tmem + (h == 0 ? 384 : 256) + s0, ad, bd, idesc_h, kk > 0 ? 1u : 0u);
             }
           }
-#pragma unroll
-          for (int kk = 0; kk < KH / 16; ++kk) {
-            uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
-            uint64_t bd = tc::sdesc(ds + kk * 16 * C::ROWB, 64 * C::ROWB, 8 * C::ROWB, C::SWZ);
-            tc::mma_bf16_ss(tmem + g * D, ad, bd, IDESC_U, kk > 0 ? 1u : 0u);
+        };
+        if (t >= 1) tc::mbar_wait(&m->dh0_free, (t - 1) & 1);  // dH region: dz2 half 0 of t-1 drained
+        tc::tc_fence_after();
+        dh_half(0);
+        tc::mma_commit(&m->dh0_full);
+        if (!next_known) {  // the next tile's MMA1 before waiting on the dz2 epilogue
+          tc::mbar_wait(&m->e_full[nb], ((t + 1) >> 1) & 1);
+          next_more = m->desc[nb].more;
+          if (next_more) {
+            tc::tc_fence_after();
+            mma1();
           }
-          tc::mma_commit(&m->ds_empty[s]);
         }
-        tc::mma_commit(&m->s_full);
+        tc::mbar_wait(&m->u_free, p1);  // U drained: dH half 1 goes to the U columns
+        tc::tc_fence_after();
+        dh_half(1);
+        tc::mma_commit(&m->dh1_full);
         tc::mma_commit(&m->v_empty);
-        tc::mma_commit(&m->ah_free);
-        tc::mbar_arrive(&m->desc_free[b]);
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) {
+          if (g >= tr.nn) break;
+          tc::mma_commit(&m->ds_empty[(dsq + g) % C::NDS]);
+        }
+        // the next tile's MMA2 while the dz2 epilogue drains both dH halves
+        if (next_more) mma2(t + 1);
+        dsq += tr.nn;
+        more = next_more;
       }
     }
     __syncwarp();
@@ -373,26 +450,35 @@ __global__ void __launch_bounds__(512, 1)
       const TileDescB *dsc = &m->desc[b];
       tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
       if (!dsc->more) break;
+      TileRegs<NMAX> tr;
+      tr.load(dsc);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
       tc::mbar_wait(&m->d1_full, p1);
-      if (t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
       tc::tc_fence_after();
-      // a1 = relu(z1 + b1) -> AH  (group cg: columns 128*cg ..)
+      // a1 = relu(z1 + b1) -> AH  (group cg: columns 128*cg .., 64 at a time).
+      // The first 64 are computed while the previous tile's U product still
+      // reads h from AH.
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c0 = cg * 128 + cc * 32;
-        uint32_t x[32];
-        tc::tmem_ld32(r + c0, x);
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c0 = cg * 128 + cc * 64;
+        uint32_t x[64], pk[32];
+        tc::tmem_ld32(r + c0, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
+        tc::tmem_ld32(r + c0 + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
         tc::tmem_ld_wait();
-        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          pk[q] = tc::pack_bf16(fmaxf(__uint_as_float(x[2 * q]) + sB1[c0 + 2 * q], 0.f),
-                                fmaxf(__uint_as_float(x[2 * q + 1]) + sB1[c0 + 2 * q + 1], 0.f));
+        for (int q4 = 0; q4 < 16; ++q4) {  // biases as float4 broadcasts
+          const float4 bb = *reinterpret_cast<const float4 *>(sB1 + c0 + 4 * q4);
+          pk[2 * q4] = tc::pack_bf16(fmaxf(__uint_as_float(x[4 * q4]) + bb.x, 0.f),
+                                     fmaxf(__uint_as_float(x[4 * q4 + 1]) + bb.y, 0.f));
+          pk[2 * q4 + 1] = tc::pack_bf16(fmaxf(__uint_as_float(x[4 * q4 + 2]) + bb.z, 0.f),
+                                         fmaxf(__uint_as_float(x[4 * q4 + 3]) + bb.w, 0.f));
+        }
+        if (cc == 0 && t >= 1) tc::mbar_wait(&m->ah_free, (t - 1) & 1);
         uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
-        const int ch = (c0 % 64) / 8;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + u)) =
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, u)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
       }
       tc::fence_async_shared();
@@ -401,8 +487,6 @@ __global__ void __launch_bounds__(512, 1)
       // a1 rows -> A1 (one 512-byte row per warp instruction), overlapping MMA2
       tc::named_sync(2, 256);
       {
-        TileRegs<NMAX> tr;
-        tr.load(dsc);
         const int j = lane >> 3, c = lane & 7;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -425,16 +509,29 @@ __global__ void __launch_bounds__(512, 1)
       tc::named_sync(2, 256);
       tc::tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        const int c0 = cg * 128 + cc * 32;
-        uint32_t x[32];
-        tc::tmem_ld32(r + c0, x);
+      for (int cc = 0; cc < 4; cc += 2) {
+        uint32_t xx[64];
+        tc::tmem_ld32(r + cg * 128 + cc * 32, *reinterpret_cast<uint32_t (*)[32]>(&xx[0]));
+        tc::tmem_ld32(r + cg * 128 + cc * 32 + 32, *reinterpret_cast<uint32_t (*)[32]>(&xx[32]));
         tc::tmem_ld_wait();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+        const int c0 = cg * 128 + (cc + half) * 32;
+        const uint32_t *x = &xx[32 * half];
         uint32_t pk[16], bits = 0;
+        float bq[32];
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {  // biases as float4 broadcasts
+          const float4 bb = *reinterpret_cast<const float4 *>(sB2 + c0 + 4 * q4);
+          bq[4 * q4] = bb.x;
+          bq[4 * q4 + 1] = bb.y;
+          bq[4 * q4 + 2] = bb.z;
+          bq[4 * q4 + 3] = bb.w;
+        }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float h0 = fmaxf(__uint_as_float(x[2 * q]) + sB2[c0 + 2 * q], 0.f);
-          const float h1 = fmaxf(__uint_as_float(x[2 * q + 1]) + sB2[c0 + 2 * q + 1], 0.f);
+          const float h0 = fmaxf(__uint_as_float(x[2 * q]) + bq[2 * q], 0.f);
+          const float h1 = fmaxf(__uint_as_float(x[2 * q + 1]) + bq[2 * q + 1], 0.f);
           pk[q] = tc::pack_bf16(h0, h1);
           // word for kappa = c0 + j over this warp's 32 slots; lane j keeps it
           const uint32_t w0 = __ballot_sync(0xffffffffu, h0 > 0.f);
@@ -449,18 +546,18 @@ __global__ void __launch_bounds__(512, 1)
           *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + u)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         sMask[grp * KH + c0 + lane] = bits;
+        }
       }
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready);
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   } else {
     // ============================================================= EPI_B
     const int grp = warp & 3;
     const uint32_t lane_off = (uint32_t)(grp * 32) << 16;
     float db2_lo = 0.f, db2_hi = 0.f;  // kappa = 32*grp + lane, and + 128
+    uint32_t dsq = 0;                  // running row count = dS ring position of this tile's row 0
     for (uint32_t t = 0;; ++t) {
       const int b = t & 1;
       const uint32_t p1 = t & 1;
@@ -476,22 +573,27 @@ __global__ void __launch_bounds__(512, 1)
         mw1[u] = sMask[u * KH + 128 + grp * 32 + lane];
       }
       tc::mbar_arrive(&m->mask_read);
-      tc::mbar_wait(&m->s_full, p1);
+      TileRegs<NMAX> tr;
+      tr.load(dsc);
+      const int nn = tr.nn;
+      tc::mbar_wait(&m->u_full, p1);
       tc::tc_fence_after();
-      const int nn = dsc->nnodes;
       // U part (thread <-> slot row): u_p = U[slot] + dS_i[k]
       {
         const int s = grp * 32 + lane;
-        const int p = slot_edge_of(dsc, nn, s);
-        for (int g = 0; g < nn; ++g) {
-          const int g0 = dsc->slot0[g], gd = dsc->deg[g];
+        const int p = tr.edge(s);
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) {
+          if (g >= nn) break;
+          const int g0 = tr.s0[g], gd = tr.deg[g];
           if (g0 >= grp * 32 + 32 || g0 + gd <= grp * 32) continue;  // row not in this warp's slots
           const bool mine = p >= 0 && s >= g0 && s < g0 + gd;
           const __nv_bfloat16 *brow = &m->brow[b][g][0];
           uint32_t xx[D];
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32)
-            tc::tmem_ld32(tmem + lane_off + g * D + c0, *reinterpret_cast<uint32_t (*)[32]>(&xx[c0]));
+            tc::tmem_ld32(tmem + lane_off + 256 + ((dsq + g) % C::NDS) * D + c0,
+                          *reinterpret_cast<uint32_t (*)[32]>(&xx[c0]));
           tc::tmem_ld_wait();
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
@@ -517,21 +619,26 @@ __global__ void __launch_bounds__(512, 1)
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&m->u_free);
-      // dz2 part (thread <-> kappa)
-#pragma unroll
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);  // brow[b] read
+      // dz2 part (thread <-> kappa), one kappa half per dH product
+#pragma unroll 1
       for (int h = 0; h < 2; ++h) {
+        tc::mbar_wait(h == 0 ? &m->dh0_full : &m->dh1_full, p1);
+        tc::tc_fence_after();
         const int kap = 128 * h + grp * 32 + lane;
         uint32_t mwh[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) mwh[u] = h ? mw1[u] : mw0[u];
         float acc = 0.f;
-        for (int g = 0; g < nn; ++g) {
-          const int s0 = dsc->slot0[g];
-          const int ns = (dsc->deg[g] + 15) & ~15;
-          const int64_t ebase = dsc->ebase[g];
-          const int deg = dsc->deg[g];
-          __nv_bfloat16 *row0 = dZ2g + ebase * KH;
-          const uint32_t ta = tmem + lane_off + 256 + h * 128 + s0;
+#pragma unroll
+        for (int g = 0; g < NMAX; ++g) {
+          if (g >= nn) break;
+          const int s0 = tr.s0[g];
+          const int deg = tr.deg[g];
+          const int ns = (deg + 15) & ~15;
+          __nv_bfloat16 *row0 = dZ2g + tr.eb[g] * KH;
+          const uint32_t ta = tmem + lane_off + (h == 0 ? 384 : 256) + s0;
           int c0 = 0;
           for (; c0 + 64 <= ns; c0 += 64) acc += dz2_chunk<64>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);
           if (c0 + 32 <= ns) {
@@ -541,11 +648,10 @@ __global__ void __launch_bounds__(512, 1)
           if (c0 < ns) acc += dz2_chunk<16>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);
         }
         if (h == 0) db2_lo += acc; else db2_hi += acc;
+        tc::tc_fence_before();
+        tc::mbar_arrive(h == 0 ? &m->dh0_free : &m->dh_free);
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&m->dh_free);
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
+      dsq += nn;
     }
     db2_part[(int64_t)blockIdx.x * KH + grp * 32 + lane] = db2_lo;
     db2_part[(int64_t)blockIdx.x * KH + 128 + grp * 32 + lane] = db2_hi;

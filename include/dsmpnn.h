@@ -141,6 +141,24 @@ dsmpnn_status dsmpnn_partition(const float *coords, const int64_t *gid, int64_t 
                                uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
                                int64_t *counts_host, void *ws, size_t ws_bytes, void *stream);
 
+/* The plans of ALL P ranks from one RCB, with no host synchronisation (the
+ * same arithmetic and outputs as P calls of dsmpnn_partition):
+ *   owner, boxes, internal   as above
+ *   local_rows int64[P x n]               rank q's local order at q*n
+ *   counts     int64[P x (5 + 2(P+1))]    rank q's counts at q*(5+2(P+1)), as above,
+ *                                         followed by the DEGENERATE flag (nonzero: a
+ *                                         split left an empty side; the caller checks
+ *                                         it after synchronising)
+ *   send_idx   int32[P x n*max(1,P-1)]    rank q's send lists at q*n*max(1,P-1)
+ *   gid_bits   0, or b in 1..52 with every gid < 2^b: the plan's radix sorts
+ *              then use b+9 / b+7 key bits instead of 61 / 59.
+ * Workspace: dsmpnn_partition_workspace_size.  Errors as dsmpnn_partition
+ * (DEGENERATE is reported through the flag). */
+dsmpnn_status dsmpnn_partition_all(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
+                                   float overlap_l, float radius, int32_t gid_bits, int32_t *owner, float *boxes,
+                                   uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
+                                   void *ws, size_t ws_bytes, void *stream);
+
 /* Gather rows (local order) of a float32 array: out[k] = in[rows[k]].  Used to
  * form local coordinates / attributes / global ids from a plan. elem_bytes 4 or 8. */
 dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,

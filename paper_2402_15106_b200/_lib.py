@@ -75,6 +75,7 @@ _f = {
     "csc": _sig("csc", P, I64, I64, P, P, P, SZ, P),
     "partition_workspace_size": _sig("partition_workspace_size", I64, C.c_int, C.c_int, C.POINTER(SZ)),
     "partition": _sig("partition", P, P, I64, C.c_int, C.c_int, F, F, C.c_int, P, P, P, P, P, P, P, P, SZ, P),
+    "partition_all": _sig("partition_all", P, P, I64, C.c_int, C.c_int, F, F, I32, P, P, P, P, P, P, P, SZ, P),
     "gather_rows": _sig("gather_rows", P, P, I64, I64, I32, P, P),
     "edge_features": _sig("edge_features", I32, P, C.c_int, P, C.c_int, P, P, I64, I64, P, P, P),
     "packed_weights_size": _sig("packed_weights_size", C.POINTER(LayerDesc), C.POINTER(SZ)),
@@ -176,6 +177,19 @@ def partition(coords, gid, nparts, overlap_l, radius, rank, owner, boxes, intern
           _p(boxes), _p(internal), _p(local_rows), _p(counts), _p(send_idx), host, _p(ws), ws.numel(),
           _stream(stream))
     return [int(x) for x in host] if sync else None
+
+
+def partition_all(coords, gid, nparts, overlap_l, radius, owner, boxes, internal, local_rows, counts, send_idx,
+                  gid_bits=0, ws=None, stream=None):
+    """Plans of every rank from one RCB (asynchronous): local_rows [P, n],
+    counts [P, 5 + 2(P+1)] (last entry per rank = degenerate flag), send_idx [P, cap]."""
+    n, dim = coords.shape
+    sz = SZ()
+    _call("partition_workspace_size", n, dim, nparts, C.byref(sz))
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, coords.device)
+    _call("partition_all", _p(coords), _p(gid), n, dim, nparts, float(overlap_l), float(radius), int(gid_bits),
+          _p(owner), _p(boxes), _p(internal), _p(local_rows), _p(counts), _p(send_idx), _p(ws), ws.numel(),
+          _stream(stream))
 
 
 def gather_rows(inp, rows, out, stream=None):

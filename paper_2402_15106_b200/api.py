@@ -83,7 +83,9 @@ class HotPath:
         L.gather_rows(coords, ids64, cs)
         a = torch.empty((ids.numel(), c.n_attr), dtype=torch.float32, device=self.dev)
         L.gather_rows(attr, ids64, a)
-        self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts)
+        gid_bits = max(1, int(c.n_points - 1).bit_length())  # sampled ids are < n_points
+        self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts,
+                                                  gid_bits=gid_bits)
         pipeline.build_graphs(self.subs, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
                               want_bf16=(c.dtype == L.BF16))
         return self

@@ -189,10 +189,11 @@ __device__ __forceinline__ bool in_ext_box(const float *xj, int dim, const PartS
   return true;
 }
 
-// key = class<<60 | owner<<52 (halo only) | gid ; class 0 deep, 1 near, 2 halo, 3 other
+// key = class<<(gb+7) | owner<<gb (halo only) | gid ; class 0 deep, 1 near, 2
+// halo, 3 other.  gb = 52 without a gid bound (gid < 2^52), else the bound.
 __global__ void plan_classify_kernel(const float *__restrict__ x, const int64_t *__restrict__ gid, int64_t n, int dim,
                                      const int32_t *__restrict__ owner, PartState *st, int q, float l, float t,
-                                     uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                                     int gb, uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     float xj[3] = {0.f, 0.f, 0.f};
     for (int d = 0; d < dim; ++d) xj[d] = x[j * dim + d];
@@ -212,7 +213,7 @@ __global__ void plan_classify_kernel(const float *__restrict__ x, const int64_t 
       cls = 3;
     }
     atomicAdd(&st->cls_count[cls], 1);
-    keys[j] = (cls << 60) | (cls == 2 ? ((uint64_t)o << 52) : 0) | (uint64_t)gid[j];
+    keys[j] = (cls << (gb + 7)) | (cls == 2 ? ((uint64_t)o << gb) : 0) | (uint64_t)gid[j];
     vals[j] = (int32_t)j;
   }
 }
@@ -230,7 +231,8 @@ __global__ void plan_local_kernel(const int32_t *__restrict__ sorted_vals, int64
 // candidate (q', gid) keys for owned points in other ranks' extended boxes
 __global__ void plan_send_kernel(const float *__restrict__ x, const int64_t *__restrict__ gid, int64_t n, int dim,
                                  const int32_t *__restrict__ owner, const int32_t *__restrict__ pos, PartState *st,
-                                 int q, int nparts, float l, uint64_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                                 int q, int nparts, float l, int gb, uint64_t *__restrict__ keys,
+                                 int32_t *__restrict__ vals) {
   int64_t total = n * nparts;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t j = t / nparts;
@@ -241,7 +243,7 @@ __global__ void plan_send_kernel(const float *__restrict__ x, const int64_t *__r
       float xj[3] = {0.f, 0.f, 0.f};
       for (int d = 0; d < dim; ++d) xj[d] = x[j * dim + d];
       if (in_ext_box(xj, dim, st, qq, l)) {
-        key = ((uint64_t)qq << 52) | (uint64_t)gid[j];
+        key = ((uint64_t)qq << gb) | (uint64_t)gid[j];
         v = pos[j];
         atomicAdd(&st->send_count[qq], 1);
       }
@@ -305,72 +307,122 @@ dsmpnn_status dsmpnn_partition_workspace_size(int64_t n, int dim, int nparts, si
   return DSMPNN_OK;
 }
 
-dsmpnn_status dsmpnn_partition(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
-                               float overlap_l, float radius, int rank, int32_t *owner, float *boxes,
-                               uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
-                               int64_t *counts_host, void *ws, size_t ws_bytes, void *stream) {
-  DS_CHECK_ARG(dim == 2 || dim == 3, DSMPNN_ERR_INVALID_ARG, "partition: dim must be 2 or 3");
-  DS_CHECK_ARG(nparts >= 1 && (nparts & (nparts - 1)) == 0 && nparts <= kMaxParts && nparts <= n,
-               DSMPNN_ERR_INVALID_ARG, "partition: nparts must be a power of two <= min(n, %d)", kMaxParts);
-  DS_CHECK_ARG(overlap_l >= 0.f && radius > 0.f, DSMPNN_ERR_INVALID_ARG, "partition: need l >= 0 and r > 0");
-  DS_CHECK_ARG(rank >= 0 && rank < nparts, DSMPNN_ERR_INVALID_ARG, "partition: rank out of range");
-  DS_CHECK_ARG(n * nparts < (1ll << 31), DSMPNN_ERR_INVALID_ARG, "partition: n*P too large");
-  cudaStream_t s = as_stream(stream);
+}  // extern "C"
+
+namespace dsmpnn {
+
+struct PartWs {
+  PartState *st;
+  int32_t *part, *vals, *vals2, *pos;
+  uint64_t *keys, *keys2;
+  int64_t *cnt_ws;
+  void *tmp;
+  size_t tmp_bytes;
+};
+
+static dsmpnn_status carve_part(int64_t n, int nparts, void *ws, size_t ws_bytes, PartWs &w) {
   size_t sort1, sort2;
   size_t need = partition_ws(n, nparts, &sort1, &sort2);
   DS_CHECK_ARG(ws_bytes >= need, DSMPNN_ERR_CAPACITY, "partition: workspace %zu < %zu", ws_bytes, need);
   Carver c(ws, ws_bytes);
-  PartState *st = c.take<PartState>(1);
-  int32_t *part = c.take<int32_t>(n);
-  uint64_t *keys = c.take<uint64_t>(n * nparts), *keys2 = c.take<uint64_t>(n * nparts);
-  int32_t *vals = c.take<int32_t>(n * nparts), *vals2 = c.take<int32_t>(n * nparts);
-  int32_t *pos = c.take<int32_t>(n);
-  int64_t *cnt_ws = c.take<int64_t>(8 + 2 * (kMaxParts + 1));
-  void *tmp = c.take<char>(std::max(sort1, sort2));
-  size_t tmp_bytes = std::max(sort1, sort2);
-  int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 4);
+  w.st = c.take<PartState>(1);
+  w.part = c.take<int32_t>(n);
+  w.keys = c.take<uint64_t>(n * nparts);
+  w.keys2 = c.take<uint64_t>(n * nparts);
+  w.vals = c.take<int32_t>(n * nparts);
+  w.vals2 = c.take<int32_t>(n * nparts);
+  w.pos = c.take<int32_t>(n);
+  w.cnt_ws = c.take<int64_t>(8 + 2 * (kMaxParts + 1));
+  w.tmp_bytes = std::max(sort1, sort2);
+  w.tmp = c.take<char>(w.tmp_bytes);
+  return DSMPNN_OK;
+}
 
-  DS_CUDA(cudaMemsetAsync(part, 0, n * sizeof(int32_t), s));
+static dsmpnn_status check_part_args(int64_t n, int dim, int nparts, float overlap_l, float radius) {
+  DS_CHECK_ARG(dim == 2 || dim == 3, DSMPNN_ERR_INVALID_ARG, "partition: dim must be 2 or 3");
+  DS_CHECK_ARG(nparts >= 1 && (nparts & (nparts - 1)) == 0 && nparts <= kMaxParts && nparts <= n,
+               DSMPNN_ERR_INVALID_ARG, "partition: nparts must be a power of two <= min(n, %d)", kMaxParts);
+  DS_CHECK_ARG(overlap_l >= 0.f && radius > 0.f, DSMPNN_ERR_INVALID_ARG, "partition: need l >= 0 and r > 0");
+  DS_CHECK_ARG(n * nparts < (1ll << 31), DSMPNN_ERR_INVALID_ARG, "partition: n*P too large");
+  return DSMPNN_OK;
+}
+
+// recursive coordinate bisection (R12): owner, boxes, internal faces
+static dsmpnn_status run_rcb(const float *coords, int64_t n, int dim, int nparts, const PartWs &w, int32_t *owner,
+                             float *boxes, uint8_t *internal, cudaStream_t s) {
+  const int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 4);
+  DS_CUDA(cudaMemsetAsync(w.part, 0, n * sizeof(int32_t), s));
   int levels = 0;
   while ((1 << levels) < nparts) ++levels;
   for (int L = 0; L <= levels; ++L) {
     int cur = 1 << L;
-    part_init_kernel<<<1, kMaxParts, 0, s>>>(st, cur);
-    part_bbox_kernel<<<g, 256, 0, s>>>(coords, n, dim, part, cur, st);
-    if (L == 0) root_box_kernel<<<1, 1, 0, s>>>(st, dim);
+    part_init_kernel<<<1, kMaxParts, 0, s>>>(w.st, cur);
+    part_bbox_kernel<<<g, 256, 0, s>>>(coords, n, dim, w.part, cur, w.st);
+    if (L == 0) root_box_kernel<<<1, 1, 0, s>>>(w.st, dim);
     if (L == levels) break;
-    part_axis_kernel<<<1, kMaxParts, 0, s>>>(st, cur, dim);
-    part_key_kernel<<<g, 256, 0, s>>>(coords, n, dim, part, st, keys);
-    size_t tb = tmp_bytes;
-    DS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, keys2, (int)n, 0, 32 + levels + 1, s));
-    part_cut_kernel<<<1, 32, 0, s>>>(keys2, st, cur);
-    part_split_kernel<<<g, 256, 0, s>>>(coords, n, dim, part, st);
-    part_boxes_kernel<<<1, 32, 0, s>>>(st, cur);
+    part_axis_kernel<<<1, kMaxParts, 0, s>>>(w.st, cur, dim);
+    part_key_kernel<<<g, 256, 0, s>>>(coords, n, dim, w.part, w.st, w.keys);
+    size_t tb = w.tmp_bytes;
+    DS_CUDA(cub::DeviceRadixSort::SortKeys(w.tmp, tb, w.keys, w.keys2, (int)n, 0, 32 + levels + 1, s));
+    part_cut_kernel<<<1, 32, 0, s>>>(w.keys2, w.st, cur);
+    part_split_kernel<<<g, 256, 0, s>>>(coords, n, dim, w.part, w.st);
+    part_boxes_kernel<<<1, 32, 0, s>>>(w.st, cur);
   }
-  DS_CUDA(cudaMemcpyAsync(owner, part, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  part_out_boxes_kernel<<<1, kMaxParts, 0, s>>>(st, nparts, dim, boxes, internal);
+  DS_CUDA(cudaMemcpyAsync(owner, w.part, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  part_out_boxes_kernel<<<1, kMaxParts, 0, s>>>(w.st, nparts, dim, boxes, internal);
   DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
 
-  // ---- plan of `rank`
+// plan of one rank from the RCB state in w (R13, R23); counts gets
+// 4 + 2(P+1) entries plus the degenerate flag when with_flag
+static dsmpnn_status run_plan(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
+                              float overlap_l, float radius, int rank, int gid_bits, const PartWs &w,
+                              int64_t *local_rows, int64_t *counts, bool with_flag, int32_t *send_idx,
+                              cudaStream_t s) {
+  const int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 4);
+  const int gb = (gid_bits >= 1 && gid_bits <= 52) ? gid_bits : 52;  // key fields: gid | owner (7) | class (2)
   float m = overlap_l > radius ? overlap_l : radius;
   float t = m * 1.0009765625f;  // fl(max(l, r) * (1 + 2^-10)), single RNE product
-  plan_reset_kernel<<<1, kMaxParts, 0, s>>>(st);
-  plan_classify_kernel<<<g, 256, 0, s>>>(coords, gid, n, dim, part, st, rank, overlap_l, t, keys, vals);
-  size_t tb = tmp_bytes;
-  DS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)n, 0, 64, s));
-  plan_local_kernel<<<g, 256, 0, s>>>(vals2, n, st, local_rows, pos);
+  plan_reset_kernel<<<1, kMaxParts, 0, s>>>(w.st);
+  plan_classify_kernel<<<g, 256, 0, s>>>(coords, gid, n, dim, w.part, w.st, rank, overlap_l, t, gb, w.keys, w.vals);
+  size_t tb = w.tmp_bytes;
+  DS_CUDA(cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.keys, w.keys2, w.vals, w.vals2, (int)n, 0, gb + 9, s));
+  plan_local_kernel<<<g, 256, 0, s>>>(w.vals2, n, w.st, local_rows, w.pos);
   int g2 = (int)std::min<int64_t>(ceil_div(n * nparts, 256), 148 * 8);
-  plan_send_kernel<<<g2, 256, 0, s>>>(coords, gid, n, dim, part, pos, st, rank, nparts, overlap_l, keys, vals);
-  tb = tmp_bytes;
-  DS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, vals, vals2, (int)(n * nparts), 0, 64, s));
-  plan_counts_kernel<<<1, 32, 0, s>>>(st, nparts, rank, cnt_ws);
-  DS_CUDA(cudaMemcpyAsync(counts, cnt_ws, (4 + 2 * (nparts + 1)) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-  copy_send_kernel<<<g, 256, 0, s>>>(vals2, cnt_ws, send_idx);
+  plan_send_kernel<<<g2, 256, 0, s>>>(coords, gid, n, dim, w.part, w.pos, w.st, rank, nparts, overlap_l, gb, w.keys,
+                                      w.vals);
+  tb = w.tmp_bytes;
+  DS_CUDA(cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.keys, w.keys2, w.vals, w.vals2, (int)(n * nparts), 0, gb + 7,
+                                          s));
+  plan_counts_kernel<<<1, 32, 0, s>>>(w.st, nparts, rank, w.cnt_ws);
+  const int nc = 4 + 2 * (nparts + 1) + (with_flag ? 1 : 0);
+  DS_CUDA(cudaMemcpyAsync(counts, w.cnt_ws, nc * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+  copy_send_kernel<<<g, 256, 0, s>>>(w.vals2, w.cnt_ws, send_idx);
   DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+}  // namespace dsmpnn
+
+extern "C" {
+
+dsmpnn_status dsmpnn_partition(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
+                               float overlap_l, float radius, int rank, int32_t *owner, float *boxes,
+                               uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
+                               int64_t *counts_host, void *ws, size_t ws_bytes, void *stream) {
+  DS_TRY(check_part_args(n, dim, nparts, overlap_l, radius));
+  DS_CHECK_ARG(rank >= 0 && rank < nparts, DSMPNN_ERR_INVALID_ARG, "partition: rank out of range");
+  cudaStream_t s = as_stream(stream);
+  PartWs w;
+  DS_TRY(carve_part(n, nparts, ws, ws_bytes, w));
+  DS_TRY(run_rcb(coords, n, dim, nparts, w, owner, boxes, internal, s));
+  DS_TRY(run_plan(coords, gid, n, dim, nparts, overlap_l, radius, rank, 0, w, local_rows, counts, false, send_idx,
+                  s));
   if (counts_host) {
     int64_t tmp_host[4 + 2 * (kMaxParts + 1) + 1];
     int nc = 4 + 2 * (nparts + 1) + 1;
-    DS_CUDA(cudaMemcpyAsync(tmp_host, cnt_ws, nc * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaMemcpyAsync(tmp_host, w.cnt_ws, nc * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     DS_CUDA(cudaStreamSynchronize(s));
     for (int k = 0; k < nc - 1; ++k) counts_host[k] = tmp_host[k];
     if (tmp_host[nc - 1]) {
@@ -378,6 +430,23 @@ dsmpnn_status dsmpnn_partition(const float *coords, const int64_t *gid, int64_t 
       return DSMPNN_ERR_DEGENERATE;
     }
   }
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_partition_all(const float *coords, const int64_t *gid, int64_t n, int dim, int nparts,
+                                   float overlap_l, float radius, int32_t gid_bits, int32_t *owner, float *boxes,
+                                   uint8_t *internal, int64_t *local_rows, int64_t *counts, int32_t *send_idx,
+                                   void *ws, size_t ws_bytes, void *stream) {
+  DS_TRY(check_part_args(n, dim, nparts, overlap_l, radius));
+  DS_CHECK_ARG(gid_bits >= 0 && gid_bits <= 63, DSMPNN_ERR_INVALID_ARG, "partition_all: gid_bits in 0..63");
+  cudaStream_t s = as_stream(stream);
+  PartWs w;
+  DS_TRY(carve_part(n, nparts, ws, ws_bytes, w));
+  DS_TRY(run_rcb(coords, n, dim, nparts, w, owner, boxes, internal, s));
+  const int64_t nc = 5 + 2 * (nparts + 1), cap = n * std::max(1, nparts - 1);
+  for (int q = 0; q < nparts; ++q)
+    DS_TRY(run_plan(coords, gid, n, dim, nparts, overlap_l, radius, q, gid_bits, w, local_rows + q * n,
+                    counts + q * nc, true, send_idx + q * cap, s));
   return DSMPNN_OK;
 }
 

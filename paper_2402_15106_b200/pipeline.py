@@ -52,42 +52,40 @@ def sample_nodes(n_points, s, seed, device):
     return ids
 
 
-def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks):
-    """Partition the sampled set and build the local arrays of the given ranks.
-    All ranks' plans are enqueued first and their sizes read back with one
-    host synchronisation."""
+def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bits=0):
+    """Partition the sampled set (all ranks' plans from one RCB, one host
+    synchronisation) and build the local arrays of the given ranks.
+    gid_bits: every gid < 2^gid_bits (0 = unknown), shortens the plan sorts."""
     dev = coords_s.device
     n, dim = coords_s.shape
     owner = torch.empty(n, dtype=torch.int32, device=dev)
     boxes = torch.empty(nparts * 2 * dim, dtype=torch.float32, device=dev)
     internal = torch.empty(nparts * 2 * dim, dtype=torch.uint8, device=dev)
-    nc = 4 + 2 * (nparts + 1)
-    ranks = list(ranks)
-    counts = torch.empty((len(ranks), nc), dtype=torch.int64, device=dev)
-    bufs = []
-    for t, q in enumerate(ranks):
-        local_rows = torch.empty(n, dtype=torch.int64, device=dev)
-        send_idx = torch.empty(max(1, n * max(1, nparts - 1)), dtype=torch.int32, device=dev)
-        L.partition(coords_s, gid_s, nparts, overlap_l, radius, q, owner, boxes, internal, local_rows, counts[t],
-                    send_idx, sync=False)
-        bufs.append((local_rows, send_idx))
+    nc = 5 + 2 * (nparts + 1)
+    cap = n * max(1, nparts - 1)
+    local_rows = torch.empty((nparts, n), dtype=torch.int64, device=dev)
+    counts = torch.empty((nparts, nc), dtype=torch.int64, device=dev)
+    send_idx = torch.empty((nparts, cap), dtype=torch.int32, device=dev)
+    L.partition_all(coords_s, gid_s, nparts, overlap_l, radius, owner, boxes, internal, local_rows, counts,
+                    send_idx, gid_bits=gid_bits)
     hcounts = counts.cpu().tolist()  # the one synchronisation
+    if any(h[-1] for h in hcounts):
+        raise L.DsmpnnError(-9, "partition_all", "partition: a split left an empty side (all split coordinates tied)")
     out = []
-    for t, q in enumerate(ranks):
-        h = hcounts[t]
-        local_rows, send_idx = bufs[t]
+    for q in ranks:
+        h = hcounts[q]
         nd, nn, nh, ns = h[0], h[1], h[2], h[3]
         halo_ptr = h[4:4 + nparts + 1]
         send_ptr = h[4 + nparts + 1:4 + 2 * (nparts + 1)]
         n_loc = nd + nn + nh
-        lr = local_rows[:n_loc]
+        lr = local_rows[q, :n_loc]
         c = torch.empty((n_loc, dim), dtype=torch.float32, device=dev)
         L.gather_rows(coords_s, lr, c)
         g = torch.empty(n_loc, dtype=torch.int64, device=dev)
         L.gather_rows(gid_s, lr, g)
         a = torch.empty((n_loc, attr_s.shape[1]), dtype=torch.float32, device=dev)
         L.gather_rows(attr_s, lr, a)
-        out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[:max(ns, 0)], c, g, a))
+        out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[q, :max(ns, 0)], c, g, a))
     return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
 
 

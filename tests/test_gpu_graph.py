@@ -167,6 +167,53 @@ def test_partition_bit_exact(L, name, gen, P, r):
             assert np.array_equal(sidx[:h[3]], rq["send_idx"])
 
 
+@pytest.mark.parametrize("name,gen,P,r", [PCASES[0], PCASES[1], PCASES[4], PCASES[6]],
+                         ids=["u2d_P4", "u3d_P8", "grid_P4", "neg_P4"])
+@pytest.mark.parametrize("gid_bits", [0, -1], ids=["gid64", "gid_bound"])
+def test_partition_all_bit_exact(L, name, gen, P, r, gid_bits):
+    """All ranks' plans from one call (one RCB, compact sort keys when a gid
+    bound is given) equal the oracle plan of every rank."""
+    g = np.random.default_rng(zlib.crc32(name.encode()) % 997)
+    x = gen(g).astype(np.float32)
+    n, dim = x.shape
+    gid = g.permutation(5 * n)[:n].astype(np.int64)
+    gb = int(5 * n - 1).bit_length() if gid_bits < 0 else 0
+    nc, cap = 5 + 2 * (P + 1), n * max(1, P - 1)
+    for l in (r, 0.5 * r):
+        o_owner, o_boxes, o_int, ranks = partition.plan(x, gid, P, l, r)
+        owner = torch.empty(n, dtype=torch.int32, device=cuda())
+        boxes = torch.empty(P * 2 * dim, dtype=torch.float32, device=cuda())
+        internal = torch.empty(P * 2 * dim, dtype=torch.uint8, device=cuda())
+        lr = torch.empty((P, n), dtype=torch.int64, device=cuda())
+        counts = torch.empty((P, nc), dtype=torch.int64, device=cuda())
+        sidx = torch.empty((P, cap), dtype=torch.int32, device=cuda())
+        L.partition_all(T(x), T(gid), P, l, r, owner, boxes, internal, lr, counts, sidx, gid_bits=gb)
+        assert np.array_equal(N(owner), o_owner)
+        assert np.array_equal(N(boxes).reshape(P, 2, dim).view(np.uint32), o_boxes.view(np.uint32))
+        assert np.array_equal(N(internal).reshape(P, 2, dim).astype(bool), o_int)
+        h_all, lr_all, s_all = N(counts), N(lr), N(sidx)
+        for q in range(P):
+            h, rq = h_all[q], ranks[q]
+            n_loc = len(rq["local_rows"])
+            assert h[0] == rq["n_deep"] and h[1] == rq["n_near"] and h[2] == rq["n_halo"] and h[-1] == 0
+            assert np.array_equal(lr_all[q, :n_loc], rq["local_rows"])
+            assert list(h[4:4 + P + 1]) == list(rq["halo_ptr"])
+            assert list(h[5 + P:5 + 2 * P + 1]) == list(rq["send_ptr"])
+            assert np.array_equal(s_all[q, :h[3]], rq["send_idx"])
+
+
+def test_partition_all_degenerate_flag(L):
+    x = np.zeros((16, 2), np.float32)
+    P = 2
+    counts = torch.empty((P, 5 + 2 * (P + 1)), dtype=torch.int64, device=cuda())
+    o = torch.empty(16, dtype=torch.int32, device=cuda())
+    L.partition_all(T(x), T(np.arange(16)), P, 0.1, 0.1, o, torch.empty(8, device=cuda()),
+                    torch.empty(8, dtype=torch.uint8, device=cuda()), torch.empty((P, 16), dtype=torch.int64,
+                                                                                  device=cuda()),
+                    counts, torch.empty((P, 16), dtype=torch.int32, device=cuda()), gid_bits=4)
+    assert N(counts)[:, -1].any()
+
+
 def test_partition_degenerate(L):
     x = np.zeros((16, 2), np.float32)
     with pytest.raises(L.DsmpnnError) as ei:

@@ -277,7 +277,9 @@ __global__ void __launch_bounds__(512, 1)
       for (uint32_t t = 0; more; ++t) {
         const int b = t & 1;
         const uint32_t p1 = t & 1;
-        const TileDesc2 *dsc = &m->desc[b];
+        TileRegs<NMAX> tr;
+        tr.load(&m->desc[b]);
+        tc::mbar_arrive(&m->desc_free[b]);
         const uint32_t r = tmem + b * 256;
         // MMA2: z2 = a1 W2^T in two N halves.  Half 0 (kappa 0..127) goes to
         // columns 128..255, whose z1 the epilogue drains first (a1 blocks 2, 3),
@@ -302,12 +304,13 @@ __global__ void __launch_bounds__(512, 1)
         }
         // S_i = H_i^T V_i per row, kappa half h at column h*128 + g*D
         tc::mbar_wait(&m->v_full, p1);
-        const int nn = dsc->nnodes;
         for (int h = 0; h < 2; ++h) {
           tc::mbar_wait(&m->h_ready[h], p1);
           tc::tc_fence_after();
-          for (int g = 0; g < nn; ++g) {
-            const int s0 = dsc->slot0[g], nk = (dsc->deg[g] + 15) >> 4;
+#pragma unroll
+          for (int g = 0; g < NMAX; ++g) {
+            if (g >= tr.nn) break;
+            const int s0 = tr.s0[g], nk = (tr.deg[g] + 15) >> 4;
             for (int q = 0; q < nk; ++q) {
               int s = s0 + 16 * q;
               uint64_t ad = tc::sdesc(aAH + (2 * h) * (128 * 128) + (s / 8) * 1024, 128 * 128, 1024, tc::kSw128);
@@ -320,7 +323,6 @@ __global__ void __launch_bounds__(512, 1)
         tc::mma_commit(&m->s_full);
         tc::mma_commit(&m->v_empty);
         tc::mma_commit(&m->ah_free);
-        tc::mbar_arrive(&m->desc_free[b]);
         more = mma1(t + 1);
       }
     }
@@ -336,6 +338,8 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t ph = (t >> 1) & 1, p1 = t & 1;
       tc::mbar_wait(&m->e_full[b], ph);
       if (!m->desc[b].more) break;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
       const uint32_t r = tmem + b * 256 + lane_off;
       tc::mbar_wait(&m->d1_full[b], ph);
       tc::tc_fence_after();
@@ -415,8 +419,6 @@ __global__ void __launch_bounds__(512, 1)
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->h_ready[1]);
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   } else {
     // ============================================================= EPI_B
@@ -428,43 +430,47 @@ __global__ void __launch_bounds__(512, 1)
       const TileDesc2 *dsc = &m->desc[b];
       tc::mbar_wait(&m->e_full[b], ph);
       if (!dsc->more) break;
+      TileRegs<NMAX> tr;
+      tr.load(dsc);
+      int64_t node[NMAX];
+#pragma unroll
+      for (int g = 0; g < NMAX; ++g) node[g] = g < tr.nn ? dsc->node[g] : 0;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
       tc::mbar_wait(&m->s_full, p1);
       tc::tc_fence_after();
       const uint32_t r = tmem + b * 256 + lane_off;
-      const int nn = dsc->nnodes;
-      for (int g = 0; g < nn; ++g) {
-        const float inv = 1.0f / (float)dsc->deg[g];
-        __nv_bfloat16 *Si = S + dsc->node[g] * kp;
+      // S~_i layout [c][kappa] (kappa contiguous): lane pairs (kappa, kappa+1)
+      // swap packed bf16 pairs so every 4-byte store of the warp covers 64
+      // contiguous bytes of two S~ rows (columns c and c+1)
+      const bool odd = lane & 1;
+      const uint32_t sel = odd ? 0x3276u : 0x5410u;
+#pragma unroll
+      for (int g = 0; g < NMAX; ++g) {
+        if (g >= tr.nn) break;
+        const float inv = 1.0f / (float)tr.deg[g];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int kap = 128 * h + grp * 32 + lane;
+          __nv_bfloat16 *dst = S + node[g] * kp + (odd ? 1 : 0) * KH + (kap & ~1);
+          uint32_t x[D];
 #pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 16) {
-            uint32_t x[16];
-            tc::tmem_ld16(r + (h == 0 ? 128 : 0) + g * D + c0, x);
-            tc::tmem_ld_wait();
-            // S~_i layout [c][kappa] (kappa contiguous): lane pairs (kappa, kappa+1)
-            // swap halves so every 4-byte store of the warp covers 64
-            // contiguous bytes (two coalesced segments per instruction)
-            const bool odd = lane & 1;
-            const int cb = odd ? 8 : 0;  // columns this lane stores: c0+cb .. c0+cb+7
+          for (int c0 = 0; c0 < D; c0 += 32)
+            tc::tmem_ld32(r + (h == 0 ? 128 : 0) + g * D + c0, *reinterpret_cast<uint32_t (*)[32]>(&x[c0]));
+          tc::tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float mine = __uint_as_float(x[cb + q]) * inv;
-              const float give = __uint_as_float(x[(8 - cb) + q]) * inv;   // partner's columns
-              const float other = __shfl_xor_sync(0xffffffffu, give, 1);
-              const uint32_t pair = odd ? tc::pack_bf16(other, mine) : tc::pack_bf16(mine, other);
-              asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(Si + (int64_t)(c0 + cb + q) * KH + (kap & ~1)),
-                           "r"(pair)
-                           : "memory");
-            }
+          for (int q = 0; q < D / 2; ++q) {
+            const uint32_t own = tc::pack_bf16(__uint_as_float(x[2 * q]) * inv, __uint_as_float(x[2 * q + 1]) * inv);
+            const uint32_t oth = __shfl_xor_sync(0xffffffffu, own, 1);
+            const uint32_t pr = __byte_perm(own, oth, sel);
+            asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(dst + (int64_t)(2 * q) * KH), "r"(pr)
+                         : "memory");
           }
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&m->region_free[b]);
-      if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
     }
   }
   tc::tc_fence_before();

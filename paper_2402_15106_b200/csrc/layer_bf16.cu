@@ -105,7 +105,22 @@ __global__ void s_fill_kernel(const __nv_bfloat16 *__restrict__ v, const int64_t
     float acc[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) acc[q] = 0.f;
-    for (int64_t p = p0; p < p1; ++p) {
+    int64_t p = p0;
+    for (; p + 8 <= p1; p += 8) {  // eight rows in flight, summed in edge order
+      int32_t j[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) j[u] = __ldg(col + p + u);
+      float x[8][PER];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) x[u][q] = __bfloat162float(v[(int64_t)j[u] * D + lane * PER + q]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) acc[q] += x[u][q];
+    }
+    for (; p < p1; ++p) {
       const __nv_bfloat16 *vj = v + (int64_t)col[p] * D;
 #pragma unroll
       for (int q = 0; q < PER; ++q) acc[q] += __bfloat162float(vj[lane * PER + q]);

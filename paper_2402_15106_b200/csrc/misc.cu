@@ -46,6 +46,40 @@ __global__ void edge_features_kernel(int32_t mode, const float *__restrict__ x, 
       if (row_ptr[mid] <= p) lo = mid; else hi = mid;
     }
     int64_t i = lo, j = col[p];
+    if (de <= 16) {
+      // value k of the edge attribute, k unrolled so everything stays in registers
+      float vals[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        float v = 0.f;
+        if (mode == DSMPNN_EDGE_DIFF) {
+          if (k < dim) v = __fsub_rn(x[i * dim + k], x[j * dim + k]);
+          else if (k < dim + n_attr) v = __fsub_rn(a[i * n_attr + (k - dim)], a[j * n_attr + (k - dim)]);
+        } else {
+          if (k < dim) v = x[i * dim + k];
+          else if (k < 2 * dim) v = x[j * dim + (k - dim)];
+          else if (k < 2 * dim + n_attr) v = a[i * n_attr + (k - 2 * dim)];
+          else if (k < de) v = a[j * n_attr + (k - 2 * dim - n_attr)];
+        }
+        vals[k] = v;
+      }
+      if (e32)
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < de) e32[p * de + k] = vals[k];
+      if (e16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(vals[2 * k], vals[2 * k + 1]);
+          w[k] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        uint4 *o = reinterpret_cast<uint4 *>(e16 + p * 16);
+        o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+      continue;
+    }
     float vals[32];
     int c = 0;
     if (mode == DSMPNN_EDGE_DIFF) {
@@ -59,10 +93,6 @@ __global__ void edge_features_kernel(int32_t mode, const float *__restrict__ x, 
     }
     if (e32)
       for (int d = 0; d < de; ++d) e32[p * de + d] = vals[d];
-    if (e16) {
-      __nv_bfloat16 *o = e16 + p * 16;
-      for (int d = 0; d < 16; ++d) o[d] = __float2bfloat16_rn(d < de ? vals[d] : 0.f);
-    }
   }
 }
 

@@ -120,7 +120,7 @@ def _edge_arrays(sd, edge_mode, want_f32, want_bf16):
     E = sd.n_edges
     de = (sd.coords.shape[1] + sd.attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
     sd.e32 = torch.empty((max(E, 1), de), dtype=torch.float32, device=dev) if want_f32 else None
-    sd.e16 = torch.zeros((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None
+    sd.e16 = torch.empty((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None  # all 16 written
     L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, sd.n_own, sd.e32, sd.e16)
     sd.csc_perm = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)

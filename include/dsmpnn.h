@@ -257,6 +257,22 @@ dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *val
                                                const int64_t *const *send_ptr, const int32_t *const *send_idx,
                                                int32_t width, void *stream);
 
+/* ----------------------------------------------------------- f4 --------- */
+/* Inference by sub-domain reassembly ("randomly selected
+ * sub-domains ... sequentially fed into the trained model ... reassembled in
+ * post-processing").  Each pass (sample, partition, L-layer
+ * forward) contributes its owned rows' predictions; the assembled field is
+ * their per-node average.
+ *   accumulate: sum[gid[k]] += pred[k] (width floats), count[gid[k]] += 1, for
+ *               k < n.  gid values within one call must be distinct (one
+ *               sub-domain's owned rows); calls are applied in stream order,
+ *               so the result is deterministic.
+ *   finalize:   out[g] = count[g] ? sum[g] / count[g] : 0, g < n_points. */
+dsmpnn_status dsmpnn_reassemble_accumulate(const float *pred, const int64_t *gid, int64_t n, int32_t width,
+                                           float *sum, int32_t *count, void *stream);
+dsmpnn_status dsmpnn_reassemble_finalize(const float *sum, const int32_t *count, int64_t n_points, int32_t width,
+                                         float *out, void *stream);
+
 /* --------------------------------------------------------------- GEMM --- */
 /* Dense bf16 GEMM on the tcgen05 tensor cores, fp32 accumulate:
  *   C[M x N] (+)= A[M x K] . B[K x N]

@@ -8,7 +8,7 @@ overlap from the neighbours' interiors after every hop.  Used by tests to pin
 """
 import numpy as np
 
-from . import features, graph, halo, layer, partition
+from . import features, graph, halo, layer, partition, sample
 
 
 def build_local(coords, gid, attr, nparts, overlap_l, r, n_e, seed, edge_mode):
@@ -111,3 +111,28 @@ def undecomposed_forward_backward(desc, W, coords, gid, attr, r, n_e, seed, edge
             grads[k] += g[k]
         g_out = dv
     return grads
+
+
+def infer_reassemble(desc, W, coords, attr, nparts, overlap_l, r, n_e, seed_capping, s, seeds, v0_global,
+                     n_layers, edge_mode):
+    """Inference by sub-domain reassembly: for
+    every sampling seed, sample s of the N points, decompose, run the L-layer
+    forward with halo refresh (ds_forward) and add every rank's owned-row
+    outputs to its global node; the field is the per-node average over the
+    passes that visited it (0 where none did).  Returns (field [N x d], count)."""
+    coords = np.asarray(coords, np.float32)
+    N = len(coords)
+    v0_global = np.asarray(v0_global, np.float64)
+    acc = np.zeros((N, v0_global.shape[1]))
+    cnt = np.zeros(N, np.int64)
+    for seed in seeds:
+        ids = sample.sample(N, s, seed).astype(np.int64)
+        _, _, _, ranks = build_local(coords[ids], ids, np.asarray(attr, np.float32)[ids], nparts, overlap_l, r, n_e,
+                                     seed_capping, edge_mode)
+        outs = ds_forward(desc, W, ranks, lambda rows: v0_global[ids[rows]], n_layers)
+        for q, o in zip(ranks, outs):
+            g = q["local_gid"][: len(o)]
+            acc[g] += o
+            cnt[g] += 1
+    field = np.where(cnt[:, None] > 0, acc / np.maximum(cnt, 1)[:, None], 0.0)
+    return field, cnt

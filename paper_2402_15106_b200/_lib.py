@@ -92,6 +92,8 @@ _f = {
                                    C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, P),
     "halo_reverse_add_loopback": _sig("halo_reverse_add_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
                                       C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, P),
+    "reassemble_accumulate": _sig("reassemble_accumulate", P, P, I64, I32, P, P, P),
+    "reassemble_finalize": _sig("reassemble_finalize", P, P, I64, I32, P, P),
     "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
     "probe_begin": _sig("probe_begin", I32, I32),
     "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
@@ -296,6 +298,16 @@ def halo_reverse_add_loopback(values_list, halo_ptr_list, send_ptr_list, send_id
     spp = (C.POINTER(I64) * P_)(*[C.cast(s, C.POINTER(I64)) for s in sp])
     sidx = (P * P_)(*[s.data_ptr() for s in send_idx_list])
     _call("halo_reverse_add_loopback", P_, vals, hpp, spp, sidx, width, _stream(stream))
+
+
+def reassemble_accumulate(pred, gid, sum_, count, stream=None):
+    """sum_[gid[k]] += pred[k]; count[gid[k]] += 1 (f4)."""
+    _call("reassemble_accumulate", _p(pred), _p(gid), pred.shape[0], pred.shape[1], _p(sum_), _p(count),
+          _stream(stream))
+
+
+def reassemble_finalize(sum_, count, out, stream=None):
+    _call("reassemble_finalize", _p(sum_), _p(count), sum_.shape[0], sum_.shape[1], _p(out), _stream(stream))
 
 
 def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=None, accumulate=False,

@@ -116,15 +116,14 @@ class HotPath:
         else:
             pipeline.halo_reverse_mixed(self.subs, grads, self.proc_of, self.rank, self.group)
 
-    def forward_backward(self, v0, G):
-        """v0: [s x d] initial latent of the sampled nodes (sampled order);
-        G: [s x d] dL/d(last layer output) (rows of owned nodes are used).
-        Returns the accumulated weight gradients (dict of device tensors)."""
+    def forward(self, v0):
+        """L layers forward (Alg. 1 :404-411) with a halo refresh after each.
+        v0: [s x d] initial latent of the sampled nodes (sampled order).
+        Returns (acts, outs): every layer's input per sub-domain (local order)
+        and the last layer's fp32 outputs of each sub-domain's owned rows."""
         c, desc = self.cfg, self.desc
         lowp = c.dtype == L.BF16
         vdt = torch.bfloat16 if lowp else torch.float32
-        for g in self.grads.values():
-            g.zero_()
         # layer-0 inputs of every sub-domain (local order)
         vals = []
         for sd in self.subs:
@@ -146,6 +145,19 @@ class HotPath:
                 nxt.append(nv)
             self.halo(nxt, L.BF16 if lowp else L.F32)
             acts.append(nxt)
+        outs = [self.ws[("out", q)].view(torch.float32)[: sd.n_own * c.d].view(sd.n_own, c.d)
+                for q, sd in enumerate(self.subs)]
+        return acts, outs
+
+    def forward_backward(self, v0, G):
+        """v0: [s x d] initial latent of the sampled nodes (sampled order);
+        G: [s x d] dL/d(last layer output) (rows of owned nodes are used).
+        Returns the accumulated weight gradients (dict of device tensors)."""
+        c, desc = self.cfg, self.desc
+        lowp = c.dtype == L.BF16
+        for g in self.grads.values():
+            g.zero_()
+        acts, _ = self.forward(v0)
         # backward: DETACH or REVERSE_ADD halo rows (R16, f2)
         gouts = []
         for sd in self.subs:
@@ -181,6 +193,38 @@ class HotPath:
             m = self.grads[n].numel()
             self.grads[n].copy_(flat[off:off + m].view_as(self.grads[n]))
             off += m
+
+    def infer(self, coords, attr, v0_global, seeds):
+        """Inference by sub-domain reassembly:
+        for every sampling seed, sample / decompose / build graphs and run the
+        L-layer forward; each owned row's output is added to its global node,
+        and the field is the per-node average over the passes that visited it
+        (0 where none did).  v0_global: [n_points x d] initial latent of every
+        point.  Returns (field [n_points x d] fp32, count [n_points] int32)."""
+        import dataclasses
+        c0 = self.cfg
+        N, d = c0.n_points, c0.d
+        acc = torch.zeros((N, d), dtype=torch.float32, device=self.dev)
+        cnt = torch.zeros(N, dtype=torch.int32, device=self.dev)
+        try:
+            for seed in seeds:
+                self.cfg = dataclasses.replace(c0, seed_sampling=int(seed))
+                self.build(coords, attr)
+                ids64 = self.ids.to(torch.int64)
+                v0 = torch.empty((ids64.numel(), d), dtype=torch.float32, device=self.dev)
+                L.gather_rows(v0_global, ids64, v0)
+                _, outs = self.forward(v0)
+                for sd, o in zip(self.subs, outs):
+                    L.reassemble_accumulate(o, sd.gid[: sd.n_own], acc, cnt)
+        finally:
+            self.cfg = c0
+        if self.world > 1:  # each process holds some sub-domains of every pass
+            import torch.distributed as dist
+            dist.all_reduce(acc, group=self.group)
+            dist.all_reduce(cnt, group=self.group)
+        field = torch.empty_like(acc)
+        L.reassemble_finalize(acc, cnt, field)
+        return field, cnt
 
     def step(self, coords, attr, v0, G):
         """One full hot-path step on device inputs."""

@@ -118,6 +118,25 @@ __global__ void halo_scatter_add_kernel(const float *__restrict__ in, const int3
   }
 }
 
+// ------------------------------------------------------------ f4 reassembly --
+__global__ void reassemble_acc_kernel(const float *__restrict__ pred, const int64_t *__restrict__ gid, int64_t n,
+                                      int width, float *__restrict__ sum, int32_t *__restrict__ count) {
+  // gids within one call are distinct: plain read-modify-write is race free
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * width; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / width, c = t - k * width, g = gid[k];
+    sum[g * width + c] = __fadd_rn(sum[g * width + c], pred[t]);
+    if (c == 0) count[g] += 1;
+  }
+}
+__global__ void reassemble_fin_kernel(const float *__restrict__ sum, const int32_t *__restrict__ count,
+                                      int64_t n_points, int width, float *__restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_points * width;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = count[t / width];
+    out[t] = c > 0 ? __fdiv_rn(sum[t], (float)c) : 0.f;
+  }
+}
+
 // ------------------------------------------------------------------- CSC --
 __global__ void iota_i32(int32_t *o, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
@@ -285,6 +304,24 @@ dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *val
       if (b == a) continue;
       DS_TRY(dsmpnn_halo_scatter_add(values[q] + a * width, send_idx[p] + s0, b - a, width, values[p], stream));
     }
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_reassemble_accumulate(const float *pred, const int64_t *gid, int64_t n, int32_t width,
+                                           float *sum, int32_t *count, void *stream) {
+  DS_CHECK_ARG(n >= 0 && width > 0, DSMPNN_ERR_INVALID_ARG, "reassemble_accumulate: sizes");
+  if (n == 0) return DSMPNN_OK;
+  reassemble_acc_kernel<<<grid_for(n * width), 256, 0, as_stream(stream)>>>(pred, gid, n, width, sum, count);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_reassemble_finalize(const float *sum, const int32_t *count, int64_t n_points, int32_t width,
+                                         float *out, void *stream) {
+  DS_CHECK_ARG(n_points >= 0 && width > 0, DSMPNN_ERR_INVALID_ARG, "reassemble_finalize: sizes");
+  if (n_points == 0) return DSMPNN_OK;
+  reassemble_fin_kernel<<<grid_for(n_points * width), 256, 0, as_stream(stream)>>>(sum, count, n_points, width, out);
+  DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
 

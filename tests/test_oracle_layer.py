@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from oracle import decomp, graph, layer
+from oracle import decomp, graph, layer, sample
 from oracle.layer import ACT_IDENTITY, ACT_RELU, ROOT_DENSE, ROOT_IDENTITY, ROOT_NONE, LayerDesc
 
 ROOTS = {"none": ROOT_NONE, "identity": ROOT_IDENTITY, "dense": ROOT_DENSE}
@@ -358,3 +358,42 @@ def test_ds_detach_exact_at_one_layer_only():
     g2_ds, _ = _ds_grads(4, 2, decomp.DETACH)
     g2_ref, _ = _ds_grads(1, 2, decomp.DETACH)
     assert not _close(g2_ds, g2_ref, 1e-6)
+
+
+def _infer_case(seed=71, n=300, P=4):
+    x, gid, attr, r, desc, W, vg = _decomp_case(seed, P, 1, 2)
+    return x, attr, r, desc, W, vg
+
+
+def test_infer_reassemble_single_pass_equals_undecomposed():
+    # f4 with s = N and one pass: every node visited once, and the decomposed
+    # forward equals the single-domain forward (north_star property), so the
+    # reassembled field is exactly the S-MPNN output
+    x, attr, r, desc, W, vg = _infer_case()
+    n = len(x)
+    l = r * (1 + 2 ** -12)
+    field, cnt = decomp.infer_reassemble(desc, W, x, attr, 4, l, r, 8, 5, n, [9], vg, 2, "diff")
+    assert np.all(cnt == 1)
+    ids = sample.sample(n, n, 9).astype(np.int64)
+    _, _, _, single = decomp.build_local(x[ids], ids, attr[ids], 1, l, r, 8, 5, "diff")
+    ref = decomp.ds_forward(desc, W, single, lambda rows: vg[ids[rows]], 2)[0]
+    g = single[0]["local_gid"]
+    assert np.array_equal(field[g], ref)
+
+
+def test_infer_reassemble_counts_and_averages():
+    x, attr, r, desc, W, vg = _infer_case(seed=72)
+    n = len(x)
+    l = r * (1 + 2 ** -12)
+    s = n // 3
+    seeds = [1, 2, 3]
+    field, cnt = decomp.infer_reassemble(desc, W, x, attr, 2, l, r, 8, 5, s, seeds, vg, 1, "diff")
+    want = np.zeros(n, np.int64)
+    for sd in seeds:
+        want[sample.sample(n, s, sd)] += 1
+    assert np.array_equal(cnt, want)
+    assert np.all(field[cnt == 0] == 0.0)
+    # the same pass twice averages to the pass itself (exact in fp64)
+    f1, c1 = decomp.infer_reassemble(desc, W, x, attr, 2, l, r, 8, 5, s, [4], vg, 1, "diff")
+    f2, c2 = decomp.infer_reassemble(desc, W, x, attr, 2, l, r, 8, 5, s, [4, 4], vg, 1, "diff")
+    assert np.array_equal(c2, 2 * c1) and np.array_equal(f1, f2)

@@ -273,6 +273,26 @@ dsmpnn_status dsmpnn_reassemble_accumulate(const float *pred, const int64_t *gid
 dsmpnn_status dsmpnn_reassemble_finalize(const float *sum, const int32_t *count, int64_t n_points, int32_t width,
                                          float *out, void *stream);
 
+/* ----------------------------------------------------------- f3 --------- */
+/* GCN layer, the paper's node-based comparison model ("GCN here
+ * uses 6 hidden layers with a size of 378"; SURVEY §8(f) f3;
+ * reading R24: same radius graph as the MPNN, mean over N(i) u {i}), fp32:
+ *   agg_i = (v_i + sum_{p in row i} v_{col p}) / (deg_i + 1)
+ *   out_i = act(W agg_i + c),  W float32 [d_out x d_in] (PyTorch layout), c [d_out]
+ * v [n_loc x d_in] (rows 0..n_dst-1 are the destinations), CSR by destination.
+ * gcn_fwd writes agg [n_dst x d_in] (kept for the backward) and out
+ * [n_dst x d_out].  gcn_bwd, for grad_out [n_dst x d_out], ACCUMULATES
+ * grad_v [n_loc x d_in] (+=, any may be NULL), grad_W, grad_c; csc_perm /
+ * csc_ptr from dsmpnn_csc.  Deterministic (fixed summation orders). */
+dsmpnn_status dsmpnn_gcn_fwd(int32_t d_in, int32_t d_out, int32_t act, const float *W, const float *c,
+                             const float *v, const int64_t *row_ptr, const int32_t *col_idx, int64_t n_dst,
+                             float *agg, float *out, void *stream);
+dsmpnn_status dsmpnn_gcn_bwd_workspace_size(int32_t d_in, int32_t d_out, int64_t n_dst, size_t *bytes);
+dsmpnn_status dsmpnn_gcn_bwd(int32_t d_in, int32_t d_out, int32_t act, const float *W, const int64_t *row_ptr,
+                             const int32_t *col_idx, const int32_t *csc_perm, const int64_t *csc_ptr, int64_t n_dst,
+                             int64_t n_loc, const float *agg, const float *out, const float *grad_out, float *grad_v,
+                             float *grad_W, float *grad_c, void *ws, size_t ws_bytes, void *stream);
+
 /* --------------------------------------------------------------- GEMM --- */
 /* Dense bf16 GEMM on the tcgen05 tensor cores, fp32 accumulate:
  *   C[M x N] (+)= A[M x K] . B[K x N]

@@ -94,6 +94,9 @@ _f = {
                                       C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, P),
     "reassemble_accumulate": _sig("reassemble_accumulate", P, P, I64, I32, P, P, P),
     "reassemble_finalize": _sig("reassemble_finalize", P, P, I64, I32, P, P),
+    "gcn_fwd": _sig("gcn_fwd", I32, I32, I32, P, P, P, P, P, I64, P, P, P),
+    "gcn_bwd_workspace_size": _sig("gcn_bwd_workspace_size", I32, I32, I64, C.POINTER(SZ)),
+    "gcn_bwd": _sig("gcn_bwd", I32, I32, I32, P, P, P, P, P, I64, I64, P, P, P, P, P, P, P, SZ, P),
     "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
     "probe_begin": _sig("probe_begin", I32, I32),
     "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
@@ -308,6 +311,24 @@ def reassemble_accumulate(pred, gid, sum_, count, stream=None):
 
 def reassemble_finalize(sum_, count, out, stream=None):
     _call("reassemble_finalize", _p(sum_), _p(count), sum_.shape[0], sum_.shape[1], _p(out), _stream(stream))
+
+
+def gcn_fwd(W, c, act, v, row_ptr, col_idx, n_dst, agg, out, stream=None):
+    """f3 GCN layer forward (fp32): agg = mean over N(i) u {i}; out = act(agg W^T + c)."""
+    d_out, d_in = W.shape
+    _call("gcn_fwd", d_in, d_out, act, _p(W), _p(c), _p(v), _p(row_ptr), _p(col_idx), n_dst, _p(agg), _p(out),
+          _stream(stream))
+
+
+def gcn_bwd(W, act, row_ptr, col_idx, csc_perm, csc_ptr, n_dst, n_loc, agg, out, grad_out, grad_v, grad_W, grad_c,
+            ws=None, stream=None):
+    """f3 GCN layer backward; accumulates grad_v, grad_W, grad_c (any may be None)."""
+    d_out, d_in = W.shape
+    sz = SZ()
+    _call("gcn_bwd_workspace_size", d_in, d_out, n_dst, C.byref(sz))
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, out.device)
+    _call("gcn_bwd", d_in, d_out, act, _p(W), _p(row_ptr), _p(col_idx), _p(csc_perm), _p(csc_ptr), n_dst, n_loc,
+          _p(agg), _p(out), _p(grad_out), _p(grad_v), _p(grad_W), _p(grad_c), _p(ws), ws.numel(), _stream(stream))
 
 
 def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=None, accumulate=False,

@@ -222,13 +222,15 @@ def run_reference(args):
     for _ in range(args.warmup):
         oracle_baseline(args.config, per_step_budget / 4, world)
     vals = []
+    t0 = time.perf_counter()
     for _ in range(args.steps):
         vals.append(oracle_baseline(args.config, per_step_budget, world))
+    step_ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
     value = float(np.median([v["value"] for v in vals]))
     cb = dict(vals[-1])
     cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: BASELINE.json configs sample (CPU oracle, bounded)"},
             "cpu_baseline": cb,

@@ -25,11 +25,14 @@
 
 namespace dsmpnn {
 
+constexpr int kReach = 2;
+
 struct GridParams {
   float lo[3];
   float inv_h;
   int n[3];
   int n_cells;
+  int reach;  // neighbour cells scanned on each side: cell edge >= r / reach
 };
 
 // fp32 predicate in the fixed order of R7 (no FMA contraction)
@@ -90,6 +93,7 @@ __global__ void grid_params_kernel(const float *__restrict__ bb, int dim, float 
   for (int d = 0; d < 3; ++d) { p.lo[d] = d < dim ? bb[d] : 0.f; p.n[d] = d < dim ? n[d] : 1; }
   p.inv_h = 1.0f / h;
   p.n_cells = p.n[0] * p.n[1] * p.n[2];
+  p.reach = kReach;
   *gp = p;
 }
 
@@ -133,9 +137,10 @@ __device__ __forceinline__ void scan_candidates(int64_t i, const float *__restri
   for (int d = 0; d < dim; ++d) xi[d] = x[i * dim + d];
   int c[3] = {0, 0, 0};
   for (int d = 0; d < dim; ++d) c[d] = cell_coord(xi[d], p.lo[d], p.inv_h, p.n[d]);
-  int z0 = dim == 3 ? max(c[2] - 1, 0) : 0, z1 = dim == 3 ? min(c[2] + 1, p.n[2] - 1) : 0;
-  int y0 = max(c[1] - 1, 0), y1 = min(c[1] + 1, p.n[1] - 1);
-  int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, p.n[0] - 1);
+  const int R = p.reach;
+  int z0 = dim == 3 ? max(c[2] - R, 0) : 0, z1 = dim == 3 ? min(c[2] + R, p.n[2] - 1) : 0;
+  int y0 = max(c[1] - R, 0), y1 = min(c[1] + R, p.n[1] - 1);
+  int x0 = max(c[0] - R, 0), x1 = min(c[0] + R, p.n[0] - 1);
   for (int cz = z0; cz <= z1; ++cz)
     for (int cy = y0; cy <= y1; ++cy) {
       // cells (x0..x1, cy, cz) are contiguous in the sorted order
@@ -310,9 +315,10 @@ __device__ __forceinline__ void scan_sorted(int64_t i, const float *__restrict__
   for (int d = 0; d < dim; ++d) xi[d] = x[i * dim + d];
   int c[3] = {0, 0, 0};
   for (int d = 0; d < dim; ++d) c[d] = cell_coord(xi[d], p.lo[d], p.inv_h, p.n[d]);
-  const int z0 = dim == 3 ? max(c[2] - 1, 0) : 0, z1 = dim == 3 ? min(c[2] + 1, p.n[2] - 1) : 0;
-  const int y0 = max(c[1] - 1, 0), y1 = min(c[1] + 1, p.n[1] - 1);
-  const int x0 = max(c[0] - 1, 0), x1 = min(c[0] + 1, p.n[0] - 1);
+  const int R = p.reach;
+  const int z0 = dim == 3 ? max(c[2] - R, 0) : 0, z1 = dim == 3 ? min(c[2] + R, p.n[2] - 1) : 0;
+  const int y0 = max(c[1] - R, 0), y1 = min(c[1] + R, p.n[1] - 1);
+  const int x0 = max(c[0] - R, 0), x1 = min(c[0] + R, p.n[0] - 1);
   for (int cz = z0; cz <= z1; ++cz)
     for (int cy = y0; cy <= y1; ++cy) {
       const int base = (cz * p.n[1] + cy) * p.n[0];
@@ -532,7 +538,10 @@ static dsmpnn_status build_cells(const float *coords, const int64_t *gid, int64_
   st.scan_tmp = c.take<char>(scan_tmp);
   st.scan_bytes = scan_tmp;
   bbox_kernel<<<1, 1024, 0, s>>>(coords, n_loc, dim, bb);
-  float h0 = r * 1.00390625f;  // cell edge r(1+2^-8): only needs to be >= r
+  // cell edge r(1+2^-8)/kReach: kReach cells on each side cover r with a margin
+  // for the rounding of the cell index; smaller cells scan less area per row
+  // ((2 kReach + 1)^dim cells of edge r/kReach: 6.25 r^2 instead of 9 r^2 in 2-D)
+  float h0 = r * 1.00390625f / (float)kReach;
   grid_params_kernel<<<1, 1, 0, s>>>(bb, dim, h0, maxc, st.gp);
   int g = (int)std::min<int64_t>(ceil_div(n_loc, 256), 148 * 8);
   cell_id_kernel<<<g, 256, 0, s>>>(coords, n_loc, dim, st.gp, cell, idx);

@@ -367,7 +367,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None,
+            "scaling": "weak" if cfg.kind == "weak" else "strong", "vs_baseline": None,
             "dtype": "bf16" if sc.dtype == L.BF16 else "f32", "data": "synthetic",
             "config": {"workload": f"{cfg.name} (BASELINE.json configs[{list(synth.CONFIGS).index(cfg.name)}])",
                        "n_points": sc.n_points, "sampled": sc.s, "subdomains": sc.nparts, "radius": sc.r,

@@ -46,6 +46,7 @@ class StepConfig:
     seed_sampling: int = 0
     seed_capping: int = 0
     grad_mode: int = DETACH
+    overlap_halo: int = -1  # 1: deep rows of a layer run while the previous halo refresh is in flight; -1: when world > 1
 
 
 def parts_of_process(nparts, world, rank):
@@ -102,12 +103,18 @@ class HotPath:
             self.ws[key] = t
         return t
 
-    def halo(self, vals, dtype):
+    def _comm_stream(self):
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream(self.dev)
+        return self._comm
+
+    def halo(self, vals, dtype, stream=None):
         """Overlap update (Alg. 1) for every local sub-domain."""
         if self.world == 1:
-            pipeline.halo_exchange_loopback(self.subs, vals, dtype)
+            pipeline.halo_exchange_loopback(self.subs, vals, dtype, stream=stream)
         else:
-            pipeline.halo_exchange_mixed(self.subs, vals, dtype, self.proc_of, self.rank, self.group)
+            pipeline.halo_exchange_mixed(self.subs, vals, dtype, self.proc_of, self.rank, self.group,
+                                         stream=stream)
 
     def halo_reverse(self, grads):
         """REVERSE_ADD of fp32 gradients (f2) for every local sub-domain."""
@@ -131,20 +138,53 @@ class HotPath:
             L.gather_rows(v0, sd.local_rows, v)
             vals.append(v.to(vdt) if lowp else v)
         acts = [vals]
+        overlap = c.overlap_halo == 1 or (c.overlap_halo < 0 and self.world > 1)
+        main = torch.cuda.current_stream(self.dev)
+        comm = self._comm_stream() if overlap else None
+        ex_done = None
+
+        def run(layer, q, sd, out, nv, a, b):
+            if b <= a:
+                return
+            ws = self._ws(("fwd", layer, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
+            e = sd.e16 if lowp else sd.e32
+            L.layer_fwd(desc, self.W, self.packed, acts[-1][q], e, sd.row_ptr, sd.col_idx, sd.n_own, a, b,
+                        out, nv[: sd.n_own] if lowp else None, ws, row_ptr_host=sd.row_ptr_host)
+            if not lowp:
+                nv[a:b].copy_(out[a:b])
+
         for layer in range(c.L):
-            nxt = []
+            nxt, outs_l = [], []
             for q, sd in enumerate(self.subs):
-                ws = self._ws(("fwd", layer, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
-                out = self._ws(("out", q), sd.n_own * c.d * 4).view(torch.float32)[: sd.n_own * c.d].view(sd.n_own, c.d)
-                nv = torch.empty((sd.n_loc, c.d), dtype=vdt, device=self.dev)
-                e = sd.e16 if lowp else sd.e32
-                L.layer_fwd(desc, self.W, self.packed, acts[-1][q], e, sd.row_ptr, sd.col_idx, sd.n_own, 0, sd.n_own,
-                            out, nv[: sd.n_own] if lowp else None, ws, row_ptr_host=sd.row_ptr_host)
-                if not lowp:
-                    nv[: sd.n_own].copy_(out)
-                nxt.append(nv)
-            self.halo(nxt, L.BF16 if lowp else L.F32)
+                outs_l.append(self._ws(("out", q), sd.n_own * c.d * 4).view(torch.float32)[: sd.n_own * c.d]
+                              .view(sd.n_own, c.d))
+                nxt.append(torch.empty((sd.n_loc, c.d), dtype=vdt, device=self.dev))
+            if not overlap:
+                for q, sd in enumerate(self.subs):
+                    run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_own)
+                self.halo(nxt, L.BF16 if lowp else L.F32)
+            else:
+                # deep rows have no halo neighbour (R23): they run while the
+                # previous layer's halo refresh is still in flight
+                for q, sd in enumerate(self.subs):
+                    run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_deep)
+                if ex_done is not None:
+                    main.wait_event(ex_done)
+                for q, sd in enumerate(self.subs):
+                    run(layer, q, sd, outs_l[q], nxt[q], sd.n_deep, sd.n_own)
+                # only near rows are sent (R23): the refresh can start now
+                ready = torch.cuda.Event()
+                ready.record(main)
+                comm.wait_event(ready)
+                for t in nxt:
+                    t.record_stream(comm)
+                with torch.cuda.stream(comm):
+                    self.halo(nxt, L.BF16 if lowp else L.F32, stream=comm)
+                ex_done = torch.cuda.Event()
+                ex_done.record(comm)
             acts.append(nxt)
+        if ex_done is not None:
+            main.wait_event(ex_done)
         outs = [self.ws[("out", q)].view(torch.float32)[: sd.n_own * c.d].view(sd.n_own, c.d)
                 for q, sd in enumerate(self.subs)]
         return acts, outs

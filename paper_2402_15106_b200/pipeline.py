@@ -131,10 +131,10 @@ def build_graph(sd: Subdomain, r, n_e, seed, edge_mode, want_f32=True, want_bf16
     return build_graphs([sd], r, n_e, seed, edge_mode, want_f32, want_bf16)[0]
 
 
-def halo_exchange_loopback(subs, values, dtype):
+def halo_exchange_loopback(subs, values, dtype, stream=None):
     """FORWARD halo refresh among virtual ranks resident on this device."""
     L.halo_exchange_loopback(values, [s.halo_ptr for s in subs], [s.send_ptr for s in subs],
-                             [s.send_idx for s in subs], dtype)
+                             [s.send_idx for s in subs], dtype, stream=stream)
 
 
 def halo_reverse_loopback(subs, grads):
@@ -195,7 +195,7 @@ def halo_reverse_mixed(subs, grads, proc_of, my_proc, group=None, scatter_add=No
             scatter_add(src, psd.send_idx[s0:s1], pg)
 
 
-def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gather=None):
+def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gather=None, stream=None):
     """FORWARD halo refresh when sub-domains are spread over processes.
 
     subs/values: this process's sub-domains and their [n_loc x width] arrays.
@@ -210,7 +210,7 @@ def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gathe
     import torch.distributed as dist
     if gather is None:
         def gather(vals, rows, out):
-            L.halo_gather(vals, rows, out, dtype)
+            L.halo_gather(vals, rows, out, dtype, stream=stream)
     local = {sd.rank: (sd, v) for sd, v in zip(subs, values)}
     nparts = subs[0].nparts
     ops = []

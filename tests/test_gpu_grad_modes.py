@@ -76,3 +76,27 @@ def test_reverse_add_equals_undecomposed_and_detach_does_not(lib):
         assert nerr(got[n], single[n]) <= 1e-5, n
     det = _gpu(c, decomp.DETACH, 0)
     assert max(nerr(det[n], single[n]) for n in NAMES) > 1e-3
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_overlapped_halo_refresh_is_bitwise_identical(lib, dtype):
+    """a6 overlapped with interior compute: deep rows (no halo neighbour, R23)
+    of each layer run while the previous halo refresh is in flight on a
+    separate stream; results must not change."""
+    import dataclasses
+    from paper_2402_15106_b200 import _lib as Lib
+    from paper_2402_15106_b200.api import HotPath, StepConfig
+    c = _case(seed=63) if dtype == 0 else _case(seed=63, d=64, k=256)
+    l = c["r"] * (1 + 2 ** -12)
+    base = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
+                      n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
+                      seed_sampling=3, seed_capping=5, overlap_halo=0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda())
+    res = []
+    for ov in (0, 1):
+        hp = HotPath(dataclasses.replace(base, overlap_halo=ov), c["W"], cuda())
+        g = hp.step(T(c["x"]), T(c["a"]), T(c["v0"]), T(c["G"]))
+        torch.cuda.synchronize()
+        res.append({n: g[n].cpu().numpy().copy() for n in NAMES})
+    for n in NAMES:
+        assert np.array_equal(res[0][n], res[1][n]), n

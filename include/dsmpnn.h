@@ -293,6 +293,37 @@ dsmpnn_status dsmpnn_gcn_bwd(int32_t d_in, int32_t d_out, int32_t act, const flo
                              int64_t n_loc, const float *agg, const float *out, const float *grad_out, float *grad_v,
                              float *grad_W, float *grad_c, void *ws, size_t ws_bytes, void *stream);
 
+/* ----------------------------------------------------------- f1 --------- */
+/* The training step around the layer (PAPER.md eqs. (i), (iii), (iv) :39-42,
+ * Alg. 1 :404-419), fp32:
+ * mlp3: 3 Linear layers, ReLU after the first two (encoder N_e, decoder N_d).
+ *   Wb = {W0, b0, W1, b1, W2, b2}, W_l PyTorch [out, in]; x [n x in_dim],
+ *   h1, h2 [n x hid] (kept for the backward), y [n x out_dim].
+ *   mlp3_bwd ACCUMULATES dWb (+=, entries may be NULL) and dx (+=, may be
+ *   NULL) for dy [n x out_dim].
+ * edge_refresh_bwd: backward of (iv) e_ij = (.., u_i - u_j, ..) where the u
+ *   difference occupies columns [off, off + width) of the d_e-wide edge
+ *   attribute: grad_u[j] += sum_{p in row j} grad_e[p] - sum_{p: col p = j}
+ *   grad_e[p] (rows j < n_dst are destinations; CSC view from dsmpnn_csc).
+ * mse: *sse += sum (pred - target)^2 (one block, fixed order) and, if grad is
+ *   not NULL, grad = 2 (pred - target) * scale.
+ * sgd: w -= lr g (Alg. 1 :419).  adam: Adam with bias
+ *   correction for step >= 1, m / v updated in place. */
+dsmpnn_status dsmpnn_mlp3_fwd(int32_t in_dim, int32_t hid, int32_t out_dim, const float *const *Wb, const float *x,
+                              int64_t n, float *h1, float *h2, float *y, void *stream);
+dsmpnn_status dsmpnn_mlp3_bwd_workspace_size(int32_t in_dim, int32_t hid, int32_t out_dim, int64_t n, size_t *bytes);
+dsmpnn_status dsmpnn_mlp3_bwd(int32_t in_dim, int32_t hid, int32_t out_dim, const float *const *Wb, const float *x,
+                              const float *h1, const float *h2, const float *dy, int64_t n, float *dx,
+                              float *const *dWb, void *ws, size_t ws_bytes, void *stream);
+dsmpnn_status dsmpnn_edge_refresh_bwd(const float *grad_e, int32_t d_e, int32_t off, int32_t width,
+                                      const int64_t *row_ptr, const int32_t *csc_perm, const int64_t *csc_ptr,
+                                      int64_t n_dst, int64_t n_loc, float *grad_u, void *stream);
+dsmpnn_status dsmpnn_mse(const float *pred, const float *target, int64_t n_elems, float scale, float *grad,
+                         float *sse, void *stream);
+dsmpnn_status dsmpnn_sgd(float *w, const float *g, int64_t n, float lr, void *stream);
+dsmpnn_status dsmpnn_adam(float *w, const float *g, float *m, float *v, int64_t n, float lr, float beta1, float beta2,
+                          float eps, int32_t step, void *stream);
+
 /* --------------------------------------------------------------- GEMM --- */
 /* Dense bf16 GEMM on the tcgen05 tensor cores, fp32 accumulate:
  *   C[M x N] (+)= A[M x K] . B[K x N]

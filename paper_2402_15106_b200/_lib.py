@@ -97,6 +97,13 @@ _f = {
     "gcn_fwd": _sig("gcn_fwd", I32, I32, I32, P, P, P, P, P, I64, P, P, P),
     "gcn_bwd_workspace_size": _sig("gcn_bwd_workspace_size", I32, I32, I64, C.POINTER(SZ)),
     "gcn_bwd": _sig("gcn_bwd", I32, I32, I32, P, P, P, P, P, I64, I64, P, P, P, P, P, P, P, SZ, P),
+    "mlp3_fwd": _sig("mlp3_fwd", I32, I32, I32, C.POINTER(P), P, I64, P, P, P, P),
+    "mlp3_bwd_workspace_size": _sig("mlp3_bwd_workspace_size", I32, I32, I32, I64, C.POINTER(SZ)),
+    "mlp3_bwd": _sig("mlp3_bwd", I32, I32, I32, C.POINTER(P), P, P, P, P, I64, P, C.POINTER(P), P, SZ, P),
+    "edge_refresh_bwd": _sig("edge_refresh_bwd", P, I32, I32, I32, P, P, P, I64, I64, P, P),
+    "mse": _sig("mse", P, P, I64, F, P, P, P),
+    "sgd": _sig("sgd", P, P, I64, F, P),
+    "adam": _sig("adam", P, P, P, P, I64, F, F, F, F, I32, P),
     "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
     "probe_begin": _sig("probe_begin", I32, I32),
     "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
@@ -329,6 +336,46 @@ def gcn_bwd(W, act, row_ptr, col_idx, csc_perm, csc_ptr, n_dst, n_loc, agg, out,
     ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, out.device)
     _call("gcn_bwd", d_in, d_out, act, _p(W), _p(row_ptr), _p(col_idx), _p(csc_perm), _p(csc_ptr), n_dst, n_loc,
           _p(agg), _p(out), _p(grad_out), _p(grad_v), _p(grad_W), _p(grad_c), _p(ws), ws.numel(), _stream(stream))
+
+
+def _ptrs(ts):
+    return (P * len(ts))(*[None if t is None else t.data_ptr() for t in ts])
+
+
+def mlp3_fwd(Wb, x, h1, h2, y, stream=None):
+    """3-layer MLP forward (f1): Wb = [W0, b0, W1, b1, W2, b2]."""
+    hid, in_dim = Wb[0].shape
+    out_dim = Wb[4].shape[0]
+    _call("mlp3_fwd", in_dim, hid, out_dim, _ptrs(Wb), _p(x), x.shape[0], _p(h1), _p(h2), _p(y), _stream(stream))
+
+
+def mlp3_bwd(Wb, x, h1, h2, dy, dx, dWb, ws=None, stream=None):
+    hid, in_dim = Wb[0].shape
+    out_dim = Wb[4].shape[0]
+    n = x.shape[0]
+    sz = SZ()
+    _call("mlp3_bwd_workspace_size", in_dim, hid, out_dim, n, C.byref(sz))
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, x.device)
+    _call("mlp3_bwd", in_dim, hid, out_dim, _ptrs(Wb), _p(x), _p(h1), _p(h2), _p(dy), n, _p(dx), _ptrs(dWb),
+          _p(ws), ws.numel(), _stream(stream))
+
+
+def edge_refresh_bwd(grad_e, off, width, row_ptr, csc_perm, csc_ptr, n_dst, n_loc, grad_u, stream=None):
+    _call("edge_refresh_bwd", _p(grad_e), grad_e.shape[1], off, width, _p(row_ptr), _p(csc_perm), _p(csc_ptr),
+          n_dst, n_loc, _p(grad_u), _stream(stream))
+
+
+def mse(pred, target, scale, grad, sse, stream=None):
+    _call("mse", _p(pred), _p(target), pred.numel(), float(scale), _p(grad), _p(sse), _stream(stream))
+
+
+def sgd(w, g, lr, stream=None):
+    _call("sgd", _p(w), _p(g), w.numel(), float(lr), _stream(stream))
+
+
+def adam(w, g, m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+    _call("adam", _p(w), _p(g), _p(m), _p(v), w.numel(), float(lr), float(beta1), float(beta2), float(eps),
+          int(step), _stream(stream))
 
 
 def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=None, accumulate=False,

@@ -270,3 +270,174 @@ class HotPath:
         """One full hot-path step on device inputs."""
         self.build(coords, attr)
         return self.forward_backward(v0, G)
+
+
+class TrainStep:
+    """one DS-MPNN training step (PAPER.md eqs. (i)-(iv),
+    Alg. 1 :404-419) over the C ABI, fp32.  Per sub-domain: the encoder N_e on
+    every local row, then `hops` times {residual convolution (the layer in
+    paper form: identity root = the residual, identity sigma) on owned rows,
+    halo refresh of the latent values, decoder N_d on every local row, edge
+    refresh (iv) e_ij = (x_i - x_j, u_i - u_j)}; MSE of the last decoded values
+    on owned rows; backward with received values detached (R16); gradient sum
+    over processes; SGD (Alg. 1 :419) or Adam.  The oracle is
+    oracle/train.py (O9).
+
+    params: dict enc=[(W, b)] * 3, dec=[(W, b)] * 3 (PyTorch [out, in]),
+    conv=layer weights (W1, b1, W2, b2, W3, b3, b)."""
+
+    CONV = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
+
+    def __init__(self, cfg: StepConfig, params: dict, hops: int, device, rank=0, world=1, group=None,
+                 optimizer="sgd", lr=1e-3):
+        import dataclasses
+        assert cfg.dtype == L.F32, "the training step runs in F32 mode"
+        cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops)
+        conv = dict(params["conv"])
+        conv.setdefault("W_root", np.zeros((cfg.d, cfg.d), np.float32))  # identity root: unused
+        self.hp = HotPath(cfg, conv, device, rank, world, group)
+        self.dev, self.hops, self.opt, self.lr = device, hops, optimizer, lr
+        T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32).to(device)
+        self.enc = [T(x) for Wl, bl in params["enc"] for x in (Wl, bl)]
+        self.dec = [T(x) for Wl, bl in params["dec"] for x in (Wl, bl)]
+        self.g_enc = [torch.zeros_like(t) for t in self.enc]
+        self.g_dec = [torch.zeros_like(t) for t in self.dec]
+        self.m = self.v = None
+        self.t = 0
+
+    def build(self, coords, attr):
+        self.hp.build(coords, attr)
+        self.coords = coords
+        return self
+
+    def _mlp(self, Wb, x):
+        n = x.shape[0]
+        hid, out_dim = Wb[0].shape[0], Wb[4].shape[0]
+        h1 = torch.empty((n, hid), device=self.dev)
+        h2 = torch.empty((n, hid), device=self.dev)
+        y = torch.empty((n, out_dim), device=self.dev)
+        L.mlp3_fwd(Wb, x, h1, h2, y)
+        return y, (x, h1, h2)
+
+    def loss_and_grads(self, v0_global, Y_global):
+        """v0_global [N x (dim + n_attr)] initial node values, Y_global
+        [N x n_attr] targets (rows = point ids).  Returns (loss, grads) with
+        grads = dict(enc=[...], dec=[...], conv=HotPath.grads)."""
+        hp, c = self.hp, self.hp.cfg
+        desc, subs = hp.desc, hp.subs
+        n_attr, dim = c.n_attr, c.dim
+        for g in self.g_enc + self.g_dec + list(hp.grads.values()):
+            g.zero_()
+        gidx = [sd.gid.to(torch.int64) for sd in subs]  # local rows -> point ids
+        enc_cache, vL, e = [], [], []
+        for sd, gi in zip(subs, gidx):
+            v0 = torch.empty((sd.n_loc, v0_global.shape[1]), device=self.dev)
+            L.gather_rows(v0_global, gi, v0)
+            y, cache = self._mlp(self.enc, v0)
+            enc_cache.append(cache)
+            vL.append(y)
+            e.append(sd.e32)
+        hist = []
+        for hop in range(self.hops):
+            new = []
+            for q, sd in enumerate(subs):
+                ws = hp._ws(("fwd", hop, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
+                out = torch.empty((sd.n_own, c.d), device=self.dev)
+                L.layer_fwd(desc, hp.W, hp.packed, vL[q], e[q], sd.row_ptr, sd.col_idx, sd.n_own, 0, sd.n_own, out,
+                            None, ws, row_ptr_host=sd.row_ptr_host)
+                nv = vL[q].clone()
+                nv[: sd.n_own].copy_(out)
+                new.append(nv)
+            hp.halo(new, L.F32)
+            dec_cache, u, e_next = [], [], []
+            for q, sd in enumerate(subs):
+                uq, cache = self._mlp(self.dec, new[q])
+                dec_cache.append(cache)
+                u.append(uq)
+                en = torch.empty((max(sd.n_edges, 1), dim + n_attr), device=self.dev)
+                L.edge_features(L.EDGE_DIFF, sd.coords, uq, sd.row_ptr, sd.col_idx, sd.n_own, e32=en)
+                e_next.append(en)
+            hist.append(dict(vin=vL, e=e, vout=new, dec_cache=dec_cache, u=u))
+            vL, e = new, e_next
+        # loss: MSE of the last decoded values on owned rows, over all ranks
+        count = sum(sd.n_own for sd in subs) * n_attr
+        if hp.world > 1:
+            import torch.distributed as dist
+            ct = torch.tensor([float(count)], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(ct, group=hp.group)
+            count = int(ct.item())
+        sse = torch.zeros(1, device=self.dev)
+        du = []
+        for q, sd in enumerate(subs):
+            d = torch.zeros((sd.n_loc, n_attr), device=self.dev)
+            yq = torch.empty((sd.n_own, n_attr), device=self.dev)
+            L.gather_rows(Y_global, gidx[q][: sd.n_own], yq)
+            L.mse(hist[-1]["u"][q][: sd.n_own].contiguous(), yq, 1.0 / count, d, sse)
+            du.append(d)
+        # backward
+        dvL_in = None
+        for hop in reversed(range(self.hops)):
+            H = hist[hop]
+            dvout = []
+            for q, sd in enumerate(subs):
+                dd = du[q]
+                dd[sd.n_own:].zero_()  # decoded halo values are received (detached)
+                # gradient of the hop's output: from the next hop's input (if any)
+                # plus the decoder's (mlp3_bwd accumulates dx)
+                dx = dvL_in[q] if dvL_in is not None else torch.zeros((sd.n_loc, c.d), device=self.dev)
+                x_, h1, h2 = H["dec_cache"][q]
+                L.mlp3_bwd(self.dec, x_, h1, h2, dd, dx, self.g_dec)
+                dvout.append(dx)
+            dvL_in, du = [], []
+            for q, sd in enumerate(subs):
+                ws = hp.ws[("fwd", hop, q)]
+                bws = hp._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
+                dv = torch.zeros((sd.n_loc, c.d), device=self.dev)
+                de = torch.zeros((max(sd.n_edges, 1), dim + n_attr), device=self.dev) if hop > 0 else None
+                G = dvout[q][: sd.n_own].contiguous()
+                L.layer_bwd(desc, hp.W, hp.packed, H["vin"][q], H["e"][q], sd.row_ptr, sd.col_idx, sd.csc_perm,
+                            sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, G, dv, de, hp.grads, ws, bws,
+                            row_ptr_host=sd.row_ptr_host)
+                dp = torch.zeros((sd.n_loc, n_attr), device=self.dev)
+                if hop > 0:
+                    dv[sd.n_own:].zero_()  # halo latent values of hops > 1 are received (detached)
+                    L.edge_refresh_bwd(de, dim, n_attr, sd.row_ptr, sd.csc_perm, sd.csc_ptr, sd.n_own, sd.n_loc,
+                                       dp)
+                dvL_in.append(dv)
+                du.append(dp)
+        for q, sd in enumerate(subs):
+            x_, h1, h2 = enc_cache[q]
+            L.mlp3_bwd(self.enc, x_, h1, h2, dvL_in[q], None, self.g_enc)
+        if hp.world > 1:
+            import torch.distributed as dist
+            flat = torch.cat([t.reshape(-1) for t in self.g_enc + self.g_dec + [hp.grads[n] for n in self.CONV]]
+                             + [sse])
+            dist.all_reduce(flat, group=hp.group)
+            off = 0
+            for t in self.g_enc + self.g_dec + [hp.grads[n] for n in self.CONV] + [sse]:
+                t.copy_(flat[off:off + t.numel()].view_as(t))
+                off += t.numel()
+        loss = float(sse.item()) / count
+        return loss, dict(enc=self.g_enc, dec=self.g_dec, conv=hp.grads)
+
+    def _params(self):
+        conv = [self.hp.W[n] for n in self.CONV if n != "W_root"]
+        convg = [self.hp.grads[n] for n in self.CONV if n != "W_root"]
+        return self.enc + self.dec + conv, self.g_enc + self.g_dec + convg
+
+    def step(self, v0_global, Y_global):
+        """loss_and_grads, then the parameter update; returns the loss."""
+        loss, _ = self.loss_and_grads(v0_global, Y_global)
+        ws, gs = self._params()
+        self.t += 1
+        if self.opt == "adam":
+            if self.m is None:
+                self.m = [torch.zeros_like(w) for w in ws]
+                self.v = [torch.zeros_like(w) for w in ws]
+            for w, g, m, v in zip(ws, gs, self.m, self.v):
+                L.adam(w, g, m, v, self.lr, self.t)
+        else:
+            for w, g in zip(ws, gs):
+                L.sgd(w, g, self.lr)
+        L.pack_weights(self.hp.desc, self.hp.W, self.hp.packed)  # the layer reads the packed copy
+        return loss

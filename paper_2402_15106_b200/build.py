@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdsmpnn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu"]
+SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu", "train.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]

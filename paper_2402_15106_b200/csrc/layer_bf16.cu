@@ -1,5 +1,5 @@
 // layer_bf16.cu - BF16 mode of the edge-conditioned convolution on the
-// tcgen05 tensor cores (sm_100a).  Formulation: DESIGN.md §4 ("aggregate
+// tcgen05 tensor cores (sm_100a).  Formulation: DESIGN.md §6 ("aggregate
 // first", see layer.cu).  Widths supported: k = 256, d_in = d_out = D in
 // {32, 64}, d_e <= 16 (zero-padded).
 //
@@ -7,13 +7,13 @@
 //   1. fill kernel   : S~_aug[i][k*D + c] = mean_p v_j[c]  (the h~ = 1 row),
 //                      S~_aug[i][(k+1)*D + c] = v_i[c]      (root operand),
 //                      zero S~ rows of isolated nodes.
-//   2. edge kernel   : per 128-slot tile (each row padded to a multiple of 16
-//                      slots): a1 = relu(E W1^T + b1), h = relu(a1 W2^T + b2)
-//                      as two tcgen05 GEMMs (W1, W2 resident in SMEM, D in
-//                      TMEM), then S_i = H_i^T V_i per row (tcgen05, A = H^T
-//                      read MN-major from the same SMEM tile, B = gathered v
-//                      rows), scaled by 1/deg_i -> S~_aug[i][kap*D + c] (bf16).
-//                      K_p = kappa(e_p) (D x D) is never formed.
+//   2. edge kernel   : edge_fwd2.cuh, per 128-slot tile (each row padded to a
+//                      multiple of 16 slots): a1 = relu(E W1^T + b1),
+//                      h = relu(a1 W2^T + b2) as two tcgen05 GEMMs (W1, W2
+//                      resident in SMEM, D in TMEM), then S_i = H_i^T V_i per
+//                      row (A = H^T read MN-major from the same SMEM tile,
+//                      B = gathered v rows), scaled by 1/deg_i ->
+//                      S~_aug[i][c*k + kap] (bf16).  K_p is never formed.
 //   3. node GEMM     : [S~_aug] . [Theta~ ; W_root^T] on tcgen05 (split-K),
 //   4. node epilogue : + b (+ v_i), sigma, out (fp32), out_lowp (bf16), pre.
 #include <cuda.h>
@@ -137,214 +137,6 @@ __global__ void s_fill_kernel(const __nv_bfloat16 *__restrict__ v, const int64_t
   }
 }
 
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    edge_fwd_kernel(const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
-                    const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int64_t eb, int64_t ee,
-                    Packed pw, const float *__restrict__ b1, const float *__restrict__ b2,
-                    __nv_bfloat16 *__restrict__ S, int64_t kp, const int32_t *__restrict__ col) {
-  using C = EF<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space (LDS/STS)
-  uint8_t *sW2 = sm + C::OFF_W2, *sAH = sm + C::OFF_AH, *sV = sm + C::OFF_V, *sW1 = sm + C::OFF_W1,
-          *sE = sm + C::OFF_E;
-  EdgeMisc *m = reinterpret_cast<EdgeMisc *>(sm + C::OFF_MISC);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  // ---- setup: row range of this CTA (balanced by edges), weights -> SMEM, TMEM
-  if (tid == 0) {
-    int64_t E = ee - eb;
-    int64_t t0 = eb + E * (int64_t)blockIdx.x / gridDim.x;
-    int64_t t1 = eb + E * (int64_t)(blockIdx.x + 1) / gridDim.x;
-    // first row whose edge range starts at or after t (lower bound on row_ptr over [rb, re])
-    auto lb = [&](int64_t t) {
-      int64_t lo = rb, hi = re;
-      while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (row_ptr[mid] < t) lo = mid + 1; else hi = mid;
-      }
-      return lo;
-    };
-    m->cur_row = blockIdx.x == 0 ? rb : lb(t0);
-    m->row_end = blockIdx.x + 1 == gridDim.x ? re : lb(t1);
-    m->cur_off = 0;
-    m->node_ctr = 0;
-    tc::mbar_init(&m->bar, 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&m->tmem);
-  {  // W2 (K-major SW128, 4 K-blocks of 64) and W1 (interleaved K=16)
-    const uint4 *g2 = reinterpret_cast<const uint4 *>(pw.W2);
-    for (int q = tid; q < KH * KH / 8; q += 256) {
-      int n = q / (KH / 8), rem = q % (KH / 8);
-      int j = rem / 8, c = rem % 8;
-      *reinterpret_cast<uint4 *>(sW2 + j * (KH * 128) + tc::sw128_off(n, c)) = g2[q];
-    }
-    const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
-    for (int q = tid; q < KH * 2; q += 256) {
-      int r = q / 2, u = q % 2;
-      *reinterpret_cast<uint4 *>(sW1 + il_off(r, u)) = g1[q];
-    }
-  }
-  tc::fence_async_shared();
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = m->tmem;
-  uint32_t phase = 0;  // completed commits on m->bar (uniform across threads)
-
-  const uint32_t aW2 = tc::smem_u32(sW2), aAH = tc::smem_u32(sAH), aV = tc::smem_u32(sV), aW1 = tc::smem_u32(sW1),
-                 aE = tc::smem_u32(sE);
-  constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
-  constexpr uint32_t IDESC_S = tc::idesc_bf16(128, D, true, true);
-  const bool epi = warp >= 4;
-  const int erow = tid - 128;                                    // slot row of an epilogue thread
-  const uint32_t lane_base = epi ? ((uint32_t)(32 * (warp - 4)) << 16) : 0u;
-
-  auto wait_mma = [&]() {
-    tc::mbar_wait(&m->bar, phase & 1);
-    phase++;
-    tc::tc_fence_after();
-  };
-
-  for (;;) {
-    if (tid == 0) build_tile(m, row_ptr);
-    __syncthreads();
-    if (!m->more) break;
-
-    // ---- gather E (interleaved) and V (swizzled) rows of the 128 slots
-    {
-      int s = tid >> 1, u = tid & 1;
-      int p = m->slot_edge[s];
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (p >= 0) val = reinterpret_cast<const uint4 *>(e16 + (int64_t)p * 16)[u];
-      *reinterpret_cast<uint4 *>(sE + il_off(s, u)) = val;
-      constexpr int CH = D / 8;  // 16-byte chunks per v row
-#pragma unroll
-      for (int q = tid; q < 128 * CH; q += 256) {
-        int sl = q / CH, c = q % CH;
-        int pe = m->slot_edge[sl];
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (pe >= 0) x = reinterpret_cast<const uint4 *>(v + (int64_t)col[pe] * D)[c];
-        *reinterpret_cast<uint4 *>(sV + v_off<D>(sl, c)) = x;
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- MMA1: z1 = E . W1^T  (M=128 slots, N=KH, K=16)
-    if (tid == 0) {
-      tc::tc_fence_after();
-      tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC_MLP,
-                      0u);
-      tc::mma_commit(&m->bar);
-    }
-    wait_mma();
-    // ---- epilogue 1: a1 = relu(z1 + b1) -> AH (K-major SW128)
-    if (epi) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < KH; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(tmem + lane_base + c0, r);
-        tc::tmem_ld_wait();
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b1 + c0 + 2 * j), 0.f),
-                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b1 + c0 + 2 * j + 1), 0.f));
-        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
-        int ch = (c0 % 64) / 8;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- MMA2: z2 = a1 . W2^T  (M=128, N=KH, K=KH)
-    if (tid == 0) {
-      tc::tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < KH / 16; ++kk) {
-        uint64_t ad = tc::sdesc(aAH + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
-        uint64_t bd = tc::sdesc(aW2 + (kk / 4) * (KH * 128) + (kk % 4) * 32, 16, 1024, tc::kSw128);
-        tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, kk > 0 ? 1u : 0u);
-      }
-      tc::mma_commit(&m->bar);
-    }
-    wait_mma();
-    // ---- epilogue 2: h = relu(z2 + b2) -> AH
-    if (epi) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < KH; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(tmem + lane_base + c0, r);
-        tc::tmem_ld_wait();
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          pk[j] = tc::pack_bf16(fmaxf(__uint_as_float(r[2 * j]) + __ldg(b2 + c0 + 2 * j), 0.f),
-                                fmaxf(__uint_as_float(r[2 * j + 1]) + __ldg(b2 + c0 + 2 * j + 1), 0.f));
-        uint8_t *blk = sAH + (c0 / 64) * (128 * 128);
-        int ch = (c0 % 64) / 8;
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4 *>(blk + tc::sw128_off(erow, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-    tc::fence_async_shared();
-    tc::tc_fence_before();
-    __syncthreads();
-
-    // ---- per row segment: S_i += H_seg^T V_seg (two kappa halves), then write S~_i
-    const int nseg = m->nseg;
-    for (int g = 0; g < nseg; ++g) {
-      const Seg sg = m->seg[g];
-      const uint32_t ts = (uint32_t)(KH + sg.tslot * 2 * D);
-      if (tid == 0) {
-        tc::tc_fence_after();
-        for (int h = 0; h < 2; ++h) {
-          for (int q = 0; q < sg.nslots / 16; ++q) {
-            int s = sg.slot0 + 16 * q;
-            uint64_t ad = tc::sdesc(aAH + (2 * h) * (128 * 128) + (s / 8) * 1024, 128 * 128, 1024, tc::kSw128);
-            uint64_t bd = D == 64 ? tc::sdesc(aV + (s / 8) * 1024, 8192, 1024, tc::kSw128)
-                                  : tc::sdesc(aV + (s / 8) * 512, 4096, 512, tc::kSw64);
-            tc::mma_bf16_ss(tmem + ts + h * D, ad, bd, IDESC_S, (sg.start && q == 0) ? 0u : 1u);
-          }
-        }
-        tc::mma_commit(&m->bar);
-      }
-      wait_mma();
-      if (epi && sg.complete) {
-        const float inv = 1.0f / (float)sg.deg;
-        __nv_bfloat16 *Si = S + sg.node * kp;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kap = 128 * h + erow;
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 16) {
-            uint32_t r[16];
-            tc::tmem_ld16(tmem + lane_base + ts + h * D + c0, r);
-            tc::tmem_ld_wait();
-            uint32_t pk[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              pk[j] = tc::pack_bf16(__uint_as_float(r[2 * j]) * inv, __uint_as_float(r[2 * j + 1]) * inv);
-            uint4 *dst = reinterpret_cast<uint4 *>(Si + (int64_t)kap * D + c0);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          }
-        }
-      }
-      tc::tc_fence_before();
-      __syncthreads();
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-}
 
 // ------------------------------------------------------- node epilogue
 // pre = sum_z partial[z] + b (+ v_i for IDENTITY); out = sigma(pre)

@@ -25,7 +25,7 @@
 
 namespace dsmpnn {
 
-constexpr int kReach = 2;
+constexpr int kReach = 3;
 
 struct GridParams {
   float lo[3];

@@ -305,6 +305,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     a.mask16 = b.A1 + eb * k;
     a.ldmask = k;
     a.colsum_part = b.db1_part;
+    a.b_resident = true;
     DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
     DS_TRY(tgemm(a, s));
     DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, gr.b1, 1, b.cs_ws, s));

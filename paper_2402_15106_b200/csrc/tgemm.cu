@@ -59,44 +59,48 @@ dsmpnn_status make_tmap_bf16(CUtensorMap *m, const void *base, int64_t inner, in
   return DSMPNN_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool E16 = false>
+template <int BN, bool A_MN, bool B_MN, bool E16 = false, bool BRES = false>
 struct TG {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGES = BN >= 256 ? (E16 ? 3 : 4) : (BN >= 128 ? 5 : 6);
+  // BRES: the whole B (N <= BN, K <= NKB_RES * BK) stays in SMEM for every
+  // tile; only A streams through the stages
+  static constexpr int NKB_RES = 4;
+  static constexpr int STAGES = BRES ? 2 : (BN >= 256 ? (E16 ? 3 : 4) : (BN >= 128 ? 5 : 6));
+  static constexpr int B_STAGE_BYTES = BRES ? 0 : B_BYTES;
+  static constexpr int B_RES_BYTES = BRES ? NKB_RES * B_BYTES : 0;
   // bf16 epilogue staging per epilogue warp: 2 output buffers + 2 mask buffers (32 rows x 128 B each)
   static constexpr int STG_BYTES = E16 ? 4 * 4 * 4096 : 0;
   static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
   static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
   static constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   static constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;                 // double-buffered accumulator
-  static constexpr int SCR_BYTES = 4 * 32 * 17 * 4;                  // colsum transpose scratch
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STG_BYTES + SCR_BYTES + 512;
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_STAGE_BYTES) + B_RES_BYTES + STG_BYTES + 512;
 };
 
 // Persistent: CTA c handles tiles c, c + G, ...  (tile = (m-block, n-block,
 // k-slice), m fastest).  Warp 0 = TMA producer, warp 1 = MMA issuer, warps
 // 2..5 = epilogue; the accumulator is double-buffered in TMEM so the epilogue
 // of tile i overlaps the mainloop of tile i+1.
-template <int BN, bool A_MN, bool B_MN, bool E16>
+template <int BN, bool A_MN, bool B_MN, bool E16, bool BRES>
 __global__ void __launch_bounds__(192, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                  const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap tmask, int64_t M,
                  int64_t N, int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
-  using T = TG<BN, A_MN, B_MN, E16>;
+  using T = TG<BN, A_MN, B_MN, E16, BRES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint8_t *sA = smem;
   uint8_t *sB = smem + T::STAGES * T::A_BYTES;
-  uint8_t *sStg = sB + T::STAGES * T::B_BYTES;  // E16 staging (1024-aligned)
-  float *scr = reinterpret_cast<float *>(sStg + T::STG_BYTES);
-  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(scr) + T::SCR_BYTES);
+  uint8_t *sStg = sB + T::STAGES * T::B_STAGE_BYTES + T::B_RES_BYTES;  // E16 staging (1024-aligned)
+  uint64_t *full = reinterpret_cast<uint64_t *>(sStg + T::STG_BYTES);
   uint64_t *empty = full + T::STAGES;
   uint64_t *tfull = empty + T::STAGES;   // [2]
   uint64_t *tempty = tfull + 2;          // [2]
   uint64_t *mbar = tempty + 2;           // [4][2] mask loads, two buffers per epilogue warp
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 8);
+  uint64_t *bres = mbar + 8;             // resident B loaded (BRES)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nm = (M + T::BM - 1) / T::BM, nn = (N + BN - 1) / BN;
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(192, 1)
       tc::mbar_init(&tempty[a], 4);
     }
     for (int a = 0; a < 8; ++a) tc::mbar_init(&mbar[a], 1);
+    tc::mbar_init(bres, 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&ta);
     tc::tma_prefetch(&tb);
@@ -136,6 +141,20 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (tc::elect_one()) {
+      if (BRES) {  // the whole B once (single N block, no split-K)
+        tc::mbar_expect_tx(bres, (uint32_t)(nkb_total * T::B_BYTES));
+        for (int i = 0; i < nkb_total; ++i) {
+          uint8_t *b = sB + i * T::B_BYTES;
+          const int32_t kc = (int32_t)(i * T::BK);
+          if (!B_MN) {
+            tc::tma_load_2d(b, &tb, bres, kc, 0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / T::B_INNER; ++j)
+              tc::tma_load_2d(b + j * (T::B_ROW * T::BK), &tb, bres, j * T::B_INNER, kc);
+          }
+        }
+      }
       uint32_t it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int64_t m0, n0, kb0;
@@ -144,17 +163,18 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % T::STAGES, r = it / T::STAGES;
           if (r > 0) tc::mbar_wait(&empty[s], (r - 1) & 1);
-          tc::mbar_expect_tx(&full[s], T::A_BYTES + T::B_BYTES);
+          tc::mbar_expect_tx(&full[s], T::A_BYTES + T::B_STAGE_BYTES);
           const int32_t kc = (int32_t)((kb0 + i) * T::BK);
           uint8_t *a = sA + s * T::A_BYTES;
-          uint8_t *b = sB + s * T::B_BYTES;
+          uint8_t *b = sB + s * T::B_STAGE_BYTES;
           if (!A_MN) {
             tc::tma_load_2d(a, &ta, &full[s], kc, (int32_t)m0);
           } else {
             tc::tma_load_2d(a, &ta, &full[s], (int32_t)m0, kc);
             tc::tma_load_2d(a + 8192, &ta, &full[s], (int32_t)(m0 + 64), kc);
           }
-          if (!B_MN) {
+          if (BRES) {
+          } else if (!B_MN) {
             tc::tma_load_2d(b, &tb, &full[s], kc, (int32_t)n0);
           } else {
 #pragma unroll
@@ -169,6 +189,7 @@ __global__ void __launch_bounds__(192, 1)
     // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = tc::idesc_bf16(T::BM, BN, A_MN, B_MN);
     if (tc::elect_one()) {
+      if (BRES) tc::mbar_wait(bres, 0);
       uint32_t it = 0, li = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
         int64_t m0, n0, kb0;
@@ -183,7 +204,7 @@ __global__ void __launch_bounds__(192, 1)
           tc::mbar_wait(&full[s], (it / T::STAGES) & 1);
           tc::tc_fence_after();
           const uint32_t a = tc::smem_u32(sA + s * T::A_BYTES);
-          const uint32_t b = tc::smem_u32(sB + s * T::B_BYTES);
+          const uint32_t b = tc::smem_u32(BRES ? sB + (kb0 + i) * T::B_BYTES : sB + s * T::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < T::BK / 16; ++kk) {
             uint64_t ad = A_MN ? tc::sdesc(a + kk * 2048, 8192, 1024, tc::kSw128)
@@ -337,9 +358,9 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tc::tmem_dealloc<T::TMEM_COLS>(tmem);
 }
 
-template <int BN, bool A_MN, bool B_MN, bool E16>
+template <int BN, bool A_MN, bool B_MN, bool E16, bool BRES = false>
 static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
-  using T = TG<BN, A_MN, B_MN, E16>;
+  using T = TG<BN, A_MN, B_MN, E16, BRES>;
   CUtensorMap ta, tb, tout, tmask;
   memset(&tout, 0, sizeof(tout));
   memset(&tmask, 0, sizeof(tmask));
@@ -351,7 +372,7 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   else DS_TRY(make_tmap_bf16(&ta, a.A, a.M, a.K, a.lda, 64, 64));
   if (!B_MN) DS_TRY(make_tmap_bf16(&tb, a.B, a.K, a.N, a.ldb, 64, BN));
   else DS_TRY(make_tmap_bf16(&tb, a.B, a.N, a.K, a.ldb, T::B_INNER, 64));
-  auto kern = tgemm_kernel<BN, A_MN, B_MN, E16>;
+  auto kern = tgemm_kernel<BN, A_MN, B_MN, E16, BRES>;
   static bool attr_set = false;
   if (!attr_set) {
     DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
@@ -380,6 +401,8 @@ static dsmpnn_status dispatch_bn(const TgemmArgs &a, cudaStream_t s) {
     DS_CHECK_ARG(!a.colsum_part || a.N <= 256, DSMPNN_ERR_UNSUPPORTED, "tgemm: column sums need N <= 256");
     if (a.N <= 64) return launch_tgemm<64, A_MN, B_MN, true>(a, s);
     if (a.N <= 128) return launch_tgemm<128, A_MN, B_MN, true>(a, s);
+    if (a.b_resident && a.N <= 256 && a.K <= 4 * 64 && a.splits <= 1)
+      return launch_tgemm<256, A_MN, B_MN, true, true>(a, s);
     return launch_tgemm<256, A_MN, B_MN, true>(a, s);
   }
   if (a.N <= 16) return launch_tgemm<16, A_MN, B_MN, false>(a, s);

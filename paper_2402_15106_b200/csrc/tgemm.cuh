@@ -39,6 +39,9 @@ struct TgemmArgs {
   const __nv_bfloat16 *mask16 = nullptr;
   int64_t ldmask = 0;
   float *colsum_part = nullptr;
+  // keep the whole B in SMEM across tiles (bf16 epilogue, N <= 256, K <= 256,
+  // no split-K): only A streams (B5's W2)
+  bool b_resident = false;
 };
 
 // 2-D bf16 TMA descriptor: `inner` contiguous elements, `outer` rows of `ld`

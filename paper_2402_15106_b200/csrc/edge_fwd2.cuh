@@ -302,6 +302,19 @@ __global__ void __launch_bounds__(512, 1)
           }
           tc::mma_commit(&m->d2_full[nh]);
         }
+        // the next tile's MMA1 now if its edge tile and TMEM region are ready
+        // (non-blocking probes), so its a1 epilogue can follow this tile's h
+        // epilogue without waiting for the S products
+        bool next_done = false, next_more = false;
+        {
+          const uint32_t tn = t + 1;
+          const int bn = tn & 1;
+          if (tc::mbar_test(&m->e_full[bn], (tn >> 1) & 1) &&
+              (tn < 2 || tc::mbar_test(&m->region_free[bn], ((tn >> 1) - 1) & 1))) {
+            next_done = true;
+            next_more = mma1(tn);
+          }
+        }
         // S_i = H_i^T V_i per row, kappa half h at column h*128 + g*D
         tc::mbar_wait(&m->v_full, p1);
         for (int h = 0; h < 2; ++h) {
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(512, 1)
         tc::mma_commit(&m->s_full);
         tc::mma_commit(&m->v_empty);
         tc::mma_commit(&m->ah_free);
-        more = mma1(t + 1);
+        more = next_done ? next_more : mma1(t + 1);
       }
     }
     __syncwarp();

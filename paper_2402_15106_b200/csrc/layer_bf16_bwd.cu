@@ -23,6 +23,7 @@
 #include "tc.cuh"
 #include "tgemm.cuh"
 #include "edge_bwd2.cuh"
+#include "dz1w1.cuh"
 
 namespace dsmpnn {
 
@@ -103,6 +104,8 @@ struct BBwd {
   float *cs_ws;            // colsum partials [kColsumChunks x max(D, k)]
   float *dW1f;             // [k x 16]
   float *de16;             // [E x 16]
+  float *w1_part;          // [kNumSMs/2 x KH x 16] fused B5+B6 per-pair dW1
+  float *b1_part;          // [kNumSMs/2 x 2 x KH]  fused B5+B6 per-pair db1
 };
 constexpr int kSplitsW = 64;
 static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst, int64_t E) {
@@ -125,6 +128,8 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.cs_ws = c.take<float>((int64_t)kColsumChunks * std::max(d.k, d.d_in));
   b.dW1f = c.take<float>((int64_t)d.k * 16);
   b.de16 = c.take<float>(E * 16);
+  b.w1_part = c.take<float>((int64_t)(kNumSMs / 2) * KH * 16);
+  b.b1_part = c.take<float>((int64_t)kNumSMs * KH);
   return b;
 }
 
@@ -235,6 +240,34 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
   return DSMPNN_OK;
 }
 
+// B5 + B6 fused (dz1w1.cuh): dW1 += dz1^T e, db1 += colsum(dz1) with
+// dz1 = (dz2 W2) * [a1 > 0] kept on chip
+static dsmpnn_status launch_dz1w1(const Packed &pw, const __nv_bfloat16 *dZ2, const __nv_bfloat16 *e, int64_t nE,
+                                  const float *b1, float *part_w, float *part_b, int d_e, float *gW1, float *gb1,
+                                  cudaStream_t s) {
+  if (nE <= 0 || (!gW1 && !gb1)) return DSMPNN_OK;
+  CUtensorMap tW2, tW1, tDZ, tE;
+  DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, 64));
+  DS_TRY(make_tmap_bf16(&tW1, pw.W1, 16, KH, 16, 16, 128));
+  DS_TRY(make_tmap_bf16(&tDZ, dZ2, KH, nE, KH, 64, 128));
+  DS_TRY(make_tmap_bf16(&tE, e, 16, nE, 16, 16, 128));
+  static bool attr_set = false;
+  if (!attr_set) {
+    DS_CUDA(cudaFuncSetAttribute(dz1w1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZ1C::SMEM));
+    attr_set = true;
+  }
+  const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
+  {
+    ProbeScope probe(DSMPNN_PROBE_BF16_DZ1W1, s);
+    dz1w1_kernel<<<2 * npairs, DZ1C::THREADS, DZ1C::SMEM, s>>>(tW2, tW1, tDZ, tE, nE, b1, part_w, part_b);
+    DS_LAUNCH_CHECK();
+  }
+  const int n = KH * (d_e + 1) * 32;
+  dz1w1_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part_w, part_b, npairs, d_e, gW1, gb1);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
 dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, const __nv_bfloat16 *v,
                        const __nv_bfloat16 *e, const int64_t *row_ptr, const int32_t *col, const int32_t *perm,
                        const int64_t *cptr, int64_t n_dst, int64_t n_loc, int64_t E, int64_t rb, int64_t re,
@@ -297,36 +330,42 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
     DS_TRY(splitk_sum(b.part, real, (int64_t)k * k, k, k, k, gr.W2, k, 1, s));
   }
-  // B5: dz1 = (dz2 W2) * [a1 > 0]  (bf16), column sums -> db1
-  {
-    TgemmArgs a{nE, k, k, b.dZ2 + eb * k, k, false, pw.W2, k, true, nullptr, 0, 1, 0, 0};
-    a.out16 = b.dZ1 + eb * k;
-    a.ld16 = k;
-    a.mask16 = b.A1 + eb * k;
-    a.ldmask = k;
-    a.colsum_part = b.db1_part;
-    a.b_resident = true;
-    DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
-    DS_TRY(tgemm(a, s));
-    DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, gr.b1, 1, b.cs_ws, s));
-  }
-  // B6: dW1 += dz1^T e ;  de = dz1 W1
-  if (gr.W1) {
-    int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
-    TgemmArgs a{k, 16, nE, b.dZ1 + eb * k, k, true, e + eb * 16, 16, true, b.part, 16, splits, (int64_t)k * 16, 0};
-    DS_TRY(tgemm(a, s));
-    int64_t nkb = (nE + 63) / 64;
-    int kbps = (int)std::max<int64_t>(1, ceil_div(nkb, splits));
-    int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
-    DS_TRY(splitk_sum(b.part, real, (int64_t)k * 16, k, 16, 16, b.dW1f, 16, 0, s));
-    add_cols_kernel<<<grid_of((int64_t)k * d.d_e), 256, 0, s>>>(b.dW1f, k, 16, d.d_e, gr.W1, 1);
-    DS_LAUNCH_CHECK();
-  }
-  if (de) {
-    TgemmArgs a{nE, 16, k, b.dZ1 + eb * k, k, false, pw.W1, 16, true, b.de16, 16, 1, 0, 0};
-    DS_TRY(tgemm(a, s));
-    add_cols_kernel<<<grid_of(nE * d.d_e), 256, 0, s>>>(b.de16, nE, 16, d.d_e, de + eb * d.d_e, 0);
-    DS_LAUNCH_CHECK();
+  // B5 + B6 fused (dz1 stays on chip) unless the edge-attribute gradient is
+  // requested, which needs dz1 in HBM
+  if (!de && k == KH && d.d_e <= 16) {
+    DS_TRY(launch_dz1w1(pw, b.dZ2 + eb * k, e + eb * 16, nE, w.b1, b.w1_part, b.b1_part, d.d_e, gr.W1, gr.b1, s));
+  } else {
+    // B5: dz1 = (dz2 W2) * [a1 > 0]  (bf16), column sums -> db1
+    {
+      TgemmArgs a{nE, k, k, b.dZ2 + eb * k, k, false, pw.W2, k, true, nullptr, 0, 1, 0, 0};
+      a.out16 = b.dZ1 + eb * k;
+      a.ld16 = k;
+      a.mask16 = b.A1 + eb * k;
+      a.ldmask = k;
+      a.colsum_part = b.db1_part;
+      a.b_resident = true;
+      DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
+      DS_TRY(tgemm(a, s));
+      DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, gr.b1, 1, b.cs_ws, s));
+    }
+    // B6: dW1 += dz1^T e ;  de = dz1 W1
+    if (gr.W1) {
+      int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
+      TgemmArgs a{k, 16, nE, b.dZ1 + eb * k, k, true, e + eb * 16, 16, true, b.part, 16, splits, (int64_t)k * 16, 0};
+      DS_TRY(tgemm(a, s));
+      int64_t nkb = (nE + 63) / 64;
+      int kbps = (int)std::max<int64_t>(1, ceil_div(nkb, splits));
+      int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
+      DS_TRY(splitk_sum(b.part, real, (int64_t)k * 16, k, 16, 16, b.dW1f, 16, 0, s));
+      add_cols_kernel<<<grid_of((int64_t)k * d.d_e), 256, 0, s>>>(b.dW1f, k, 16, d.d_e, gr.W1, 1);
+      DS_LAUNCH_CHECK();
+    }
+    if (de) {
+      TgemmArgs a{nE, 16, k, b.dZ1 + eb * k, k, false, pw.W1, 16, true, b.de16, 16, 1, 0, 0};
+      DS_TRY(tgemm(a, s));
+      add_cols_kernel<<<grid_of(nE * d.d_e), 256, 0, s>>>(b.de16, nE, 16, d.d_e, de + eb * d.d_e, 0);
+      DS_LAUNCH_CHECK();
+    }
   }
   // B7: dv[j] += sum of u_p over edges with source j (CSC order)
   if (dv) {

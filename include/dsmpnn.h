@@ -350,7 +350,8 @@ typedef enum {
   DSMPNN_PROBE_BF16_EDGE_FWD = 3, /* BF16: fused kappa MLP + S formation (tcgen05) */
   DSMPNN_PROBE_BF16_NODE_GEMM = 4,/* BF16: [S~ | v] . [Theta~ ; W_root^T] GEMM + epilogue (tcgen05) */
   DSMPNN_PROBE_BF16_EDGE_BWD = 5, /* BF16: fused edge backward (tcgen05) */
-  DSMPNN_PROBE_BF16_DZ1W1 = 6     /* BF16: fused dz1 = (dz2 W2)[a1>0] -> dW1, db1 (tcgen05) */
+  DSMPNN_PROBE_BF16_DZ1W1 = 6,    /* BF16: fused dz1 = (dz2 W2)[a1>0] -> dW1, db1 (tcgen05) */
+  DSMPNN_PROBE_BF16_DW2 = 7       /* BF16: dW2 = dz2^T a1 with a1 recomputed (tcgen05) */
 } dsmpnn_probe_kernel;
 dsmpnn_status dsmpnn_probe_begin(int32_t kernel_id, int32_t max_launches);
 dsmpnn_status dsmpnn_probe_end(float *total_ms /*host*/, int64_t *launches /*host*/);

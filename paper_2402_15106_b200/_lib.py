@@ -393,7 +393,7 @@ def gemm_bf16(A, B, C, a_mn_major=False, b_mn_major=False, splits=1, partial=Non
 
 # ---------------------------------------------------------------- probes --
 PROBE_F32_MLP2, PROBE_F32_EDGE_BWD = 1, 2
-PROBE_BF16_EDGE_FWD, PROBE_BF16_NODE_GEMM, PROBE_BF16_EDGE_BWD, PROBE_BF16_DZ1W1 = 3, 4, 5, 6
+PROBE_BF16_EDGE_FWD, PROBE_BF16_NODE_GEMM, PROBE_BF16_EDGE_BWD, PROBE_BF16_DZ1W1, PROBE_BF16_DW2 = 3, 4, 5, 6, 7
 
 
 def probe_begin(kernel_id, max_launches=4096):

@@ -4,7 +4,9 @@
 //   dH^T = dS_i V_seg^T   (M = kappa halves, N = the row's slots, K = c)
 //   U    = H dS_i         (M = 128 slots, N = D, K = kappa)
 // then  dz2 = dH * [h > 0]  -> dZ2 (global, bf16),  u_p = U + dS_i[k] -> U
-// (global, bf16), a1 -> A1 (global, bf16) and per-CTA db2 partial sums.
+// (global, bf16), a1 -> A1 (global, bf16; skipped when A1 is null: the
+// unfused B4/B5 read it, dw2.cuh / dz1w1.cuh recompute a1) and per-CTA db2
+// partial sums.
 //
 // Roles (16 warps):
 //   loader (warps 0,2)  : tile walker, e / v row gathers (register staged),
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(512, 1)
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            if (ps[k] >= 0) reinterpret_cast<uint4 *>(A1g + (int64_t)ps[k] * KH)[lane] = xs[k];
+            if (ps[k] >= 0 && A1g) reinterpret_cast<uint4 *>(A1g + (int64_t)ps[k] * KH)[lane] = xs[k];
         }
       }
       // h = relu(z2 + b2) -> AH (after MMA2 and the a1 copy-out), + [h > 0] bits

@@ -9,7 +9,11 @@
 //   B3  edge kernel per 128-slot tile: recompute a1, h (W1 resident, W2
 //       streamed by TMA), then per row  dH^T = dS_i V^T  and  U = H dS_i
 //       (tcgen05), dz2 = dH * [h > 0] -> global, u_p = U + dS_i[k] -> global,
-//       a1 -> global, per-CTA db2 partial sums.
+//       a1 -> global (only for the unfused B4/B5), per-CTA db2 partial sums.
+//   Without the edge-attribute gradient (the hot path):
+//   B4' dW2 += dz2^T a1, a1 recomputed from e     (dw2.cuh)
+//   B56 dz1 = (dz2 W2) * [a1 > 0] on chip; dW1 += dz1^T e, db1 (dz1w1.cuh)
+//   With it (training with edge refresh, f1):
 //   B4  dW2 += dz2^T a1                           (tgemm, split-K over edges)
 //   B5  dz1 = (dz2 W2) * [a1 > 0]                  (tgemm, bf16 + mask epilogue,
 //                                                   column sums -> db1)
@@ -24,6 +28,7 @@
 #include "tgemm.cuh"
 #include "edge_bwd2.cuh"
 #include "dz1w1.cuh"
+#include "dw2.cuh"
 
 namespace dsmpnn {
 
@@ -106,6 +111,7 @@ struct BBwd {
   float *de16;             // [E x 16]
   float *w1_part;          // [kNumSMs/2 x KH x 16] fused B5+B6 per-pair dW1
   float *b1_part;          // [kNumSMs/2 x 2 x KH]  fused B5+B6 per-pair db1
+  float *w2_part;          // [kNumSMs/2 x KH x KH] B4 (dw2.cuh) per-pair dW2
 };
 constexpr int kSplitsW = 64;
 static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst, int64_t E) {
@@ -130,6 +136,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.de16 = c.take<float>(E * 16);
   b.w1_part = c.take<float>((int64_t)(kNumSMs / 2) * KH * 16);
   b.b1_part = c.take<float>((int64_t)kNumSMs * KH);
+  b.w2_part = c.take<float>((int64_t)(kNumSMs / 2 + kDw2Groups) * KH * KH);
   return b;
 }
 
@@ -223,7 +230,7 @@ template <int D>
 static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &pw, const __nv_bfloat16 *e,
                                      const __nv_bfloat16 *v, const int64_t *row_ptr, const int32_t *col, int64_t n_dst,
                                      int64_t rb, int64_t re, int64_t eb, int64_t ee, const float *b1, const float *b2,
-                                     const BBwd &b, int *grid_out, cudaStream_t s) {
+                                     const BBwd &b, bool write_a1, int *grid_out, cudaStream_t s) {
   using C = EB2<D>;
   CUtensorMap tW2, tDS;
   DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
@@ -234,8 +241,8 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   *grid_out = grid;
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_BWD, s);
-  kern<<<grid, 512, C::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS, b.A1, b.dZ2, b.U,
-                                  b.db2_part);
+  kern<<<grid, 512, C::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS,
+                                  write_a1 ? b.A1 : nullptr, b.dZ2, b.U, b.db2_part);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -264,6 +271,34 @@ static dsmpnn_status launch_dz1w1(const Packed &pw, const __nv_bfloat16 *dZ2, co
   }
   const int n = KH * (d_e + 1) * 32;
   dz1w1_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part_w, part_b, npairs, d_e, gW1, gb1);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+// B4 with a1 recomputed from e (dw2.cuh): gW2 += dz2^T a1
+static dsmpnn_status launch_dw2(const Packed &pw, const __nv_bfloat16 *dZ2, const __nv_bfloat16 *e, int64_t nE,
+                                const float *b1, float *part, float *gW2, cudaStream_t s) {
+  if (nE <= 0) return DSMPNN_OK;
+  CUtensorMap tW1, tDZ, tE;
+  DS_TRY(make_tmap_bf16(&tW1, pw.W1, 16, KH, 16, 16, 128));
+  DS_TRY(make_tmap_bf16(&tDZ, dZ2, KH, nE, KH, 64, 128));
+  DS_TRY(make_tmap_bf16(&tE, e, 16, nE, 16, 16, 128));
+  static bool attr_set = false;
+  if (!attr_set) {
+    DS_CUDA(cudaFuncSetAttribute(dw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DW2C::SMEM));
+    attr_set = true;
+  }
+  const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
+  {
+    ProbeScope probe(DSMPNN_PROBE_BF16_DW2, s);
+    dw2_kernel<<<2 * npairs, DW2C::THREADS, DW2C::SMEM, s>>>(tW1, tDZ, tE, nE, b1, part);
+    DS_LAUNCH_CHECK();
+  }
+  float4 *tmp = reinterpret_cast<float4 *>(part + (int64_t)(kNumSMs / 2) * KH * KH);
+  dw2_reduce1_kernel<<<dim3(KH * KH / 4 / 256, kDw2Groups), 256, 0, s>>>(reinterpret_cast<const float4 *>(part),
+                                                                         npairs, tmp);
+  DS_LAUNCH_CHECK();
+  dw2_reduce2_kernel<<<KH * KH / 4 / 256, 256, 0, s>>>(tmp, reinterpret_cast<float4 *>(gW2));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -315,13 +350,21 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     a.row_scale = b.inv_deg + rb;
     DS_TRY(tgemm(a, s));
   }
+  // Without the edge-attribute gradient (which needs dz1 in HBM) the
+  // kappa_phi weight gradients recompute a1 from e instead of reading A1:
+  // B4 -> dw2.cuh, B5 + B6 -> dz1w1.cuh (dz1 stays on chip)
+  const bool fused = !de && k == KH && d.d_e <= 16;
   // B3: edge kernel
   int grid = 1;
-  if (D == 64) DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, &grid, s));
-  else DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, &grid, s));
+  if (D == 64)
+    DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, !fused, &grid, s));
+  else
+    DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, !fused, &grid, s));
   DS_TRY(colsum(b.db2_part, grid, k, k, gr.b2, 1, s));
   // B4: dW2 += dz2^T a1   (M = k, N = k, K = edges)
-  if (gr.W2) {
+  if (gr.W2 && fused) {
+    DS_TRY(launch_dw2(pw, b.dZ2 + eb * k, e + eb * 16, nE, w.b1, b.w2_part, gr.W2, s));
+  } else if (gr.W2) {
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
     TgemmArgs a{k, k, nE, b.dZ2 + eb * k, k, true, b.A1 + eb * k, k, true, b.part, k, splits, (int64_t)k * k, 0};
     DS_TRY(tgemm(a, s));
@@ -330,9 +373,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
     DS_TRY(splitk_sum(b.part, real, (int64_t)k * k, k, k, k, gr.W2, k, 1, s));
   }
-  // B5 + B6 fused (dz1 stays on chip) unless the edge-attribute gradient is
-  // requested, which needs dz1 in HBM
-  if (!de && k == KH && d.d_e <= 16) {
+  if (fused) {
     DS_TRY(launch_dz1w1(pw, b.dZ2 + eb * k, e + eb * 16, nE, w.b1, b.w1_part, b.b1_part, d.d_e, gr.W1, gr.b1, s));
   } else {
     // B5: dz1 = (dz2 W2) * [a1 > 0]  (bf16), column sums -> db1

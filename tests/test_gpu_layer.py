@@ -246,9 +246,10 @@ def test_fwd_bwd_bf16(L, d, dim, mode, root, act):
 @pytest.mark.parametrize("d,dim,mode,root,act,n", [(64, 2, "diff", 2, 1, 700), (32, 3, "concat", 2, 1, 700),
                                                     (64, 2, "diff", 2, 1, 37)])
 def test_fwd_bwd_bf16_no_de(L, d, dim, mode, root, act, n):
-    """Without the edge-attribute gradient the library fuses B5 and B6 (dz1
-    stays on chip, dW1/db1 accumulated in TMEM): same oracle bar, and the
-    fused and unfused paths agree closely on dW1 and db1."""
+    """Without the edge-attribute gradient the library recomputes a1 from e
+    (B4 in dw2.cuh, the edge kernel skips A1) and fuses B5 and B6 (dz1 stays
+    on chip, dW1 accumulated in TMEM): same oracle bar, and the fused and
+    unfused paths agree closely on dW1, db1 and dW2, exactly elsewhere."""
     p = _problem(n, dim, 0.1 if dim == 2 else 0.2, 40, mode, d, 256, seed=41 + d + n, n_dst=n - 50 if n > 100 else n,
                  isolated=3 if n > 100 else 0)
     _mask_kinks(p, 1, root, act)
@@ -262,7 +263,9 @@ def test_fwd_bwd_bf16_no_de(L, d, dim, mode, root, act, n):
     # values (the oracle's dz1 is unrounded): they differ by ~bf16 resolution
     for nm in ("W1", "b1"):
         assert nerr(got["grads"][nm], unf["grads"][nm]) <= 1e-2, nm
-    for nm in ("W2", "b2", "W3", "b3", "W_root", "b"):
+    # dW2: same bf16 operands, another fp32 summation order
+    assert nerr(got["grads"]["W2"], unf["grads"]["W2"]) <= 1e-4
+    for nm in ("b2", "W3", "b3", "W_root", "b"):
         assert np.array_equal(got["grads"][nm], unf["grads"][nm]), nm
 
 

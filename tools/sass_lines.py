@@ -1,5 +1,5 @@
 """Map ncu per-SASS stall samples to CUDA source lines using nvdisasm -g output.
-usage: sass_lines.py <ncu sass csv> <nvdisasm -g file> <function mangled name> [topN]"""
+usage: sass_lines.py <ncu sass csv> <nvdisasm -g or -gi file (-gi: outermost call site)> <function mangled name> [topN]"""
 import csv, re, sys, collections
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]; data = [r for r in rows[2:] if len(r) == len(hdr)]
@@ -13,8 +13,10 @@ start = next(i for i, l in enumerate(lines) if l.startswith('.text.' + fn + ':')
 cur = None; off2line = {}
 for l in lines[start + 1:]:
     if l.startswith('.text.'): break
-    m = re.search(r'//## File "([^"]+)", line (\d+)', l)
-    if m: cur = (m.group(1).split('/')[-1], int(m.group(2))); continue
+    if l.lstrip().startswith('//## File'):
+        locs = re.findall(r'"([^"]+)", line (\d+)', l)  # innermost first; with nvdisasm -gi the
+        f, n = locs[-1]                                  # last one is the outermost call site
+        cur = (f.split('/')[-1], int(n)); continue
     m = re.search(r'/\*([0-9a-f]{4,})\*/', l)
     if m and cur: off2line[int(m.group(1), 16)] = cur
 agg = collections.defaultdict(float); stall = collections.defaultdict(lambda: collections.defaultdict(float))

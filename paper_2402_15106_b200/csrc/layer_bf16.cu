@@ -94,42 +94,58 @@ template <int D>
 __global__ void s_fill_kernel(const __nv_bfloat16 *__restrict__ v, const int64_t *__restrict__ row_ptr,
                               const int32_t *__restrict__ col, int64_t rb, int64_t re, int64_t kp,
                               __nv_bfloat16 *__restrict__ S) {
-  const int lane = threadIdx.x & 31;
+  // warp per row; lane = (edge sub-slot, 16-byte column chunk): D / 8 lanes
+  // cover one v row, so a warp instruction gathers 32 / (D / 8) rows and
+  // UNR instructions are in flight; sub-slot sums combine by a butterfly
+  // (fixed order)
+  constexpr int LPR = D / 8, EPI = 32 / LPR, UNR = 32 / EPI;  // one batch of 32 edges in flight
+  const int lane = threadIdx.x & 31, cl = lane % LPR, sub = lane / LPR;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = rb + warp; i < re; i += nw) {
-    int64_t p0 = row_ptr[i], p1 = row_ptr[i + 1];
-    int deg = (int)(p1 - p0);
+    const int64_t p0 = row_ptr[i], p1 = row_ptr[i + 1];
+    const int deg = (int)(p1 - p0);
     __nv_bfloat16 *Si = S + i * kp;
-    constexpr int PER = D / 32;  // columns per lane
-    float acc[PER];
+    float acc[8];
 #pragma unroll
-    for (int q = 0; q < PER; ++q) acc[q] = 0.f;
-    int64_t p = p0;
-    for (; p + 8 <= p1; p += 8) {  // eight rows in flight, summed in edge order
-      int32_t j[8];
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    for (int64_t pb = p0; pb < p1; pb += 32) {
+      // 32 column indices per coalesced load, handed out by shuffles, so the
+      // row gathers of a batch are independent of each other
+      const int32_t jl = pb + lane < p1 ? __ldg(col + pb + lane) : 0;
+      const int nb = (int)(p1 - pb < 32 ? p1 - pb : 32);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) j[u] = __ldg(col + p + u);
-      float x[8][PER];
+      for (int q0 = 0; q0 < 32; q0 += EPI * UNR) {
+        uint4 x[UNR];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < UNR; ++u) {
+          const int q = q0 + u * EPI + sub;
+          const int32_t j = __shfl_sync(0xffffffffu, jl, q & 31);
+          x[u] = q < nb ? __ldg(reinterpret_cast<const uint4 *>(v + (int64_t)j * D) + cl) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-        for (int q = 0; q < PER; ++q) x[u][q] = __bfloat162float(v[(int64_t)j[u] * D + lane * PER + q]);
+        for (int u = 0; u < UNR; ++u) {
+          const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&x[u]);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int q = 0; q < PER; ++q) acc[q] += x[u][q];
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(h[q]);
+            acc[2 * q] += f.x;
+            acc[2 * q + 1] += f.y;
+          }
+        }
+      }
     }
-    for (; p < p1; ++p) {
-      const __nv_bfloat16 *vj = v + (int64_t)col[p] * D;
 #pragma unroll
-      for (int q = 0; q < PER; ++q) acc[q] += __bfloat162float(vj[lane * PER + q]);
-    }
-    float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+    for (int off = LPR; off < 32; off <<= 1)
 #pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      Si[(int64_t)KH * D + lane * PER + q] = __float2bfloat16_rn(acc[q] * inv);
-      Si[(int64_t)(KH + 1) * D + lane * PER + q] = v[i * D + lane * PER + q];
+      for (int q = 0; q < 8; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+    const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+    if (sub == 0) {
+      reinterpret_cast<uint4 *>(Si + (int64_t)KH * D)[cl] =
+          make_uint4(tc::pack_bf16(acc[0] * inv, acc[1] * inv), tc::pack_bf16(acc[2] * inv, acc[3] * inv),
+                     tc::pack_bf16(acc[4] * inv, acc[5] * inv), tc::pack_bf16(acc[6] * inv, acc[7] * inv));
+    } else if (sub == 1) {
+      reinterpret_cast<uint4 *>(Si + (int64_t)(KH + 1) * D)[cl] = reinterpret_cast<const uint4 *>(v + i * D)[cl];
     }
     for (int64_t t = (int64_t)(KH + 2) * D + lane; t < kp; t += 32) Si[t] = __float2bfloat16_rn(0.f);
     if (deg == 0)

@@ -33,21 +33,83 @@
 namespace dsmpnn {
 
 // ------------------------------------------------------------- B0 kernels
-__global__ void ghat_bf16_kernel(const float *__restrict__ G, const float *__restrict__ pre,
-                                 const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int D, int act,
-                                 float *__restrict__ gh, __nv_bfloat16 *__restrict__ gh16, float *__restrict__ inv_deg) {
-  int64_t total = (re - rb) * D;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t idx = rb * D + t;
-    float g = G[idx];
-    if (act == DSMPNN_ACT_RELU && !(pre[idx] > 0.f)) g = 0.f;
-    gh[idx] = g;
-    gh16[idx] = __float2bfloat16_rn(g);
-    if (t % D == 0) {
-      int64_t i = rb + t / D;
-      int64_t deg = row_ptr[i + 1] - row_ptr[i];
-      inv_deg[i] = deg > 0 ? 1.0f / (float)deg : 0.f;
+// B0 in one pass over 32-row blocks: ghat = G * sigma'(pre) (fp32 + bf16
+// copy), 1/deg, the block's column sums of ghat (-> db, summed over blocks in
+// block order by colsum), and the root term of dv: dv += ghat W_root (dense)
+// or dv += ghat (identity).  W_root is [D x D] with dv[m][n] += sum_c ghat[m][c] W_root[c][n].
+template <int D>
+__global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ G, const float *__restrict__ pre,
+                                                      const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re,
+                                                      int act, int root, const float *__restrict__ Wr,
+                                                      float *__restrict__ gh, __nv_bfloat16 *__restrict__ gh16,
+                                                      float *__restrict__ inv_deg, float *__restrict__ cs_part,
+                                                      float *__restrict__ dv) {
+  __shared__ float sg[32][D + 1];
+  __shared__ __align__(16) float sw[D][D];
+  const int t = threadIdx.x;
+  const int64_t r0 = rb + (int64_t)blockIdx.x * 32;
+  const bool dense = root == DSMPNN_ROOT_DENSE && dv != nullptr;
+  if (dense)
+    for (int i = t; i < D * D / 4; i += 256) reinterpret_cast<float4 *>(&sw[0][0])[i] = reinterpret_cast<const float4 *>(Wr)[i];
+  for (int i = t; i < 32 * D; i += 256) {
+    const int r = i / D, c = i % D;
+    const int64_t row = r0 + r;
+    float g = 0.f;
+    if (row < re) {
+      const int64_t idx = row * D + c;
+      g = G[idx];
+      if (act == DSMPNN_ACT_RELU && !(pre[idx] > 0.f)) g = 0.f;
+      gh[idx] = g;
+      gh16[idx] = __float2bfloat16_rn(g);
     }
+    sg[r][c] = g;
+  }
+  if (t < 32 && r0 + t < re) {
+    const int64_t i = r0 + t;
+    const int64_t deg = row_ptr[i + 1] - row_ptr[i];
+    inv_deg[i] = deg > 0 ? 1.0f / (float)deg : 0.f;
+  }
+  __syncthreads();
+  if (t < D) {
+    float cs = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) cs += sg[r][t];
+    cs_part[(int64_t)blockIdx.x * D + t] = cs;
+  }
+  if (dv == nullptr || root == DSMPNN_ROOT_NONE) return;
+  // thread = (row r, group of D / 8 consecutive columns): 256 threads = 32 rows x 8 groups
+  constexpr int NC = D / 8;
+  const int r = t >> 3, n0 = (t & 7) * NC;
+  if (r0 + r >= re) return;
+  float acc[NC];
+  if (dense) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[j] = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < D; ++c) {
+      const float g = sg[r][c];
+#pragma unroll
+      for (int j = 0; j < NC; j += 4) {
+        const float4 w4 = *reinterpret_cast<const float4 *>(&sw[c][n0 + j]);
+        acc[j] += g * w4.x;
+        acc[j + 1] += g * w4.y;
+        acc[j + 2] += g * w4.z;
+        acc[j + 3] += g * w4.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[j] = sg[r][n0 + j];
+  }
+  float *o = dv + (r0 + r) * D + n0;
+#pragma unroll
+  for (int j = 0; j < NC; j += 4) {
+    float4 x = *reinterpret_cast<float4 *>(o + j);
+    x.x += acc[j];
+    x.y += acc[j + 1];
+    x.z += acc[j + 2];
+    x.w += acc[j + 3];
+    *reinterpret_cast<float4 *>(o + j) = x;
   }
 }
 
@@ -112,6 +174,7 @@ struct BBwd {
   float *w1_part;          // [kNumSMs/2 x KH x 16] fused B5+B6 per-pair dW1
   float *b1_part;          // [kNumSMs/2 x 2 x KH]  fused B5+B6 per-pair db1
   float *w2_part;          // [kNumSMs/2 x KH x KH] B4 (dw2.cuh) per-pair dW2
+  float *b0_part;          // [ceil(n_dst/32) x D] B0 per-block column sums of ghat
 };
 constexpr int kSplitsW = 64;
 static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst, int64_t E) {
@@ -137,6 +200,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.w1_part = c.take<float>((int64_t)(kNumSMs / 2) * KH * 16);
   b.b1_part = c.take<float>((int64_t)kNumSMs * KH);
   b.w2_part = c.take<float>((int64_t)(kNumSMs / 2 + kDw2Groups) * KH * KH);
+  b.b0_part = c.take<float>(ceil_div(std::max<int64_t>(n_dst, 1), 32) * D);
   return b;
 }
 
@@ -217,13 +281,6 @@ __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, con
       o[1] = a1;
     }
   }
-}
-
-__global__ void add_rows_f32_kernel(const float *__restrict__ src, int64_t rb, int64_t re, int w,
-                                    float *__restrict__ dst) {
-  int64_t total = (re - rb) * w;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
-    dst[rb * w + t] += src[rb * w + t];
 }
 
 template <int D>
@@ -319,15 +376,16 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   if (nR <= 0) return DSMPNN_OK;
 
   // B0
-  ghat_bf16_kernel<<<grid_of(nR * D), 256, 0, s>>>(G, f.pre, row_ptr, rb, re, D, d.act, b.gh, b.gh16, b.inv_deg);
-  DS_LAUNCH_CHECK();
-  DS_TRY(colsum_ws(b.gh + rb * D, nR, D, D, gr.b, 1, b.cs_ws, s));
-  if (d.root == DSMPNN_ROOT_DENSE && dv) {
-    SgemmArgs g{nR, D, D, b.gh + rb * D, D, 1, w.W_root, D, 1, dv + rb * D, D, nullptr, 0, 1, 1.f};
-    DS_TRY(sgemm(g, 1, nullptr, s));
-  } else if (d.root == DSMPNN_ROOT_IDENTITY && dv) {
-    add_rows_f32_kernel<<<grid_of(nR * D), 256, 0, s>>>(b.gh, rb, re, D, dv);
+  {
+    const int nblk = (int)ceil_div(nR, 32);
+    if (D == 64)
+      b0_bf16_kernel<64><<<nblk, 256, 0, s>>>(G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
+                                              b.inv_deg, b.b0_part, dv);
+    else
+      b0_bf16_kernel<32><<<nblk, 256, 0, s>>>(G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
+                                              b.inv_deg, b.b0_part, dv);
     DS_LAUNCH_CHECK();
+    if (gr.b) DS_TRY(colsum(b.b0_part, nblk, D, D, gr.b, 1, s));
   }
   // B1: dTheta~_aug [kp x D] = S~_aug^T ghat  (K = rows)
   if (gr.W3 || gr.b3 || gr.W_root) {

@@ -279,8 +279,10 @@ def main():
     probe_id = L.PROBE_BF16_EDGE_BWD if sc.dtype == L.BF16 else L.PROBE_F32_MLP2
     # algorithmic HBM bytes of one step's edge-backward launches (DESIGN.md
     # "Rooflines"): per edge e (32 B, bf16 padded to 16) + v_j (2d) + col (4)
-    # + a1, dz2 (2k each) + u_p (2d); per destination row dS_i (2(k+1)d)
-    bwd_bytes_step = sum(sd.n_edges * (32 + 4 + 4 * sc.d + 4 * sc.k) + sd.n_own * 2 * (sc.k + 1) * sc.d
+    # + dz2 (2k) + u_p (2d); per destination row dS_i (2(k+1)d).  The step
+    # requests no edge-attribute gradient, so the kernel writes no A1 (the
+    # dW2 / dW1 kernels recompute a1 from e; layer_bf16_bwd.cu)
+    bwd_bytes_step = sum(sd.n_edges * (32 + 4 + 4 * sc.d + 2 * sc.k) + sd.n_own * 2 * (sc.k + 1) * sc.d
                          for sd in hp.subs) * sc.L
 
     # ---- device-resident timed region

@@ -179,14 +179,33 @@ __global__ void node_epi_bf16_kernel(const float *__restrict__ part, int splits,
 struct BFwd {
   __nv_bfloat16 *S;  // [n_dst x kp]
   float *pre;        // [n_dst x D]
-  float *part;       // [kSplitsFwd x n_dst x D]
+  float *part;       // [kMaxSplitsFwd x n_dst x D]
 };
-constexpr int kSplitsFwd = 6;
+constexpr int kMaxSplitsFwd = 16;
+// split-K count of the node GEMM: the persistent tgemm runs ceil(T / 148)
+// rounds of T = m-tiles x splits tiles, so pick the split count in [4, 16]
+// whose last round is fullest (fewest idle SMs), ties to fewer splits
+static int node_gemm_splits(int64_t nR, int64_t kp, int *real_out) {
+  const int64_t mt = ceil_div(nR, 128), nkb = ceil_div(kp, 64);
+  int best = 4, best_real = 4;
+  double best_eff = -1.0;
+  for (int sp = 4; sp <= kMaxSplitsFwd; ++sp) {
+    const int64_t kbps = ceil_div(nkb, sp), real = ceil_div(nkb, kbps), T = mt * real;
+    const double eff = (double)T / (double)(kNumSMs * ceil_div(T, kNumSMs));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+      best_real = (int)real;
+    }
+  }
+  *real_out = best_real;
+  return best;
+}
 static BFwd carve_bf16_fwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst) {
   BFwd f;
   f.S = c.take<__nv_bfloat16>(n_dst * kpad_of(d));
   f.pre = c.take<float>(n_dst * d.d_out);
-  f.part = c.take<float>((int64_t)kSplitsFwd * n_dst * d.d_out);
+  f.part = c.take<float>((int64_t)kMaxSplitsFwd * n_dst * d.d_out);
   return f;
 }
 
@@ -236,14 +255,13 @@ dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     else DS_TRY(launch_edge_fwd<32>(e, v, row_ptr, col, rb, re, eb, ee, pw, w.b1, w.b2, f.S, kp, s));
   }
   // 3. node GEMM [S~_aug] . [Theta~_aug]  (split-K partials)
+  int real = 1;
+  const int splits = node_gemm_splits(nR, kp, &real);
   {
     ProbeScope probe(DSMPNN_PROBE_BF16_NODE_GEMM, s);
-    TgemmArgs a{nR, D, kp, f.S + rb * kp, kp, false, pw.ThT, kp, false, f.part, D, kSplitsFwd, nR * D, 0};
+    TgemmArgs a{nR, D, kp, f.S + rb * kp, kp, false, pw.ThT, kp, false, f.part, D, splits, nR * D, 0};
     DS_TRY(tgemm(a, s));
   }
-  int64_t nkb = (kp + 63) / 64;
-  int kbps = (int)ceil_div(nkb, kSplitsFwd);
-  int real = (int)ceil_div(nkb, kbps);
   node_epi_bf16_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * D, 256), 148 * 8)), 256, 0, s>>>(
       f.part, real, nR * D, rb, re, D, w.b, v, d.root, d.act, f.pre, out, out_lowp);
   DS_LAUNCH_CHECK();

@@ -226,14 +226,16 @@ static BFwdView view_fwd(const dsmpnn_layer_desc &d, const void *ws, int64_t n_d
 }
 
 // dv[j] += sum over the CSC list of j of u_p (p in [eb, ee)).  One warp per
-// node: lane = (channel group of 8, sub-list); sub-lists interleave the list
-// and are combined by a butterfly, so the summation order is fixed.
+// node: the list's edge ids are read 32 at a time (one coalesced load) and
+// handed out by shuffles; lane = (edge sub-slot, 16-byte channel chunk), so
+// every U row gather of a batch is in flight at once.  Sub-slot sums combine
+// by a butterfly: the summation order is fixed.
 template <int D>
 __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, const int32_t *__restrict__ perm,
                                         const int64_t *__restrict__ cptr, int64_t n_loc, int64_t eb, int64_t ee,
                                         float *__restrict__ dv) {
-  constexpr int CG = D / 8, SL = 32 / CG, UNR = 4;
-  const int lane = threadIdx.x & 31, cg = lane % CG, sub = lane / CG;
+  constexpr int LPR = D / 8, EPI = 32 / LPR, UNR = 32 / EPI;
+  const int lane = threadIdx.x & 31, cl = lane % LPR, sub = lane / LPR;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_loc; j += nw) {
     const int64_t q0 = cptr[j], q1 = cptr[j + 1];
@@ -241,19 +243,17 @@ __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, con
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
     bool any = false;
-    for (int64_t q = q0 + sub; q < q1; q += SL * UNR) {
-      int64_t p[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int64_t qq = q + u * SL;
-        p[u] = qq < q1 ? (int64_t)__ldg(perm + qq) : -1;
-      }
+    for (int64_t qb = q0; qb < q1; qb += 32) {
+      const int32_t pl = qb + lane < q1 ? __ldg(perm + qb + lane) : -1;
+      const int nb = (int)(q1 - qb < 32 ? q1 - qb : 32);
       uint4 x[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const bool ok = p[u] >= eb && p[u] < ee;
+        const int q = u * EPI + sub;
+        const int64_t pe = __shfl_sync(0xffffffffu, pl, q);
+        const bool ok = q < nb && pe >= eb && pe < ee;
         any |= ok;
-        x[u] = ok ? __ldg(reinterpret_cast<const uint4 *>(U + p[u] * D) + cg) : make_uint4(0, 0, 0, 0);
+        x[u] = ok ? __ldg(reinterpret_cast<const uint4 *>(U + pe * D) + cl) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -267,13 +267,13 @@ __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, con
       }
     }
 #pragma unroll
-    for (int off = CG; off < 32; off <<= 1) {
+    for (int off = LPR; off < 32; off <<= 1) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
     }
     any = __any_sync(0xffffffffu, any);
     if (any && sub == 0) {
-      float4 *o = reinterpret_cast<float4 *>(dv + j * D + cg * 8);
+      float4 *o = reinterpret_cast<float4 *>(dv + j * D + cl * 8);
       float4 a0 = o[0], a1 = o[1];
       a0.x += acc[0]; a0.y += acc[1]; a0.z += acc[2]; a0.w += acc[3];
       a1.x += acc[4]; a1.y += acc[5]; a1.z += acc[6]; a1.w += acc[7];

@@ -11,7 +11,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdsmpnn.so")
+# DSMPNN_LIB: an alternative build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("DSMPNN_LIB") or os.path.join(_HERE, "libdsmpnn.so")
 
 F32, BF16 = 0, 1
 ROOT_NONE, ROOT_IDENTITY, ROOT_DENSE = 0, 1, 2

@@ -17,6 +17,8 @@ Under torchrun (N > 1) every process holds nparts/N sub-domains; halos between
 processes go over NCCL (torch.distributed), timing is the max over ranks.
 """
 import argparse
+import dataclasses
+import gc
 import json
 import os
 import statistics
@@ -43,6 +45,7 @@ def parse():
     ap.add_argument("--dtype", default=os.environ.get("DSMPNN_BENCH_DTYPE", "bf16"), choices=["bf16", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--streams", type=int, default=2, help="CUDA streams the local sub-domains are spread over")
     return ap.parse_args()
 
 
@@ -72,16 +75,47 @@ def step_config(cfg_name, world, dtype):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: an NVML
+    poll thread (NVML initialised before the region, so no process start-up
+    lands inside it), else an `nvidia-smi -lms 100` process."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        while not self.done.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, {n for n, bit in zip(self.NAMES, self.bits) if rs & bit}))
+            except Exception:
+                pass
+            self.done.wait(0.02)
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.samples, self.done = [], threading.Event()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -90,6 +124,14 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
+        if self.nv is not None:
+            self.done.set()
+            self.t.join()
+            if not self.samples:
+                return None
+            reasons = set().union(*[r for _, r in self.samples])
+            return {"sm_mhz": statistics.median([sm for sm, _ in self.samples]), "sm_max_mhz": self.max_sm,
+                    "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml"}
         if self.p is None:
             return None
         time.sleep(0.25)
@@ -97,12 +139,11 @@ class ClockSampler:
         out, _ = self.p.communicate()
         rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[0]))
                 mx.append(float(r[1]))
-                for nm, flag in zip(names, r[3:7]):
+                for nm, flag in zip(self.NAMES, r[3:7]):
                     if flag.strip() == "Active":
                         reasons.add(nm)
             except (ValueError, IndexError):
@@ -110,7 +151,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 def count_our_launches(fn):
@@ -255,6 +296,7 @@ def main():
     from paper_2402_15106_b200 import synth
     from paper_2402_15106_b200.api import HotPath
     cfg, sc, coords, attr = step_config(args.config, world, args.dtype)
+    sc = dataclasses.replace(sc, streams=args.streams)
     d_e = (sc.dim + sc.n_attr) * (1 if sc.edge_mode == L.EDGE_DIFF else 2)
     W = synth.weights(d_e, sc.d, sc.d, sc.k)
     v0 = synth.node_features(sc.s, sc.d)
@@ -271,9 +313,14 @@ def main():
 
     for _ in range(args.warmup):
         step(devin)
+    # settle: at least 8 untimed steps in all (W + extra) before timing; with
+    # fewer, the first timed steps of a fresh process were occasionally 10-30 %
+    # slow (two-stream schedule not yet steady); reported as warmup_extra
+    warmup_extra = max(0, 8 - args.warmup)
+    for _ in range(warmup_extra):
+        step(devin)
     torch.cuda.synchronize()
     E_local = hp.n_edges
-    launches, lib_other = count_our_launches(lambda: step(devin))
     # dominant kernel of the step: the fused edge backward (BF16), the kappa-MLP
     # second-layer GEMM (F32)
     probe_id = L.PROBE_BF16_EDGE_BWD if sc.dtype == L.BF16 else L.PROBE_F32_MLP2
@@ -286,6 +333,11 @@ def main():
                          for sd in hp.subs) * sc.L
 
     # ---- device-resident timed region
+    # Python's cyclic GC stays off inside the timed regions (as timeit does):
+    # a full collection is a host stall of tens of ms that starves the GPU of
+    # launches; it runs right before each region instead
+    gc.collect()
+    gc.disable()
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -326,6 +378,25 @@ def main():
     x1.record(st)
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1) / args.steps
+
+    gc.enable()
+    # roofline probe of the dominant kernel with the sub-domains on one stream:
+    # with 2 streams its launches overlap other kernels, so their event
+    # durations measure the schedule, not the kernel (both are reported)
+    probe_ms_step, probe_n_step = probe_ms, probe_n
+    if sc.streams > 1:
+        hp.cfg = dataclasses.replace(hp.cfg, streams=1)
+        step(devin)
+        torch.cuda.synchronize()
+        L.probe_begin(probe_id, 64 * args.steps * sc.L * len(hp.subs) + 64)
+        for _ in range(args.steps):
+            step(devin)
+        torch.cuda.synchronize()
+        probe_ms, probe_n = L.probe_end()
+        hp.cfg = dataclasses.replace(hp.cfg, streams=sc.streams)
+    # kernels of one step (CUPTI trace); after the timed regions so that no
+    # profiler state is live while they run
+    launches, lib_other = count_our_launches(lambda: step(devin))
 
     # ---- graph build alone (sample + partition + radius graph + attributes + CSC), for reference
     torch.cuda.synchronize()
@@ -381,7 +452,8 @@ def main():
                        "edges_total": int(E_tot), "edge_attr_dim": d_e,
                        "form": "GNO: relu(W v_i + mean kappa(e) v_j + b)",
                        "l2": "256 MB buffer zeroed at the start of every step, inside the timed region",
-                       "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd"},
+                       "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd",
+                       "streams": sc.streams},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "kernel": {1: "F32 mlp2 sgemm", 5: "bf16 fused edge bwd (edge_bwd2)"}.get(probe_id,
@@ -391,11 +463,16 @@ def main():
                          "tensor_frac": (tensor_tflops / float(peaks["bf16_tflops_sustained"])
                                          if tensor_tflops else None),
                          "per_launch_ms": per_launch_ms, "launches": probe_n,
-                         "share_of_step": probe_ms / (ms * args.steps), "peak_source": src},
+                         "share_of_step": probe_ms / (ms * args.steps), "peak_source": src,
+                         "probe": ("separate pass of the same steps with the sub-domains on one stream "
+                                   "(the kernel alone); in the timed 2-stream region its launches overlap "
+                                   "other kernels" if sc.streams > 1 else "timed region"),
+                         "per_launch_ms_in_timed_region": probe_ms_step / max(1, probe_n_step)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "graph_ms": graph_ms,
             "gpu_launches": launches * args.steps,
+            "warmup_extra": warmup_extra,
             "gpu_launches_cub": lib_other * args.steps,
             "clocks": clk,
         }

@@ -337,6 +337,11 @@ dsmpnn_status dsmpnn_gemm_bf16(int64_t M, int64_t N, int64_t K, const void *A, i
                                const void *B, int64_t ldb, int32_t b_mn_major, float *C, int64_t ldc, int32_t splits,
                                float *partial, int32_t accumulate, void *stream);
 
+/* Gradient sum of sub-domains processed on separate CUDA streams (Alg. 1
+ * :418 "sum gradients"): dst[i] += src[i] for i < n (fp32, device pointers,
+ * element-wise, deterministic).  The caller orders the streams. */
+dsmpnn_status dsmpnn_accumulate_f32(float *dst, const float *src, int64_t n, void *stream);
+
 /* ------------------------------------------------------------ probes --- */
 /* Live kernel timing for the benchmark's roofline figure: while a probe is
  * armed, the library records a CUDA event pair on the launching stream around

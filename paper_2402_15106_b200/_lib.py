@@ -89,6 +89,7 @@ _f = {
                       P, P, P, C.POINTER(Grads), P, P, SZ, P),
     "halo_gather": _sig("halo_gather", P, P, I64, I32, I32, P, P),
     "halo_scatter_add": _sig("halo_scatter_add", P, P, I64, I32, P, P),
+    "accumulate_f32": _sig("accumulate_f32", P, P, I64, P),
     "halo_exchange_loopback": _sig("halo_exchange_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
                                    C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, P),
     "halo_reverse_add_loopback": _sig("halo_reverse_add_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
@@ -280,6 +281,11 @@ def layer_bwd(desc, W, packed, v, e, row_ptr, col_idx, csc_perm, csc_ptr, n_dst,
 def halo_gather(values, rows, out, dtype, stream=None):
     width = values.shape[1]
     _call("halo_gather", _p(values), _p(rows), rows.numel(), width, dtype, _p(out), _stream(stream))
+
+
+def accumulate_f32(dst, src, stream=None):
+    assert dst.numel() == src.numel() and dst.dtype == src.dtype == torch.float32
+    _call("accumulate_f32", _p(dst), _p(src), dst.numel(), _stream(stream))
 
 
 def halo_scatter_add(inp, rows, values, stream=None):

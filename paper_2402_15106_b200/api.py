@@ -47,6 +47,7 @@ class StepConfig:
     seed_capping: int = 0
     grad_mode: int = DETACH
     overlap_halo: int = -1  # 1: deep rows of a layer run while the previous halo refresh is in flight; -1: when world > 1
+    streams: int = 2  # CUDA streams the local sub-domains' layer work is spread over (1: one stream)
 
 
 def parts_of_process(nparts, world, rank):
@@ -102,6 +103,19 @@ class HotPath:
             t = torch.empty(max(1, int(nbytes)), dtype=torch.uint8, device=self.dev)
             self.ws[key] = t
         return t
+
+    def _side_streams(self):
+        """Streams for concurrent sub-domains (StepConfig.streams > 1 and more
+        than one local sub-domain); the sub-domains of a layer are independent
+        once their inputs (including halo rows) are in place."""
+        S = min(self.cfg.streams, len(self.subs))
+        if S <= 1:
+            return []
+        if getattr(self, "_side", None) is None or len(self._side) != S:
+            # stream 0 at high priority, the others fill its gaps and kernel tails
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._side = [torch.cuda.Stream(self.dev, priority=hi if k == 0 else lo) for k in range(S)]
+        return self._side
 
     def _comm_stream(self):
         if getattr(self, "_comm", None) is None:
@@ -160,8 +174,24 @@ class HotPath:
                               .view(sd.n_own, c.d))
                 nxt.append(torch.empty((sd.n_loc, c.d), dtype=vdt, device=self.dev))
             if not overlap:
-                for q, sd in enumerate(self.subs):
-                    run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_own)
+                side = self._side_streams()
+                if side:  # sub-domain q on stream q % S, joined before the halo refresh
+                    for q, sd in enumerate(self.subs):  # workspaces exist before the fork
+                        self._ws(("fwd", layer, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
+                    fork = torch.cuda.Event()
+                    fork.record(main)
+                    for st in side:
+                        st.wait_event(fork)
+                    for q, sd in enumerate(self.subs):
+                        with torch.cuda.stream(side[q % len(side)]):
+                            run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_own)
+                    for st in side:
+                        done = torch.cuda.Event()
+                        done.record(st)
+                        main.wait_event(done)
+                else:
+                    for q, sd in enumerate(self.subs):
+                        run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_own)
                 self.halo(nxt, L.BF16 if lowp else L.F32)
             else:
                 # deep rows have no halo neighbour (R23): they run while the
@@ -204,24 +234,69 @@ class HotPath:
             g = torch.empty((sd.n_own, c.d), dtype=torch.float32, device=self.dev)
             L.gather_rows(G, sd.local_rows[: sd.n_own], g)
             gouts.append(g)
-        for layer in reversed(range(c.L)):
-            new_g = []
+        side = self._side_streams() if c.grad_mode == DETACH else []
+        if side:
+            # DETACH: a sub-domain's backward needs nothing from the others, so
+            # sub-domain q runs all its layers on stream q % S with its own
+            # gradient accumulator; the accumulators are summed in stream order
+            main = torch.cuda.current_stream(self.dev)
+            accs = [self.grads] + [self._ws_grads(k) for k in range(1, len(side))]
             for q, sd in enumerate(self.subs):
-                ws = self.ws[("fwd", layer, q)]
-                bws = self._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
-                gv = torch.zeros((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
-                e = sd.e16 if lowp else sd.e32
-                # the input gradient of the first layer is not needed (no scatter / root term)
-                L.layer_bwd(desc, self.W, self.packed, acts[layer][q], e, sd.row_ptr, sd.col_idx, sd.csc_perm,
-                            sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, gouts[q], gv if layer > 0 else None, None,
-                            self.grads, ws, bws, row_ptr_host=sd.row_ptr_host)
-                new_g.append(gv)
-            if c.grad_mode == REVERSE_ADD:
-                self.halo_reverse(new_g)
-            gouts = [gv[: sd.n_own] for gv, sd in zip(new_g, self.subs)]
+                self._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
+            gvs = {(layer, q): torch.zeros((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
+                   for layer in range(1, c.L) for q, sd in enumerate(self.subs)}
+            fork = torch.cuda.Event()
+            fork.record(main)
+            for st in side:
+                st.wait_event(fork)
+            for q, sd in enumerate(self.subs):
+                k = q % len(side)
+                g = gouts[q]
+                with torch.cuda.stream(side[k]):
+                    for layer in reversed(range(c.L)):
+                        gv = gvs.get((layer, q))
+                        e = sd.e16 if lowp else sd.e32
+                        L.layer_bwd(desc, self.W, self.packed, acts[layer][q], e, sd.row_ptr, sd.col_idx,
+                                    sd.csc_perm, sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, g, gv, None, accs[k],
+                                    self.ws[("fwd", layer, q)], self.ws[("bwd", q)], row_ptr_host=sd.row_ptr_host)
+                        if gv is not None:
+                            g = gv[: sd.n_own]
+            for st in side:
+                done = torch.cuda.Event()
+                done.record(st)
+                main.wait_event(done)
+            for k in range(1, len(side)):
+                for n in GNAMES:
+                    L.accumulate_f32(self.grads[n], accs[k][n])
+        else:
+            for layer in reversed(range(c.L)):
+                new_g = []
+                for q, sd in enumerate(self.subs):
+                    ws = self.ws[("fwd", layer, q)]
+                    bws = self._ws(("bwd", q), L.layer_bwd_workspace_size(desc, sd.n_own, sd.n_loc, sd.n_edges))
+                    gv = torch.zeros((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
+                    e = sd.e16 if lowp else sd.e32
+                    # the input gradient of the first layer is not needed (no scatter / root term)
+                    L.layer_bwd(desc, self.W, self.packed, acts[layer][q], e, sd.row_ptr, sd.col_idx, sd.csc_perm,
+                                sd.csc_ptr, sd.n_own, sd.n_loc, 0, sd.n_own, gouts[q], gv if layer > 0 else None,
+                                None, self.grads, ws, bws, row_ptr_host=sd.row_ptr_host)
+                    new_g.append(gv)
+                if c.grad_mode == REVERSE_ADD:
+                    self.halo_reverse(new_g)
+                gouts = [gv[: sd.n_own] for gv, sd in zip(new_g, self.subs)]
         if self.world > 1:
             self._allreduce_grads()
         return self.grads
+
+    def _ws_grads(self, k):
+        """Zeroed gradient accumulator of side stream k (k >= 1)."""
+        if not hasattr(self, "_acc"):
+            self._acc = {}
+        if k not in self._acc:
+            self._acc[k] = {n: torch.zeros_like(t) for n, t in self.W.items()}
+        for t in self._acc[k].values():
+            t.zero_()
+        return self._acc[k]
 
     def _allreduce_grads(self):
         """Gradient sum over processes (Alg. 1), one NCCL all-reduce."""

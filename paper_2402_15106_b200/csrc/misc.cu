@@ -285,6 +285,19 @@ dsmpnn_status dsmpnn_halo_gather(const void *values, const int32_t *rows, int64_
   return DSMPNN_OK;
 }
 
+__global__ void accumulate_f32_kernel(float *__restrict__ dst, const float *__restrict__ src, int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] += src[t];
+}
+
+dsmpnn_status dsmpnn_accumulate_f32(float *dst, const float *src, int64_t n, void *stream) {
+  DS_CHECK_ARG(n >= 0, DSMPNN_ERR_INVALID_ARG, "accumulate_f32: n < 0");
+  if (n == 0) return DSMPNN_OK;
+  accumulate_f32_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(dst, src, n);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
 dsmpnn_status dsmpnn_halo_scatter_add(const float *in, const int32_t *rows, int64_t n_rows, int32_t width,
                                       float *values, void *stream) {
   DS_CHECK_ARG(width > 0 && n_rows >= 0, DSMPNN_ERR_INVALID_ARG, "halo_scatter_add: bad size");

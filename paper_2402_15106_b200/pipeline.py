@@ -89,20 +89,41 @@ def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bit
     return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
 
 
-def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
+def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, streams=None):
     """build_graph for several sub-domains with one host synchronisation: all
     radius graphs are enqueued (capacity n_own * n_e), then the edge counts and
     the host copies of row_ptr are read back together, then edge attributes
-    and CSC views are enqueued."""
+    and CSC views are enqueued.  streams: optional CUDA streams; sub-domain q's
+    kernels go to streams[q % len(streams)] (arrays are allocated on the
+    current stream, which waits for every stream before returning)."""
     if not subs:
         return subs
     dev = subs[0].coords.device
+    main = torch.cuda.current_stream(dev)
+
+    def fan_out(work):
+        if not streams:
+            for q, sd in enumerate(subs):
+                work(q, sd)
+            return
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for st in streams:
+            st.wait_event(fork)
+        for q, sd in enumerate(subs):
+            with torch.cuda.stream(streams[q % len(streams)]):
+                work(q, sd)
+        for st in streams:
+            done = torch.cuda.Event()
+            done.record(st)
+            main.wait_event(done)
+
     cols = []
     for sd in subs:
         sd.row_ptr = torch.empty(sd.n_own + 1, dtype=torch.int64, device=dev)
-        col = torch.empty(max(1, sd.n_own * n_e), dtype=torch.int32, device=dev)
-        L.radius_graph(sd.coords, sd.gid, sd.n_own, r, n_e, seed, sd.row_ptr, col, want_count=False)
-        cols.append(col)
+        cols.append(torch.empty(max(1, sd.n_own * n_e), dtype=torch.int32, device=dev))
+    fan_out(lambda q, sd: L.radius_graph(sd.coords, sd.gid, sd.n_own, r, n_e, seed, sd.row_ptr, cols[q],
+                                         want_count=False))
     host = torch.cat([sd.row_ptr for sd in subs]).cpu()  # the one synchronisation
     off = 0
     for sd, col in zip(subs, cols):
@@ -111,19 +132,23 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):
         E = int(sd.row_ptr_host[-1])
         sd.col_idx = col[:E]
         sd.n_edges = E
-        _edge_arrays(sd, edge_mode, want_f32, want_bf16)
+        _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16)
+    fan_out(lambda q, sd: _edge_arrays(sd, edge_mode))
     return subs
 
 
-def _edge_arrays(sd, edge_mode, want_f32, want_bf16):
+def _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16):
     dev = sd.coords.device
     E = sd.n_edges
     de = (sd.coords.shape[1] + sd.attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
     sd.e32 = torch.empty((max(E, 1), de), dtype=torch.float32, device=dev) if want_f32 else None
     sd.e16 = torch.empty((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None  # all 16 written
-    L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, sd.n_own, sd.e32, sd.e16)
     sd.csc_perm = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
     sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)
+
+
+def _edge_arrays(sd, edge_mode):
+    L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, sd.n_own, sd.e32, sd.e16)
     L.csc(sd.col_idx, sd.n_loc, sd.csc_perm, sd.csc_ptr)
 
 

@@ -100,3 +100,34 @@ def test_overlapped_halo_refresh_is_bitwise_identical(lib, dtype):
         res.append({n: g[n].cpu().numpy().copy() for n in NAMES})
     for n in NAMES:
         assert np.array_equal(res[0][n], res[1][n]), n
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_two_stream_schedule(lib, dtype):
+    """Sub-domains spread over two CUDA streams (StepConfig.streams, DESIGN
+    §7.1): the forward is bitwise that of one stream (the same kernels on the
+    same inputs), the DETACH gradients differ only by the fp32 order of the
+    per-stream sums, and the two-stream result is bitwise run-to-run stable."""
+    import dataclasses
+    from paper_2402_15106_b200 import _lib as Lib
+    from paper_2402_15106_b200.api import HotPath, StepConfig
+    c = _case(seed=64) if dtype == 0 else _case(seed=64, d=64, k=256)
+    l = c["r"] * (1 + 2 ** -12)
+    base = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
+                      n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
+                      seed_sampling=3, seed_capping=5)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda())
+    outs, grads = [], []
+    for streams in (1, 2, 2):
+        hp = HotPath(dataclasses.replace(base, streams=streams), c["W"], cuda())
+        hp.build(T(c["x"]), T(c["a"]))
+        _, o = hp.forward(T(c["v0"]))
+        outs.append([t.cpu().numpy().copy() for t in o])
+        g = hp.forward_backward(T(c["v0"]), T(c["G"]))
+        torch.cuda.synchronize()
+        grads.append({n: g[n].cpu().numpy().copy() for n in NAMES})
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    for n in NAMES:
+        assert nerr(grads[1][n], grads[0][n]) <= 1e-5, n
+        assert np.array_equal(grads[1][n], grads[2][n]), n

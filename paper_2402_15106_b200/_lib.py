@@ -128,9 +128,19 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+try:  # the current stream's raw handle without torch.cuda.current_stream()'s Python-side device checks
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+    _cur_device = torch._C._cuda_getDevice
+except AttributeError:  # pragma: no cover
+    _raw_stream = _cur_device = None
+
+
 def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    if _raw_stream is not None:
+        return C.c_void_p(_raw_stream(_cur_device()))
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def _ws(nbytes, device):
@@ -170,11 +180,17 @@ def radius_counts(coords, n_dst, r, counts, stream=None):
     return counts
 
 
-def csc(col_idx, n_loc, csc_perm, csc_ptr, stream=None):
+def csc_workspace_size(n_edges, n_loc):
+    sz = SZ()
+    _call("csc_workspace_size", n_edges, n_loc, C.byref(sz))
+    return sz.value
+
+
+def csc(col_idx, n_loc, csc_perm, csc_ptr, stream=None, ws=None):
     E = col_idx.numel()
     sz = SZ()
     _call("csc_workspace_size", E, n_loc, C.byref(sz))
-    ws = _ws(sz.value, col_idx.device)
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, col_idx.device)
     _call("csc", _p(col_idx), E, n_loc, _p(csc_perm), _p(csc_ptr), _p(ws), ws.numel(), _stream(stream))
 
 

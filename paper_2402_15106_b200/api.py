@@ -89,7 +89,8 @@ class HotPath:
         self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts,
                                                   gid_bits=gid_bits)
         pipeline.build_graphs(self.subs, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
-                              want_bf16=(c.dtype == L.BF16), streams=self._side_streams())
+                              want_bf16=(c.dtype == L.BF16), streams=self._side_streams(),
+                              ws_cache=self.ws.setdefault("graph", {}))
         return self
 
     @property

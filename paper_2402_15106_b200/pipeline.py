@@ -89,13 +89,15 @@ def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bit
     return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
 
 
-def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, streams=None):
+def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, streams=None, ws_cache=None):
     """build_graph for several sub-domains with one host synchronisation: all
     radius graphs are enqueued (capacity n_own * n_e), then the edge counts and
     the host copies of row_ptr are read back together, then edge attributes
     and CSC views are enqueued.  streams: optional CUDA streams; sub-domain q's
     kernels go to streams[q % len(streams)] (arrays are allocated on the
-    current stream, which waits for every stream before returning)."""
+    current stream, which waits for every stream before returning).
+    ws_cache: optional dict keeping the radius-graph / CSC workspaces of each
+    sub-domain slot across calls (grown on demand)."""
     if not subs:
         return subs
     dev = subs[0].coords.device
@@ -118,12 +120,22 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, s
             done.record(st)
             main.wait_event(done)
 
-    cols = []
-    for sd in subs:
+    def ws(key, nbytes):
+        if ws_cache is None:
+            return None
+        t = ws_cache.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(1, int(nbytes * 1.25)), dtype=torch.uint8, device=dev)  # headroom for the next step
+            ws_cache[key] = t
+        return t
+
+    cols, rws = [], []
+    for q, sd in enumerate(subs):
         sd.row_ptr = torch.empty(sd.n_own + 1, dtype=torch.int64, device=dev)
         cols.append(torch.empty(max(1, sd.n_own * n_e), dtype=torch.int32, device=dev))
+        rws.append(ws(("radius", q), L.radius_graph_workspace_size(sd.n_loc, sd.n_own, sd.coords.shape[1])))
     fan_out(lambda q, sd: L.radius_graph(sd.coords, sd.gid, sd.n_own, r, n_e, seed, sd.row_ptr, cols[q],
-                                         want_count=False))
+                                         want_count=False, ws=rws[q]))
     host = torch.cat([sd.row_ptr for sd in subs]).cpu()  # the one synchronisation
     off = 0
     for sd, col in zip(subs, cols):
@@ -133,7 +145,8 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, s
         sd.col_idx = col[:E]
         sd.n_edges = E
         _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16)
-    fan_out(lambda q, sd: _edge_arrays(sd, edge_mode))
+    cws = [ws(("csc", q), L.csc_workspace_size(sd.n_edges, sd.n_loc)) for q, sd in enumerate(subs)]
+    fan_out(lambda q, sd: _edge_arrays(sd, edge_mode, cws[q]))
     return subs
 
 
@@ -147,9 +160,9 @@ def _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16):
     sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)
 
 
-def _edge_arrays(sd, edge_mode):
+def _edge_arrays(sd, edge_mode, csc_ws=None):
     L.edge_features(edge_mode, sd.coords, sd.attr, sd.row_ptr, sd.col_idx, sd.n_own, sd.e32, sd.e16)
-    L.csc(sd.col_idx, sd.n_loc, sd.csc_perm, sd.csc_ptr)
+    L.csc(sd.col_idx, sd.n_loc, sd.csc_perm, sd.csc_ptr, ws=csc_ws)
 
 
 def build_graph(sd: Subdomain, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True):

@@ -282,18 +282,23 @@ __global__ void __launch_bounds__(512, 1)
     }
   } else if (warp == 3) {
     // ============================================================ TMA producers
-    if (lane == 0) {  // W2 K-blocks, 4 per tile, 2-slot ring
-      uint32_t q = 0;
+    if (lane == 0) {  // W2 K-blocks in a 2-slot ring, K-block k in slot k & 1
+      // Tile 0 loads all four; afterwards each tile first consumes the two
+      // blocks the previous tile left in the ring (odd tiles: 2, 3; even
+      // tiles: 0, 1) and loads only the other two, so one load per slot per
+      // tile, each after the slot's first consumption of that tile
+      uint32_t nload[2] = {0, 0};
       for (uint32_t t = 0;; ++t) {
         const int b = t & 1;
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!m->desc[b].more) break;
         tc::mbar_arrive(&m->desc_free[b]);
-        for (int j = 0; j < 4; ++j, ++q) {
-          const uint32_t s = q & 1, r = q >> 1;
-          if (r > 0) tc::mbar_wait(&m->w2_empty[s], (r - 1) & 1);
-          tc::mbar_expect_tx(&m->w2_full[s], C::W2BLK);
-          tc::tma_load_2d(sW2 + s * C::W2BLK, &tW2, &m->w2_full[s], j * 64, 0);
+        const int k0 = t == 0 ? 0 : ((t & 1) ? 0 : 2), nk = t == 0 ? 4 : 2;
+        for (int k = k0; k < k0 + nk; ++k) {
+          const uint32_t sl = (uint32_t)(k & 1), i = ++nload[sl];  // i-th load into slot sl
+          if (i >= 2) tc::mbar_wait(&m->w2_empty[sl], (i - 2) & 1);
+          tc::mbar_expect_tx(&m->w2_full[sl], C::W2BLK);
+          tc::tma_load_2d(sW2 + sl * C::W2BLK, &tW2, &m->w2_full[sl], k * 64, 0);
         }
       }
     } else if (lane == 16) {  // dS_i tiles, one per row, NMAX-slot ring
@@ -327,27 +332,33 @@ __global__ void __launch_bounds__(512, 1)
                      aV = tc::smem_u32(sV), aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
       constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
       constexpr uint32_t IDESC_U = tc::idesc_bf16(128, C::NDS * D, false, true);
-      uint32_t w2q = 0, dsq = 0;
+      uint32_t w2l[2] = {0, 0}, dsq = 0;  // W2 loads consumed per slot
       auto mma1 = [&]() {  // z1 = E W1^T into columns 0..255
         tc::mma_bf16_ss(tmem, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone),
                         IDESC_MLP, 0u);
         tc::mma_commit(&m->d1_full);
         tc::mma_commit(&m->e_empty);
       };
-      auto mma2 = [&](uint32_t t) {  // z2 = a1 W2^T (W2 streamed by K block)
+      auto mma2 = [&](uint32_t t) {  // z2 = a1 W2^T (W2 K blocks through the 2-slot ring)
         tc::mbar_wait(&m->a1_ready, t & 1);
         tc::tc_fence_after();
-        for (int j = 0; j < 4; ++j, ++w2q) {
-          const uint32_t s = w2q & 1;
-          tc::mbar_wait(&m->w2_full[s], (w2q >> 1) & 1);
+        for (int jj = 0; jj < 4; ++jj) {
+          // odd tiles start with blocks 2, 3 (left in the ring by the previous
+          // tile), even tiles with 0, 1; tile 0 has all four loaded
+          const int j = (t & 1) ? (jj + 2) & 3 : jj;
+          const uint32_t s = (uint32_t)(j & 1);
+          if (t == 0 || jj >= 2) {  // a freshly loaded block
+            tc::mbar_wait(&m->w2_full[s], w2l[s] & 1);
+            ++w2l[s];
+          }
           tc::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             uint64_t ad = tc::sdesc(aAH + j * (128 * 128) + kk * 32, 16, 1024, tc::kSw128);
             uint64_t bd = tc::sdesc(aW2 + s * C::W2BLK + kk * 32, 16, 1024, tc::kSw128);
-            tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, (j > 0 || kk > 0) ? 1u : 0u);
+            tc::mma_bf16_ss(tmem, ad, bd, IDESC_MLP, (jj > 0 || kk > 0) ? 1u : 0u);
           }
-          tc::mma_commit(&m->w2_empty[s]);
+          if (jj < 2) tc::mma_commit(&m->w2_empty[s]);  // the slot's reload for this tile may start
         }
         tc::mma_commit(&m->d2_full);
       };

@@ -497,9 +497,10 @@ __global__ void __launch_bounds__(512, 1)
       tc::fence_async_shared();
       tc::tc_fence_before();
       tc::mbar_arrive(&m->a1_ready);
-      // a1 rows -> A1 (one 512-byte row per warp instruction), overlapping MMA2
-      tc::named_sync(2, 256);
-      {
+      // a1 rows -> A1 (one 512-byte row per warp instruction), overlapping MMA2;
+      // only when A1 is requested (the unfused B4 / B5)
+      if (A1g) {
+        tc::named_sync(2, 256);
         const int j = lane >> 3, c = lane & 7;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(512, 1)
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            if (ps[k] >= 0 && A1g) reinterpret_cast<uint4 *>(A1g + (int64_t)ps[k] * KH)[lane] = xs[k];
+            if (ps[k] >= 0) reinterpret_cast<uint4 *>(A1g + (int64_t)ps[k] * KH)[lane] = xs[k];
         }
       }
       // h = relu(z2 + b2) -> AH (after MMA2 and the a1 copy-out), + [h > 0] bits

@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(512, 1)
       auto mma2 = [&](uint32_t t) {  // z2 = a1 W2^T (W2 K blocks through the 2-slot ring)
         tc::mbar_wait(&m->a1_ready, t & 1);
         tc::tc_fence_after();
+#pragma unroll 1
         for (int jj = 0; jj < 4; ++jj) {
           // odd tiles start with blocks 2, 3 (left in the ring by the previous
           // tile), even tiles with 0, 1; tile 0 has all four loaded
@@ -645,13 +646,23 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) mwh[u] = h ? mw1[u] : mw0[u];
         float acc = 0.f;
-#pragma unroll
+        // rows not unrolled: one copy of the chunk code keeps this loop's
+        // footprint in the instruction cache (the kernel is ~100 KB of SASS)
+#pragma unroll 1
         for (int g = 0; g < NMAX; ++g) {
           if (g >= nn) break;
-          const int s0 = tr.s0[g];
-          const int deg = tr.deg[g];
+          // register selects, not a dynamically indexed (local-memory) array
+          int s0 = tr.s0[0], deg = tr.deg[0];
+          int64_t ebg = tr.eb[0];
+#pragma unroll
+          for (int i = 1; i < NMAX; ++i)
+            if (g == i) {
+              s0 = tr.s0[i];
+              deg = tr.deg[i];
+              ebg = tr.eb[i];
+            }
           const int ns = (deg + 15) & ~15;
-          __nv_bfloat16 *row0 = dZ2g + tr.eb[g] * KH;
+          __nv_bfloat16 *row0 = dZ2g + ebg * KH;
           const uint32_t ta = tmem + lane_off + (h == 0 ? 384 : 256) + s0;
           int c0 = 0;
           for (; c0 + 64 <= ns; c0 += 64) acc += dz2_chunk<64>(ta + c0, slot_bits(mwh, s0 + c0), kap, c0, deg, row0);

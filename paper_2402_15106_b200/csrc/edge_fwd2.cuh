@@ -100,6 +100,7 @@ __device__ __forceinline__ void walk_tile(MiscT *m, DescT *d, const int64_t *__r
     const int64_t my = cur + lane <= end ? cur + lane : end;
     const int64_t rp = row_ptr[my];
     int k = 0;
+#pragma unroll 1
     for (; k < 31; ++k) {
       const int64_t a = __shfl_sync(0xffffffffu, rp, k), z = __shfl_sync(0xffffffffu, rp, k + 1);
       if (cur + k >= end) { done = true; break; }

@@ -34,6 +34,7 @@ struct Misc2 {
   uint64_t e_full[2], e_empty, d1_full[2], region_free[2], desc_free[2];
   uint64_t v_full, v_empty, ah_free, s_full;
   uint64_t a1_ready[4], d2_full[2], h_ready[2];
+  uint64_t w2_full;          // resident W2 loaded (TMA)
   int64_t cur_row, row_end;
   uint32_t tmem;
   float b1[KH], b2[KH];     // biases (L1 is all but absent at this SMEM carve-out)
@@ -130,7 +131,8 @@ __device__ __forceinline__ void walk_tile(MiscT *m, DescT *d, const int64_t *__r
 
 template <int D>
 __global__ void __launch_bounds__(512, 1)
-    edge_fwd2_kernel(const __nv_bfloat16 *__restrict__ e16, const __nv_bfloat16 *__restrict__ v,
+    edge_fwd2_kernel(const __grid_constant__ CUtensorMap tW2, const __nv_bfloat16 *__restrict__ e16,
+                     const __nv_bfloat16 *__restrict__ v,
                      const int64_t *__restrict__ row_ptr, int64_t rb, int64_t re, int64_t eb, int64_t ee, Packed pw,
                      const float *__restrict__ b1, const float *__restrict__ b2, __nv_bfloat16 *__restrict__ S,
                      int64_t kp, const int32_t *__restrict__ col) {
@@ -173,16 +175,15 @@ __global__ void __launch_bounds__(512, 1)
     tc::mbar_init(&m->ah_free, 1);
     tc::mbar_init(&m->s_full, 1);
     for (int j = 0; j < 4; ++j) tc::mbar_init(&m->a1_ready[j], 128);
+    tc::mbar_init(&m->w2_full, 1);
     tc::fence_mbar_init();
+    // resident W2 by TMA (4 K blocks of [256 kappa][64 kappa'] SW128), in
+    // flight while the rest of the CTA sets up; the first MMA2 waits for it
+    tc::mbar_expect_tx(&m->w2_full, C::W2_BYTES);
+    for (int j = 0; j < 4; ++j) tc::tma_load_2d(sW2 + j * (KH * 128), &tW2, &m->w2_full, j * 64, 0);
   }
   if (warp == 1) tc::tmem_alloc<512>(&m->tmem);
-  {  // W2 (K-major SW128, 4 K-blocks of 64) and W1 (interleaved K=16), resident
-    const uint4 *g2 = reinterpret_cast<const uint4 *>(pw.W2);
-    for (int q = tid; q < KH * KH / 8; q += 512) {
-      int n = q / (KH / 8), rem = q % (KH / 8);
-      int j = rem / 8, c = rem % 8;
-      *reinterpret_cast<uint4 *>(sW2 + j * (KH * 128) + tc::sw128_off(n, c)) = g2[q];
-    }
+  {  // W1 (interleaved K=16), resident; W2 arrives by TMA (above)
     const uint4 *g1 = reinterpret_cast<const uint4 *>(pw.W1);
     for (int q = tid; q < KH * 2; q += 512) {
       int r = q / 2, u = q % 2;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(512, 1)
         return true;
       };
       bool more = mma1(0);
+      tc::mbar_wait(&m->w2_full, 0);  // resident W2 landed
       for (uint32_t t = 0; more; ++t) {
         const int b = t & 1;
         const uint32_t p1 = t & 1;

@@ -221,12 +221,14 @@ static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16
                                      const Packed &pw, const float *b1, const float *b2, __nv_bfloat16 *S,
                                      int64_t kp, cudaStream_t s) {
   using C = EF2<D>;
+  CUtensorMap tW2;
+  DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
   auto kern = edge_fwd2_kernel<D>;
   DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_FWD, s);
-  kern<<<grid, 512, C::SMEM, s>>>(e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  kern<<<grid, 512, C::SMEM, s>>>(tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

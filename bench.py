@@ -346,11 +346,16 @@ def main():
     L.probe_begin(probe_id, 64 * args.steps * sc.L * len(hp.subs) + 64)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     e0.record(st)
-    for _ in range(args.steps):
+    for k_ in range(args.steps):
         step(devin)
+        if k_ < args.steps - 1:
+            marks[k_].record(st)
     e1.record(st)
     torch.cuda.synchronize()
+    bounds = [e0] + marks + [e1]
+    step_ms = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(args.steps)]
     probe_ms, probe_n = L.probe_end()
     clk = clocks.stop()
     if world > 1:
@@ -499,6 +504,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "graph_ms": graph_ms,
+            "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "gpu_launches": launches * args.steps,
             "warmup_extra": warmup_extra,
             "gpu_launches_cub": lib_other * args.steps,

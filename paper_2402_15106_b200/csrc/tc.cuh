@@ -185,9 +185,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------ CTA pairs (cta_group::2) --
-// Used by kernels launched with __cluster_dims__(2, 1, 1): rank 0 (the
-// leader) issues the M = 256 products over both CTAs' shared memory and
-// tensor memory; both CTAs load their own operand halves.
+// For kernels launched with __cluster_dims__(2, 1, 1): rank 0 (the leader)
+// issues the M = 256 products over both CTAs' shared memory and tensor
+// memory; both CTAs load their own operand halves.  Validated by the 2-SM
+// variant of the fused dW1 kernel (correct, but slower: DESIGN §6.1a); no
+// kernel of the library uses them at present (the 2-SM edge backward of
+// DESIGN §10 would).
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

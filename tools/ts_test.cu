@@ -1,5 +1,5 @@
-// ts_test.cu - checks the tcgen05 "A in TMEM" operand layout assumed by the
-// kernels: A[m][k] (bf16) at TMEM lane m, column k/2, low half for even k
+// ts_test.cu - checks the tcgen05 "A in TMEM" operand layout of tc::mma_bf16_ts /
+// tc::tmem_st32 (tc.cuh): A[m][k] (bf16) at TMEM lane m, column k/2, low half for even k
 // (tcgen05.st.32x32b from the thread owning lane m).  Development tool.
 #include <cstdio>
 #include <cstdint>
@@ -10,22 +10,12 @@
 #include "../paper_2402_15106_b200/csrc/tc.cuh"
 using namespace dsmpnn;
 
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
-}
-
 // D[128 x 64] = A[128 x 64] B^T, B stored [64 n][64 k] K-major SW128
 __global__ void ts_kernel(const __nv_bfloat16 *A, const __nv_bfloat16 *B, float *D) {
   __shared__ __align__(1024) uint8_t sB[8192];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int t = threadIdx.x, warp = t >> 5;
   if (warp == 0) tc::tmem_alloc<128>(&slot);
   if (t == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
   for (int q = t; q < 64 * 8; q += 128) {
@@ -46,8 +36,8 @@ __global__ void ts_kernel(const __nv_bfloat16 *A, const __nv_bfloat16 *B, float 
       h.y = A[t * 64 + 2 * j + 1];
       r[j] = *reinterpret_cast<uint32_t *>(&h);
     }
-    tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + 64, r);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc::tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + 64, r);
+    tc::tmem_st_wait();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -56,12 +46,7 @@ __global__ void ts_kernel(const __nv_bfloat16 *A, const __nv_bfloat16 *B, float 
     constexpr uint32_t id = tc::idesc_bf16(128, 64, false, false);
     for (int kk = 0; kk < 4; ++kk) {
       const uint64_t bd = tc::sdesc(tc::smem_u32(sB) + kk * 32, 16, 1024, tc::kSw128);
-      const uint32_t acc = kk > 0;
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-          "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
-          "r"(tmem + 64 + kk * 8), "l"(bd), "r"(id), "r"(acc)
-          : "memory");
+      tc::mma_bf16_ts(tmem, tmem + 64 + kk * 8, bd, id, kk > 0 ? 1u : 0u);
     }
     tc::mma_commit(&bar);
   }

@@ -28,7 +28,10 @@ def _build(L, x, a, gid, P, l, r, n_e, seed, mode):
     return subs
 
 
-def test_halo_loopback_matches_oracle(L):
+@pytest.mark.parametrize("width", [8, 5, 6], ids=["w8", "w5", "w6"])
+def test_halo_loopback_matches_oracle(L, width):
+    # rows of whole 16-byte chunks (w8) take the one-launch job-table path,
+    # the others the per-peer gathers
     g = np.random.default_rng(3)
     x = g.random((3000, 2)).astype(np.float32)
     gid = np.arange(3000, dtype=np.int64)
@@ -38,7 +41,7 @@ def test_halo_loopback_matches_oracle(L):
     subs, _ = pipeline.decompose(T(x), T(gid), T(a), P, r, r, range(P))
     _, _, _, ranks = partition.plan(x, gid, P, r, r)
     for dt, tdt in ((0, torch.float32), (1, torch.bfloat16)):
-        vals_np = [g.normal(size=(len(q["local_rows"]), 8)).astype(np.float32) for q in ranks]
+        vals_np = [g.normal(size=(len(q["local_rows"]), width)).astype(np.float32) for q in ranks]
         if dt == 1:
             vals_np = [synth.round_bf16(v) for v in vals_np]
         vals = [T(v).to(tdt) for v in vals_np]
@@ -46,6 +49,15 @@ def test_halo_loopback_matches_oracle(L):
         want = halo.halo_forward(ranks, vals_np)
         for got, w in zip(vals, want):
             assert np.array_equal(N(got).astype(np.float32), w.astype(np.float32))
+
+
+def test_accumulate_f32(L):
+    g = np.random.default_rng(4)
+    for n in (1, 257, 1 << 20):
+        a, b = g.normal(size=n).astype(np.float32), g.normal(size=n).astype(np.float32)
+        ta, tb = T(a), T(b)
+        L.accumulate_f32(ta, tb)
+        assert np.array_equal(N(ta), a + b)
 
 
 def test_scatter_add_reverse(L):

@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--streams", type=int, default=2, help="CUDA streams the local sub-domains are spread over")
+    ap.add_argument("--no-comm", action="store_true",
+                    help="skip every halo refresh (PAPER.md:209 no-communication ablation; halos stay stale)")
+    ap.add_argument("--halo-ratio", type=float, default=1.0, help="overlap length l = ratio * r (Table 4 sweep)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the timed run")
     return ap.parse_args()
 
 
@@ -56,7 +60,7 @@ def dist_env():
     return rank, world, local
 
 
-def step_config(cfg_name, world, dtype):
+def step_config(cfg_name, world, dtype, halo_ratio=1.0, halo=True):
     from paper_2402_15106_b200 import _lib as L
     from paper_2402_15106_b200 import synth
     from paper_2402_15106_b200.api import StepConfig
@@ -66,7 +70,7 @@ def step_config(cfg_name, world, dtype):
     nparts = max(cfg.P, world) if cfg.kind != "weak" else world
     s = cfg.s if cfg.s else n
     sc = StepConfig(n_points=n, s=min(s, n), dim=cfg.dim, n_attr=attr.shape[1], nparts=nparts, r=cfg.r,
-                    overlap_l=cfg.r, n_e=cfg.n_e, d=cfg.d, k=cfg.k, L=cfg.L,
+                    overlap_l=float(np.float32(halo_ratio * cfg.r)), n_e=cfg.n_e, halo=int(halo), d=cfg.d, k=cfg.k, L=cfg.L,
                     edge_mode=L.EDGE_DIFF if cfg.edge_mode == "diff" else L.EDGE_CONCAT,
                     dtype=L.BF16 if dtype == "bf16" else L.F32,
                     seed_sampling=synth.BASE_SEED + synth.SEED_SAMPLING,
@@ -173,16 +177,17 @@ def count_our_launches(fn):
     return ours, other
 
 
-def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the committed `ncu --set full` summary (profiles/ncu_traffic.json),
-    or None when no capture of the current kernel is recorded."""
+def ncu_traffic(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` on
+    `config` from the committed `ncu --set full` summary
+    (profiles/ncu_traffic.json, keyed kernel -> config), or None when no
+    capture of that kernel on that config is recorded (never another config's)."""
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as f:
-            rec = json.load(f).get(kernel)
-        return rec["bytes_per_launch"] if rec else None
-    except (OSError, ValueError, KeyError):
-        return None
+            rec = json.load(f).get(kernel, {}).get(config)
+        return (rec["bytes_per_launch"], rec.get("source")) if rec else (None, None)
+    except (OSError, ValueError, KeyError, AttributeError):
+        return None, None
 
 
 def measured_peaks():
@@ -253,6 +258,121 @@ def oracle_baseline(cfg_name, budget_s, world=1):
                       f"attributes built outside the timed layer calls"}
 
 
+def oracle_baseline_both(cfg_name, budget_s, world=1):
+    """the oracle on all host cores (numpy's thread pool) and on
+    one core, each on half the budget; `value` is the all-cores figure."""
+    allc = oracle_baseline(cfg_name, budget_s / 2, world)
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            one = oracle_baseline(cfg_name, budget_s / 2, world)
+        allc["single_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
+    except ImportError:
+        pass
+    allc["host_cpus"] = os.cpu_count()
+    return allc
+
+
+def oracle_parity(hp, sc, cfg_name, world, n_rows=96):
+    """the benchmarked run is checked against the oracle
+    after the timed region, on the same synthetic inputs (nothing the oracle
+    consumes comes from the CUDA path):
+      * Nystrom sample (a1): all s ids, bit-exact;
+      * partition (a3): the local order of this rank's first sub-domain, bit-exact;
+      * radius graph (a2): n_rows hash-selected destination rows, bit-exact;
+      * layer forward (a4 + a5): layer 0 of that sub-domain on those rows,
+        re-run through the same HotPath.forward the timed steps use;
+      * layer backward (a7): layer 0 with the upstream gradient restricted to
+        those rows (masked upstream), all weight gradients and dv;
+    within the north_star's tolerance (1e-5 F32, 2e-2 BF16, normwise-inf)."""
+    import torch
+    from oracle import features, graph, layer, partition, sample
+    from oracle.layer import LayerDesc
+    from oracle.precision import round_bf16
+    from paper_2402_15106_b200 import _lib as L
+    from paper_2402_15106_b200 import synth
+    t0 = time.perf_counter()
+    cfg = synth.CONFIGS[cfg_name]
+    coords, attr = synth.points(cfg, parts=max(world, cfg.P) if cfg.kind == "weak" else None)
+    bf16 = sc.dtype == L.BF16
+    tol = 2e-2 if bf16 else 1e-5
+    res = {"tol": tol, "rows": n_rows}
+    ids = sample.sample(sc.n_points, sc.s, sc.seed_sampling)
+    res["sample_bit_exact"] = bool(np.array_equal(hp.ids.cpu().numpy(), ids))
+    x_s, a_s, gid_s = coords[ids], attr[ids], ids.astype(np.int64)
+    _, _, _, ranks = partition.plan(x_s, gid_s, sc.nparts, sc.overlap_l, sc.r)
+    sd = hp.subs[0]
+    rk = ranks[sd.rank]
+    res["partition_bit_exact"] = bool(np.array_equal(sd.local_rows.cpu().numpy(), rk["local_rows"])
+                                      and sd.n_deep == rk["n_deep"] and sd.n_near == rk["n_near"])
+    lr = rk["local_rows"]
+    x, a, gid = x_s[lr], a_s[lr], gid_s[lr]
+    g = np.random.default_rng(1000 + sd.rank)
+    rows = np.sort(g.choice(sd.n_own, size=min(n_rows, sd.n_own), replace=False))
+    adj = graph.radius_graph_rows(x, gid, rows, sc.r, sc.n_e, sc.seed_capping)
+    rph = sd.row_ptr_host.numpy()
+    colg = sd.col_idx.cpu().numpy()
+    res["graph_bit_exact"] = bool(all(np.array_equal(colg[rph[i]:rph[i + 1]], q) for i, q in zip(rows, adj)))
+    # the oracle's CSR over the selected rows, renumbered 0..m-1 (sources: the local rows, shifted by m)
+    m = len(rows)
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum([len(q) for q in adj])
+    col = np.concatenate(adj).astype(np.int64)
+    mode = "diff" if sc.edge_mode == L.EDGE_DIFF else "concat"
+    e = features.edge_features(mode, x, a, np.repeat(rows, np.diff(rp)), col)
+    W = synth.weights(e.shape[1], sc.d, sc.d, sc.k)
+    v0_all = synth.node_features(sc.s, sc.d)
+    G_all = synth.upstream_grad(sc.s, sc.d)
+    v = v0_all[lr]
+    Wo, vo, eo = dict(W), v, e
+    if bf16:
+        for nm in ("W1", "W2", "W3", "b3", "W_root"):
+            Wo[nm] = round_bf16(W[nm])
+        vo, eo = round_bf16(v), round_bf16(e)
+    desc = LayerDesc(e.shape[1], sc.d, sc.d, sc.k, sc.root, sc.act, "bf16" if bf16 else "none")
+    vloc = np.concatenate([vo[rows], vo])
+    out_o, pre_o = layer.layer_fwd(desc, Wo, vloc, eo, rp, col + m)
+    # GPU: the timed path's forward (same inputs, deterministic), layer 0 of this sub-domain
+    dev = hp.dev
+    v0_d = torch.from_numpy(np.ascontiguousarray(v0_all)).to(dev)
+    acts, _ = hp.forward(v0_d)
+    out_g = acts[1][0][: sd.n_own].float().cpu().numpy()[rows]
+    res["fwd_err"] = _nerr(out_g, out_o)
+    # masked-upstream backward of layer 0 (kinks within 2% of the spread masked, as in the tests)
+    Gm = G_all[lr][rows].copy()
+    if bf16 and sc.act == 1:
+        Gm[np.abs(pre_o) < 2e-2 * pre_o.std()] = 0.0
+    dv_o, _, g_o = layer.layer_bwd(desc, Wo, vloc, eo, rp, col + m, Gm, want_de=False)
+    dv_o_full = dv_o[m:].copy()
+    dv_o_full[rows] += dv_o[:m]
+    Gd = torch.zeros((sd.n_own, sc.d), dtype=torch.float32, device=dev)
+    Gd[torch.from_numpy(rows).to(dev)] = torch.from_numpy(Gm.astype(np.float32)).to(dev)
+    gv = torch.zeros((sd.n_loc, sc.d), dtype=torch.float32, device=dev)
+    grads = {n: torch.zeros_like(t) for n, t in hp.W.items()}
+    ein = sd.e16 if bf16 else sd.e32
+    bws = hp._ws(("bwd", 0), L.layer_bwd_workspace_size(hp.desc, sd.n_own, sd.n_loc, sd.n_edges))
+    L.layer_bwd(hp.desc, hp.W, hp.packed, acts[0][0], ein, sd.row_ptr, sd.col_idx, sd.csc_perm, sd.csc_ptr,
+                sd.n_own, sd.n_loc, 0, sd.n_own, Gd, gv, None, grads, hp.ws[("fwd", 0, 0)], bws,
+                row_ptr_host=sd.row_ptr_host)
+    torch.cuda.synchronize()
+    errs = {"dv": _nerr(gv.cpu().numpy(), dv_o_full)}
+    for nm, t in grads.items():
+        errs[nm] = _nerr(t.cpu().numpy(), g_o[nm])
+    res["bwd_err_max"] = max(errs.values())
+    res["bwd_err"] = errs
+    res["ok"] = bool(res["sample_bit_exact"] and res["partition_bit_exact"] and res["graph_bit_exact"]
+                     and res["fwd_err"] <= tol and res["bwd_err_max"] <= tol)
+    res["oracle_s"] = time.perf_counter() - t0
+    return res
+
+
+def _nerr(x, ref):
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    den = np.abs(ref).max() if ref.size else 0.0
+    return float(np.abs(x - ref).max() / den) if den > 0 else float(np.abs(x - ref).max() if x.size else 0.0)
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -266,6 +386,7 @@ def run_reference(args):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         vals.append(oracle_baseline(args.config, per_step_budget, world))
+    vals[-1]["host_cpus"] = os.cpu_count()
     step_ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
     value = float(np.median([v["value"] for v in vals]))
     cb = dict(vals[-1])
@@ -280,14 +401,47 @@ def run_reference(args):
     return 0
 
 
+
+
 # -------------------------------------------------------------- our leg ----
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N > 1) outside a torchrun launch: start N
+    ranks on this node with torch.distributed.run (127.0.0.1 rendezvous) and
+    forward its exit status; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def f_fb_d2(subs, k, d, d_e):
+    """Algorithmic fwd+bwd FLOPs of the formulation run (D2, "aggregate
+    first"): per edge 6k^2 + 4 d_e k + 6(k+1) d; per
+    destination row with edges 6 (k+1) d^2 (the row contraction S~ . Theta~
+    forward, its two backward products)."""
+    tot = 0.0
+    for sd in subs:
+        rp = sd.row_ptr_host.numpy()
+        rows_with_edges = int((np.diff(rp) > 0).sum())
+        tot += sd.n_edges * (6 * k * k + 4 * d_e * k + 6 * (k + 1) * d) + rows_with_edges * 6 * (k + 1) * d * d
+    return tot
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
     import torch
     import torch.distributed as dist
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -295,7 +449,7 @@ def main():
     from paper_2402_15106_b200 import _lib as L
     from paper_2402_15106_b200 import synth
     from paper_2402_15106_b200.api import HotPath
-    cfg, sc, coords, attr = step_config(args.config, world, args.dtype)
+    cfg, sc, coords, attr = step_config(args.config, world, args.dtype, args.halo_ratio, not args.no_comm)
     sc = dataclasses.replace(sc, streams=args.streams)
     d_e = (sc.dim + sc.n_attr) * (1 if sc.edge_mode == L.EDGE_DIFF else 2)
     W = synth.weights(d_e, sc.d, sc.d, sc.k)
@@ -304,7 +458,7 @@ def main():
     host = {n: torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for n, a in
             (("coords", coords), ("attr", attr), ("v0", v0), ("G", G))}
     devin = {n: t.to(dev) for n, t in host.items()}
-    hp = HotPath(sc, W, dev, rank, world)
+    hp = HotPath(sc, W, dev, rank, world)  # world > 1: the library NCCL context (dsmpnn_ctx_create)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     def step(inp):
@@ -325,10 +479,10 @@ def main():
     # second-layer GEMM (F32)
     probe_id = L.PROBE_BF16_EDGE_BWD if sc.dtype == L.BF16 else L.PROBE_F32_MLP2
     # algorithmic HBM bytes of one step's edge-backward launches (DESIGN.md
-    # "Rooflines"): per edge e (32 B, bf16 padded to 16) + v_j (2d) + col (4)
-    # + dz2 (2k) + u_p (2d); per destination row dS_i (2(k+1)d).  The step
-    # requests no edge-attribute gradient, so the kernel writes no A1 (the
-    # dW2 / dW1 kernels recompute a1 from e; layer_bf16_bwd.cu)
+    # §6): per edge e (32 B, bf16 padded to 16) + v_j (2d) + col (4) + dz2 (2k)
+    # + u_p (2d); per destination row dS_i (2(k+1)d).  The step requests no
+    # edge-attribute gradient, so the kernel writes no A1 (the dW2 / dW1
+    # kernels recompute a1 from e; layer_bf16_bwd.cu)
     bwd_bytes_step = sum(sd.n_edges * (32 + 4 + 4 * sc.d + 2 * sc.k) + sd.n_own * 2 * (sc.k + 1) * sc.d
                          for sd in hp.subs) * sc.L
 
@@ -412,7 +566,29 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1) / args.steps
 
+    # ---- layer-only time (SURVEY D.1 t_iter: L x (fwd + halo) + L x bwd on
+    # the built graphs, no graph build) with the halo exchange on and off:
+    # exposed communication = t(on) - t(off) (D.4)
+    def layers_ms(halo_on):
+        hp.cfg = dataclasses.replace(hp.cfg, halo=int(halo_on))
+        hp.forward_backward(devin["v0"], devin["G"])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        for _ in range(args.steps):
+            flush.zero_()
+            hp.forward_backward(devin["v0"], devin["G"])
+        a1.record(st)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / args.steps
+
+    layer_ms = layers_ms(sc.halo)
+    layer_ms_nocomm = layers_ms(False) if sc.halo else layer_ms
+    hp.cfg = dataclasses.replace(hp.cfg, halo=sc.halo)
     gc.enable()
+
     # roofline probe of the dominant kernel with the sub-domains on one stream:
     # with 2 streams its launches overlap other kernels, so their event
     # durations measure the schedule, not the kernel (both are reported)
@@ -441,16 +617,25 @@ def main():
     torch.cuda.synchronize()
     graph_ms = g0.elapsed_time(g1) / args.steps
 
-    stats = torch.tensor([ms, e2e_ms, float(E_local)], dtype=torch.float64, device=dev)
+    stats = torch.tensor([ms, e2e_ms, layer_ms, layer_ms_nocomm, float(E_local)], dtype=torch.float64, device=dev)
     if world > 1:
-        mx = stats.clone()
-        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
-        tot = stats[2:].clone()
+        mx = stats[:4].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = stats[4:].clone()
         dist.all_reduce(tot)
-        stats = torch.cat([mx[:2], tot])
-    ms, e2e_ms, E_tot = float(stats[0]), float(stats[1]), float(stats[2])
+        stats = torch.cat([mx, tot])
+    ms, e2e_ms, layer_ms, layer_ms_nocomm, E_tot = [float(x) for x in stats]
+    # the formulation's own algorithmic FLOPs, summed over ranks
+    fl = torch.tensor([f_fb_d2(hp.subs, sc.k, sc.d, d_e) * sc.L], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fl)
+    fl_tot = float(fl[0])
     value = E_tot * sc.L / (ms / 1e3)
     e2e_value = E_tot * sc.L / (e2e_ms / 1e3)
+
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = oracle_parity(hp, sc, args.config, world)
 
     if rank == 0:
         peaks, src = measured_peaks()
@@ -466,14 +651,16 @@ def main():
             peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         per_launch_ms = probe_ms / max(1, probe_n)
         units_per_launch = E_local * args.steps * sc.L / max(1, probe_n)
+        traffic = traffic_src = None
         if sc.dtype == L.BF16:
             bytes_per_launch = bwd_bytes_step * args.steps / max(1, probe_n)
             achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9 if probe_n else 0.0
             tensor_tflops = bwd_flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
-            traffic = ncu_traffic("edge_bwd2")
+            if world == 1 and args.halo_ratio == 1.0:
+                traffic, traffic_src = ncu_traffic("edge_bwd2", args.config)
         else:
             achieved = flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
-            bytes_per_launch, tensor_tflops, traffic = None, None, None
+            bytes_per_launch, tensor_tflops = None, None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -481,14 +668,18 @@ def main():
             "dtype": "bf16" if sc.dtype == L.BF16 else "f32", "data": "synthetic",
             "config": {"workload": f"{cfg.name} (BASELINE.json configs[{list(synth.CONFIGS).index(cfg.name)}])",
                        "n_points": sc.n_points, "sampled": sc.s, "subdomains": sc.nparts, "radius": sc.r,
-                       "overlap_l": sc.overlap_l, "n_e": sc.n_e, "width": sc.d, "ker_width": sc.k, "layers": sc.L,
+                       "overlap_l": sc.overlap_l, "halo_ratio": args.halo_ratio, "halo": "on" if sc.halo else "off",
+                       "n_e": sc.n_e, "width": sc.d, "ker_width": sc.k, "layers": sc.L,
                        "edges_total": int(E_tot), "edge_attr_dim": d_e,
                        "form": "GNO: relu(W v_i + mean kappa(e) v_j + b)",
                        "l2": "256 MB buffer zeroed at the start of every step, inside the timed region",
                        "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd",
-                       "streams": sc.streams},
+                       "streams": sc.streams,
+                       "comm": "library NCCL context (dsmpnn_halo_exchange)" if world > 1 else
+                               "sub-domains on one device: halo = device copies"},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": {1: "F32 mlp2 sgemm", 5: "bf16 fused edge bwd (edge_bwd2)"}.get(probe_id,
                                                                                                str(probe_id)),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
@@ -504,14 +695,34 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "graph_ms": graph_ms,
+            "layers_only": {"ms": layer_ms, "value": E_tot * sc.L / (layer_ms / 1e3),
+                            "ms_no_comm": layer_ms_nocomm,
+                            "exposed_comm_ms": layer_ms - layer_ms_nocomm if sc.halo else None,
+                            "what": "L x (fwd + halo) + L x bwd on the built graphs (SURVEY D.1 t_iter), "
+                                    "max over ranks; no-comm = the same with every halo refresh skipped"},
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
             "gpu_launches": launches * args.steps,
             "warmup_extra": warmup_extra,
             "gpu_launches_cub": lib_other * args.steps,
             "clocks": clk,
         }
+        if sc.dtype == L.BF16:
+            line["roofline"]["d2_flops_per_step"] = fl_tot
+            line["roofline"]["d2_tensor_frac_layers"] = fl_tot / (layer_ms / 1e3) / 1e12 / float(
+                peaks["bf16_tflops_sustained"]) / world
+            line["roofline"]["d2_tensor_frac_step"] = fl_tot / (ms / 1e3) / 1e12 / float(
+                peaks["bf16_tflops_sustained"]) / world
+            line["roofline"]["d2_note"] = ("F_fb(D2) = 6k^2 + 4 d_e k + 6(k+1)d per edge + 6(k+1)d^2 per row "
+                                           "with edges (SURVEY D.3), / bf16_tflops_sustained; layers = graph "
+                                           "build excluded, step = included")
+        if parity is not None:
+            line["parity"] = parity
+            if not parity["ok"]:
+                line["value"] = None
+                line["e2e"]["value"] = None
+                line["failed"] = "parity check of the timed run against the oracle failed"
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = oracle_baseline(args.config, args.cpu_budget_s, world)
+            line["cpu_baseline"] = oracle_baseline_both(args.config, args.cpu_budget_s, world)
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -40,6 +40,8 @@ typedef enum {
   DSMPNN_ERR_INDEX = -3,       /* index out of range */
   DSMPNN_ERR_CAPACITY = -4,    /* output or workspace buffer too small */
   DSMPNN_ERR_CUDA = -5,        /* a CUDA runtime error (text in dsmpnn_last_error) */
+  DSMPNN_ERR_NCCL = -6,        /* an NCCL error, or a communicator aborted by the watchdog */
+  DSMPNN_ERR_TIMEOUT = -7,     /* dsmpnn_ctx_sync: the exchange did not finish in time (communicator aborted) */
   DSMPNN_ERR_UNSUPPORTED = -8, /* shape/dtype combination not implemented */
   DSMPNN_ERR_DEGENERATE = -9   /* RCB split leaves an empty side (R12) */
 } dsmpnn_status;
@@ -164,6 +166,12 @@ dsmpnn_status dsmpnn_partition_all(const float *coords, const int64_t *gid, int6
 dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
                                  int32_t elem_bytes, void *out, void *stream);
 
+/* The same gather from float32 rows into bfloat16 rows, rounded to nearest
+ * even (the BF16 mode's layer-0 operand); rows may be NULL
+ * (then row k is row k). */
+dsmpnn_status dsmpnn_gather_rows_bf16(const float *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
+                                      void *out, void *stream);
+
 /* Edge attributes ("relative difference between node coordinates
  * and attributes"; Alg. 1 :397; R21).  For edge p of row i with source j:
  *   DIFF:   e_p = (x_i - x_j, a_i - a_j)            d_e = dim + n_attr
@@ -195,7 +203,13 @@ dsmpnn_status dsmpnn_pack_weights(const dsmpnn_layer_desc *desc, const dsmpnn_we
  *   ws       saved activations for dsmpnn_layer_bwd, sized by
  *            dsmpnn_layer_workspace_size(desc, n_dst, E); pass the same ws to bwd.
  * Errors: SHAPE for ROOT_IDENTITY with d_in != d_out or BF16 with d_e > 16;
- * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64}, k in {64,128,256}. */
+ * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64} and k = 256,
+ * and for a BF16 call whose rows [row_begin, row_end) include a row of more
+ * than 128 edges (the fused edge kernels tile whole rows; checked on the host
+ * from row_ptr_host, else from row_ptr with a synchronising scan).
+ * With DSMPNN_DEBUG set in the environment, layer_fwd / layer_bwd also
+ * validate the CSR (row_ptr non-decreasing, 0 <= col_idx < n_loc) and return
+ * INDEX on a violation (synchronising). */
 dsmpnn_status dsmpnn_layer_workspace_size(const dsmpnn_layer_desc *desc, int64_t n_dst, int64_t n_edges,
                                           size_t *bytes);
 dsmpnn_status dsmpnn_layer_fwd(const dsmpnn_layer_desc *desc, const dsmpnn_weights *w, const void *v,
@@ -257,6 +271,81 @@ dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *val
                                                const int64_t *const *send_ptr, const int32_t *const *send_idx,
                                                int32_t width, void *stream);
 
+/* ------------------------------------------------------- a6 over NCCL --- */
+/* The halo exchange between processes ("the overlap area of a
+ * given domain is updated from the neighboring domains' interiors"; Alg. 1
+ * :411 Comm(i_b, Omega, v_L)) and the gradient sum (Alg. 1 :418), over an NCCL
+ * communicator owned by a context.  One process per GPU; a process may hold
+ * several sub-domains ("parts").
+ *
+ * dsmpnn_comm_unique_id: rank 0 creates the communicator id (host buffer of
+ *   DSMPNN_UNIQUE_ID_BYTES); the caller distributes it to every rank (e.g. a
+ *   torch.distributed broadcast) before dsmpnn_ctx_create.
+ * dsmpnn_ctx_create: collective over the nranks processes (blocks until all
+ *   have joined); sets `device` current; creates the communicator, a
+ *   high-priority comm stream and the events of the exchange.
+ *   dsmpnn_ctx_destroy frees them (NULL is a no-op).
+ * dsmpnn_halo_exchange: for the parts this rank holds (local_parts[i], with
+ *   values[i] / halo_ptr[i] / send_ptr[i] / send_idx[i] from that part's
+ *   plan, dsmpnn_partition; part_rank[p] = rank holding part p, host int32
+ *   [nparts]; every part with part_rank == this rank must be listed):
+ *     FORWARD:     values_t[halo_ptr_t[s] + r] = values_s[send_idx_s[send_ptr_s[t] + r]]
+ *                  for every ordered pair s != t with s or t local;
+ *     REVERSE_ADD: values_p[send_idx_p[send_ptr_p[q] + r]] += values_q[halo_ptr_q[p] + r]
+ *                  (fp32 only; for each local p the holders q are added in
+ *                  ascending order, the loopback call's order: deterministic).
+ *   Same-rank pairs are device copies/adds; other pairs are ncclSend/ncclRecv
+ *   (send rows gathered into a context-owned staging buffer; FORWARD receives
+ *   land directly in the contiguous halo rows).  The work runs on the comm
+ *   stream after everything enqueued on `stream`; unless flags has
+ *   DSMPNN_HALO_ASYNC, `stream` then waits for it.  With ASYNC the caller joins
+ *   later with dsmpnn_halo_wait(ctx, stream) (e.g. after the deep rows of the
+ *   next layer, which read no halo row, reading R23).  DSMPNN_HALO_VIA_NCCL
+ *   routes same-rank pairs through NCCL too (send/recv to self: exercises the
+ *   NCCL path on one GPU).  Both ranks of a pair derive the same message
+ *   sizes from their own plans; a mismatch is SHAPE.  Errors: INVALID_ARG
+ *   (bad parts, width, dtype), UNSUPPORTED (REVERSE_ADD of bf16), NCCL.
+ * dsmpnn_halo_schedule: the host-only op list that dsmpnn_halo_exchange
+ *   issues (no GPU needed; used by the multi-process CPU tests): kind LOCAL /
+ *   SEND / RECV, the peer rank, source and destination part, rows, and offset
+ *   (FORWARD: LOCAL/RECV = first halo row in the destination part, SEND = first
+ *   staging row; REVERSE_ADD: LOCAL/SEND = first halo row in the holder part
+ *   (src_part), RECV = first staging row).  Sends and receives between two
+ *   ranks are issued in this (global source, destination) order on both
+ *   sides, which is how NCCL matches them.  stage_rows = staging rows needed.
+ * dsmpnn_allreduce_sum_f32: in-place sum over the ranks (ncclAllReduce on `stream`).
+ * dsmpnn_ctx_sync: host watchdog: waits for the context's last exchange or
+ *   all-reduce; polls ncclCommGetAsyncError; after timeout_ms (< 0: no limit)
+ *   aborts the communicator and returns TIMEOUT (NCCL on an asynchronous
+ *   error).  An aborted context fails every later call with NCCL. */
+#define DSMPNN_UNIQUE_ID_BYTES 128
+typedef struct dsmpnn_ctx_s *dsmpnn_ctx;
+typedef enum { DSMPNN_HALO_FORWARD = 0, DSMPNN_HALO_REVERSE_ADD = 1 } dsmpnn_halo_dir;
+typedef enum { DSMPNN_HALO_ASYNC = 1, DSMPNN_HALO_VIA_NCCL = 2 } dsmpnn_halo_flags;
+typedef enum { DSMPNN_HALO_OP_LOCAL = 0, DSMPNN_HALO_OP_SEND = 1, DSMPNN_HALO_OP_RECV = 2 } dsmpnn_halo_op_kind;
+typedef struct {
+  int32_t kind, peer_rank, src_part, dst_part;
+  int64_t rows, offset;
+} dsmpnn_halo_op;
+
+dsmpnn_status dsmpnn_comm_unique_id(void *id /*host, DSMPNN_UNIQUE_ID_BYTES*/);
+dsmpnn_status dsmpnn_ctx_create(int32_t device, const void *unique_id /*host*/, int32_t rank, int32_t nranks,
+                                dsmpnn_ctx *ctx /*host out*/);
+dsmpnn_status dsmpnn_ctx_destroy(dsmpnn_ctx ctx);
+dsmpnn_status dsmpnn_ctx_info(dsmpnn_ctx ctx, int32_t *rank, int32_t *nranks, void **comm_stream);
+dsmpnn_status dsmpnn_halo_schedule(int32_t nparts, const int32_t *part_rank, int32_t my_rank, int32_t n_local,
+                                   const int32_t *local_parts, const int64_t *const *halo_ptr,
+                                   const int64_t *const *send_ptr, int32_t direction, int32_t flags,
+                                   dsmpnn_halo_op *ops /*host*/, int32_t capacity, int32_t *n_ops /*host*/,
+                                   int64_t *stage_rows /*host*/);
+dsmpnn_status dsmpnn_halo_exchange(dsmpnn_ctx ctx, int32_t nparts, const int32_t *part_rank, int32_t n_local,
+                                   const int32_t *local_parts, void *const *values, const int64_t *const *halo_ptr,
+                                   const int64_t *const *send_ptr, const int32_t *const *send_idx, int32_t width,
+                                   int32_t dtype, int32_t direction, int32_t flags, void *stream);
+dsmpnn_status dsmpnn_halo_wait(dsmpnn_ctx ctx, void *stream);
+dsmpnn_status dsmpnn_allreduce_sum_f32(dsmpnn_ctx ctx, float *buf, int64_t n, void *stream);
+dsmpnn_status dsmpnn_ctx_sync(dsmpnn_ctx ctx, int32_t timeout_ms);
+
 /* ----------------------------------------------------------- f4 --------- */
 /* Inference by sub-domain reassembly ("randomly selected
  * sub-domains ... sequentially fed into the trained model ... reassembled in
@@ -306,7 +395,8 @@ dsmpnn_status dsmpnn_gcn_bwd(int32_t d_in, int32_t d_out, int32_t act, const flo
  *   attribute: grad_u[j] += sum_{p in row j} grad_e[p] - sum_{p: col p = j}
  *   grad_e[p] (rows j < n_dst are destinations; CSC view from dsmpnn_csc).
  * mse: *sse += sum (pred - target)^2 (one block, fixed order) and, if grad is
- *   not NULL, grad = 2 (pred - target) * scale.
+ *   not NULL, grad = 2 (pred - target) * scale.  mse_mean: *loss = *sse / count
+ *   (device scalars; count = number of terms over all ranks).
  * sgd: w -= lr g (Alg. 1 :419).  adam: Adam with bias
  *   correction for step >= 1, m / v updated in place. */
 dsmpnn_status dsmpnn_mlp3_fwd(int32_t in_dim, int32_t hid, int32_t out_dim, const float *const *Wb, const float *x,
@@ -320,6 +410,7 @@ dsmpnn_status dsmpnn_edge_refresh_bwd(const float *grad_e, int32_t d_e, int32_t 
                                       int64_t n_dst, int64_t n_loc, float *grad_u, void *stream);
 dsmpnn_status dsmpnn_mse(const float *pred, const float *target, int64_t n_elems, float scale, float *grad,
                          float *sse, void *stream);
+dsmpnn_status dsmpnn_mse_mean(const float *sse, int64_t count, float *loss, void *stream);
 dsmpnn_status dsmpnn_sgd(float *w, const float *g, int64_t n, float lr, void *stream);
 dsmpnn_status dsmpnn_adam(float *w, const float *g, float *m, float *v, int64_t n, float lr, float beta1, float beta2,
                           float eps, int32_t step, void *stream);

@@ -19,8 +19,12 @@ ROOT_NONE, ROOT_IDENTITY, ROOT_DENSE = 0, 1, 2
 ACT_IDENTITY, ACT_RELU = 0, 1
 EDGE_DIFF, EDGE_CONCAT = 0, 1
 
-STATUS = {0: "OK", -1: "INVALID_ARG", -2: "SHAPE", -3: "INDEX", -4: "CAPACITY", -5: "CUDA",
-          -8: "UNSUPPORTED", -9: "DEGENERATE"}
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "SHAPE", -3: "INDEX", -4: "CAPACITY", -5: "CUDA", -6: "NCCL",
+          -7: "TIMEOUT", -8: "UNSUPPORTED", -9: "DEGENERATE"}
+HALO_FORWARD, HALO_REVERSE_ADD = 0, 1
+HALO_ASYNC, HALO_VIA_NCCL = 1, 2
+HALO_OP_LOCAL, HALO_OP_SEND, HALO_OP_RECV = 0, 1, 2
+UNIQUE_ID_BYTES = 128
 
 
 class DsmpnnError(RuntimeError):
@@ -56,6 +60,11 @@ class Grads(C.Structure):
     _fields_ = [("W1", P), ("b1", P), ("W2", P), ("b2", P), ("W3", P), ("b3", P), ("W_root", P), ("b", P)]
 
 
+class HaloOp(C.Structure):
+    _fields_ = [("kind", I32), ("peer_rank", I32), ("src_part", I32), ("dst_part", I32), ("rows", I64),
+                ("offset", I64)]
+
+
 def _sig(name, *args):
     f = getattr(_lib, "dsmpnn_" + name)
     f.restype = C.c_int
@@ -78,6 +87,7 @@ _f = {
     "partition": _sig("partition", P, P, I64, C.c_int, C.c_int, F, F, C.c_int, P, P, P, P, P, P, P, P, SZ, P),
     "partition_all": _sig("partition_all", P, P, I64, C.c_int, C.c_int, F, F, I32, P, P, P, P, P, P, P, SZ, P),
     "gather_rows": _sig("gather_rows", P, P, I64, I64, I32, P, P),
+    "gather_rows_bf16": _sig("gather_rows_bf16", P, P, I64, I64, P, P),
     "edge_features": _sig("edge_features", I32, P, C.c_int, P, C.c_int, P, P, I64, I64, P, P, P),
     "packed_weights_size": _sig("packed_weights_size", C.POINTER(LayerDesc), C.POINTER(SZ)),
     "pack_weights": _sig("pack_weights", C.POINTER(LayerDesc), C.POINTER(Weights), P, SZ, P),
@@ -104,9 +114,22 @@ _f = {
     "mlp3_bwd": _sig("mlp3_bwd", I32, I32, I32, C.POINTER(P), P, P, P, P, I64, P, C.POINTER(P), P, SZ, P),
     "edge_refresh_bwd": _sig("edge_refresh_bwd", P, I32, I32, I32, P, P, P, I64, I64, P, P),
     "mse": _sig("mse", P, P, I64, F, P, P, P),
+    "mse_mean": _sig("mse_mean", P, I64, P, P),
     "sgd": _sig("sgd", P, P, I64, F, P),
     "adam": _sig("adam", P, P, P, P, I64, F, F, F, F, I32, P),
     "gemm_bf16": _sig("gemm_bf16", I64, I64, I64, P, I64, I32, P, I64, I32, P, I64, I32, P, I32, P),
+    "comm_unique_id": _sig("comm_unique_id", P),
+    "ctx_create": _sig("ctx_create", I32, P, I32, I32, C.POINTER(P)),
+    "ctx_destroy": _sig("ctx_destroy", P),
+    "ctx_info": _sig("ctx_info", P, C.POINTER(I32), C.POINTER(I32), C.POINTER(P)),
+    "halo_schedule": _sig("halo_schedule", I32, C.POINTER(I32), I32, I32, C.POINTER(I32), C.POINTER(C.POINTER(I64)),
+                          C.POINTER(C.POINTER(I64)), I32, I32, C.POINTER(HaloOp), I32, C.POINTER(I32),
+                          C.POINTER(I64)),
+    "halo_exchange": _sig("halo_exchange", P, I32, C.POINTER(I32), I32, C.POINTER(I32), C.POINTER(P),
+                          C.POINTER(C.POINTER(I64)), C.POINTER(C.POINTER(I64)), C.POINTER(P), I32, I32, I32, I32, P),
+    "halo_wait": _sig("halo_wait", P, P),
+    "allreduce_sum_f32": _sig("allreduce_sum_f32", P, P, I64, P),
+    "ctx_sync": _sig("ctx_sync", P, I32),
     "probe_begin": _sig("probe_begin", I32, I32),
     "probe_end": _sig("probe_end", C.POINTER(F), C.POINTER(I64)),
 }
@@ -229,6 +252,15 @@ def gather_rows(inp, rows, out, stream=None):
     return out
 
 
+def gather_rows_bf16(inp, rows, out, stream=None):
+    """out[k] = bf16_rn(inp[rows[k]]) (inp float32, out bfloat16); rows None: k."""
+    assert inp.dtype == torch.float32 and out.dtype == torch.bfloat16
+    n_rows = rows.numel() if rows is not None else out.shape[0]
+    row_elems = inp[0].numel() if inp.dim() > 1 else 1
+    _call("gather_rows_bf16", _p(inp), _p(rows), n_rows, row_elems, _p(out), _stream(stream))
+    return out
+
+
 def edge_features(mode, coords, attr, row_ptr, col_idx, n_dst, e32=None, e16=None, stream=None):
     dim = coords.shape[1]
     n_attr = attr.shape[1] if attr is not None else 0
@@ -333,6 +365,84 @@ def halo_reverse_add_loopback(values_list, halo_ptr_list, send_ptr_list, send_id
     _call("halo_reverse_add_loopback", P_, vals, hpp, spp, sidx, width, _stream(stream))
 
 
+# ------------------------------------------------------- a6 over NCCL -----
+def _ptr_arrays(plans):
+    """host int64 arrays (kept alive by the returned tuple) and the pointer array"""
+    arrs = [(I64 * len(p))(*[int(x) for x in p]) for p in plans]
+    return arrs, (C.POINTER(I64) * max(1, len(arrs)))(*[C.cast(a, C.POINTER(I64)) for a in arrs])
+
+
+def halo_schedule(nparts, part_rank, my_rank, local_parts, halo_ptrs, send_ptrs, direction, flags=0):
+    """The op list dsmpnn_halo_exchange would issue on `my_rank` (host only,
+    no GPU): list of dicts (kind, peer_rank, src_part, dst_part, rows,
+    offset) and the staging rows."""
+    pr = (I32 * nparts)(*part_rank)
+    lp = (I32 * max(1, len(local_parts)))(*local_parts)
+    _ha, hpp = _ptr_arrays(halo_ptrs)
+    _sa, spp = _ptr_arrays(send_ptrs)
+    cap = 2 * nparts * nparts + 1
+    ops = (HaloOp * cap)()
+    n = I32(0)
+    stage = I64(0)
+    _call("halo_schedule", nparts, pr, my_rank, len(local_parts), lp, hpp, spp, direction, flags, ops, cap,
+          C.byref(n), C.byref(stage))
+    out = [{f: getattr(ops[i], f) for f, _ in HaloOp._fields_} for i in range(n.value)]
+    return out, int(stage.value)
+
+
+def comm_unique_id():
+    buf = (C.c_uint8 * UNIQUE_ID_BYTES)()
+    _call("comm_unique_id", C.cast(buf, P))
+    return bytes(buf)
+
+
+class Comm:
+    """An NCCL communicator context of the library (dsmpnn_ctx): halo
+    exchange between processes and the gradient sum (Alg. 1 :411, :418)."""
+
+    def __init__(self, device, unique_id, rank, nranks):
+        assert len(unique_id) == UNIQUE_ID_BYTES
+        self._uid = (C.c_uint8 * UNIQUE_ID_BYTES)(*unique_id)
+        self.h = P()
+        self.rank, self.nranks = rank, nranks
+        dev = device.index if isinstance(device, torch.device) else int(device)
+        _call("ctx_create", dev, C.cast(self._uid, P), rank, nranks, C.byref(self.h))
+
+    def close(self):
+        if self.h:
+            _f["ctx_destroy"](self.h)
+            self.h = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def halo_exchange(self, nparts, part_rank, local_parts, values, halo_ptrs, send_ptrs, send_idx, dtype,
+                      direction=0, flags=0, stream=None):
+        n = len(local_parts)
+        pr = (I32 * nparts)(*part_rank)
+        lp = (I32 * max(1, n))(*local_parts)
+        vals = (P * max(1, n))(*[v.data_ptr() for v in values])
+        _ha, hpp = _ptr_arrays(halo_ptrs)
+        _sa, spp = _ptr_arrays(send_ptrs)
+        sidx = (P * max(1, n))(*[s.data_ptr() if s.numel() else None for s in send_idx])
+        width = values[0].shape[1] if n else 1
+        _call("halo_exchange", self.h, nparts, pr, n, lp, vals, hpp, spp, sidx, width, dtype, direction, flags,
+              _stream(stream))
+
+    def halo_wait(self, stream=None):
+        _call("halo_wait", self.h, _stream(stream))
+
+    def allreduce_sum_f32(self, t, stream=None):
+        assert t.dtype == torch.float32 and t.is_contiguous()
+        _call("allreduce_sum_f32", self.h, _p(t), t.numel(), _stream(stream))
+
+    def sync(self, timeout_ms=-1):
+        _call("ctx_sync", self.h, int(timeout_ms))
+
+
 def reassemble_accumulate(pred, gid, sum_, count, stream=None):
     """sum_[gid[k]] += pred[k]; count[gid[k]] += 1 (f4)."""
     _call("reassemble_accumulate", _p(pred), _p(gid), pred.shape[0], pred.shape[1], _p(sum_), _p(count),
@@ -390,6 +500,10 @@ def edge_refresh_bwd(grad_e, off, width, row_ptr, csc_perm, csc_ptr, n_dst, n_lo
 
 def mse(pred, target, scale, grad, sse, stream=None):
     _call("mse", _p(pred), _p(target), pred.numel(), float(scale), _p(grad), _p(sse), _stream(stream))
+
+
+def mse_mean(sse, count, loss, stream=None):
+    _call("mse_mean", _p(sse), int(count), _p(loss), _stream(stream))
 
 
 def sgd(w, g, lr, stream=None):

@@ -8,7 +8,8 @@ encoder/decoder and the optimiser are outside the hot path.
 
 A process owns one or more sub-domains ("virtual ranks"); halos between
 sub-domains on the same device are device copies, halos between processes go
-through torch.distributed (NCCL) point-to-point.  Gradients through halo
+through the library's NCCL context (dsmpnn_halo_exchange, dsmpnn_allreduce_sum_f32);
+torch.distributed only distributes the communicator id.  Gradients through halo
 rows (reading R16): DETACH (default, the paper's local backprop) drops them;
 REVERSE_ADD adds them to the owning rows after every
 layer's backward, which makes the decomposed gradient equal the
@@ -48,6 +49,8 @@ class StepConfig:
     grad_mode: int = DETACH
     overlap_halo: int = -1  # 1: deep rows of a layer run while the previous halo refresh is in flight; -1: when world > 1
     streams: int = 2  # CUDA streams the local sub-domains' layer work is spread over (1: one stream)
+    halo: int = 1  # 0: skip the per-layer halo refresh (bench --no-comm: measures the exposed exchange time)
+    halo_flags: int = 0  # extra dsmpnn_halo_exchange flags (L.HALO_VIA_NCCL: same-process pairs through NCCL too)
 
 
 def parts_of_process(nparts, world, rank):
@@ -56,10 +59,27 @@ def parts_of_process(nparts, world, rank):
     return list(range(rank * per, (rank + 1) * per))
 
 
+def make_comm(device, rank, world, group=None):
+    """The library's NCCL context for this process: rank 0 creates the
+    communicator id, torch.distributed broadcasts it (the only thing torch
+    carries), every rank joins (collective)."""
+    import torch.distributed as dist
+    uid = [L.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0, group=group)
+    return L.Comm(device, uid[0], rank, world)
+
+
 class HotPath:
-    def __init__(self, cfg: StepConfig, weights: dict, device, rank=0, world=1, group=None):
+    def __init__(self, cfg: StepConfig, weights: dict, device, rank=0, world=1, group=None, comm=None):
+        """comm: the library NCCL context (make_comm); created here when
+        world > 1 and none is given.  With world == 1 and no comm, halos are
+        device copies (dsmpnn_halo_exchange_loopback)."""
         assert cfg.nparts % world == 0, "sub-domain count must be a multiple of the process count"
         self.cfg, self.dev, self.rank, self.world, self.group = cfg, device, rank, world, group
+        if comm is None and world > 1:
+            comm = make_comm(device, rank, world, group)
+        self.comm = comm
         self.my_parts = parts_of_process(cfg.nparts, world, rank)
         self.proc_of = [p // (cfg.nparts // world) for p in range(cfg.nparts)]
         d_e = (cfg.dim + cfg.n_attr) * (1 if cfg.edge_mode == L.EDGE_DIFF else 2)
@@ -123,20 +143,44 @@ class HotPath:
             self._comm = torch.cuda.Stream(self.dev)
         return self._comm
 
-    def halo(self, vals, dtype, stream=None):
-        """Overlap update (Alg. 1) for every local sub-domain."""
-        if self.world == 1:
+    def halo(self, vals, dtype, stream=None, flags=0):
+        """Overlap update (Alg. 1) for every local sub-domain: the
+        library's NCCL exchange when a communicator exists, else device
+        copies among the sub-domains of this device."""
+        if not self.cfg.halo:
+            return
+        if self.comm is None:
             pipeline.halo_exchange_loopback(self.subs, vals, dtype, stream=stream)
         else:
-            pipeline.halo_exchange_mixed(self.subs, vals, dtype, self.proc_of, self.rank, self.group,
-                                         stream=stream)
+            pipeline.halo_exchange_comm(self.comm, self.subs, vals, dtype, self.proc_of, L.HALO_FORWARD,
+                                        flags | self.cfg.halo_flags, stream=stream)
 
     def halo_reverse(self, grads):
         """REVERSE_ADD of fp32 gradients (f2) for every local sub-domain."""
-        if self.world == 1:
+        if self.comm is None:
             pipeline.halo_reverse_loopback(self.subs, grads)
         else:
-            pipeline.halo_reverse_mixed(self.subs, grads, self.proc_of, self.rank, self.group)
+            pipeline.halo_exchange_comm(self.comm, self.subs, grads, L.F32, self.proc_of, L.HALO_REVERSE_ADD,
+                                        self.cfg.halo_flags)
+
+    def _halo_async(self, vals, dtype, main, side):
+        """Start the refresh of `vals` behind the work enqueued on `main`;
+        returns a callable that makes `main` wait for it.  With the library
+        communicator the exchange runs on its own comm stream
+        (DSMPNN_HALO_ASYNC + dsmpnn_halo_wait); the loopback path uses `side`."""
+        if self.comm is not None:
+            self.halo(vals, dtype, flags=L.HALO_ASYNC)
+            return lambda: self.comm.halo_wait(main)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
+        for t in vals:
+            t.record_stream(side)
+        with torch.cuda.stream(side):
+            self.halo(vals, dtype, stream=side)
+        done = torch.cuda.Event()
+        done.record(side)
+        return lambda: main.wait_event(done)
 
     def forward(self, v0):
         """L layers forward (Alg. 1 :404-411) with a halo refresh after each.
@@ -149,13 +193,16 @@ class HotPath:
         # layer-0 inputs of every sub-domain (local order)
         vals = []
         for sd in self.subs:
-            v = torch.empty((sd.n_loc, c.d), dtype=torch.float32, device=self.dev)
-            L.gather_rows(v0, sd.local_rows, v)
-            vals.append(v.to(vdt) if lowp else v)
+            v = torch.empty((sd.n_loc, c.d), dtype=vdt, device=self.dev)
+            if lowp:  # bf16 operand rounding inside the library
+                L.gather_rows_bf16(v0, sd.local_rows, v)
+            else:
+                L.gather_rows(v0, sd.local_rows, v)
+            vals.append(v)
         acts = [vals]
         overlap = c.overlap_halo == 1 or (c.overlap_halo < 0 and self.world > 1)
         main = torch.cuda.current_stream(self.dev)
-        comm = self._comm_stream() if overlap else None
+        comm = self._comm_stream() if overlap and self.comm is None else None
         ex_done = None
 
         def run(layer, q, sd, out, nv, a, b):
@@ -200,22 +247,14 @@ class HotPath:
                 for q, sd in enumerate(self.subs):
                     run(layer, q, sd, outs_l[q], nxt[q], 0, sd.n_deep)
                 if ex_done is not None:
-                    main.wait_event(ex_done)
+                    ex_done()
                 for q, sd in enumerate(self.subs):
                     run(layer, q, sd, outs_l[q], nxt[q], sd.n_deep, sd.n_own)
                 # only near rows are sent (R23): the refresh can start now
-                ready = torch.cuda.Event()
-                ready.record(main)
-                comm.wait_event(ready)
-                for t in nxt:
-                    t.record_stream(comm)
-                with torch.cuda.stream(comm):
-                    self.halo(nxt, L.BF16 if lowp else L.F32, stream=comm)
-                ex_done = torch.cuda.Event()
-                ex_done.record(comm)
+                ex_done = self._halo_async(nxt, L.BF16 if lowp else L.F32, main, comm)
             acts.append(nxt)
         if ex_done is not None:
-            main.wait_event(ex_done)
+            ex_done()
         outs = [self.ws[("out", q)].view(torch.float32)[: sd.n_own * c.d].view(sd.n_own, c.d)
                 for q, sd in enumerate(self.subs)]
         return acts, outs
@@ -300,10 +339,10 @@ class HotPath:
         return self._acc[k]
 
     def _allreduce_grads(self):
-        """Gradient sum over processes (Alg. 1), one NCCL all-reduce."""
-        import torch.distributed as dist
+        """Gradient sum over processes (Alg. 1): one all-reduce of
+        the flattened gradients through the library communicator."""
         flat = torch.cat([self.grads[n].reshape(-1) for n in GNAMES])
-        dist.all_reduce(flat, group=self.group)
+        self.comm.allreduce_sum_f32(flat)
         off = 0
         for n in GNAMES:
             m = self.grads[n].numel()
@@ -335,9 +374,10 @@ class HotPath:
         finally:
             self.cfg = c0
         if self.world > 1:  # each process holds some sub-domains of every pass
-            import torch.distributed as dist
-            dist.all_reduce(acc, group=self.group)
-            dist.all_reduce(cnt, group=self.group)
+            self.comm.allreduce_sum_f32(acc)
+            cntf = cnt.to(torch.float32)  # counts <= len(seeds): exact in fp32
+            self.comm.allreduce_sum_f32(cntf)
+            cnt.copy_(cntf.round().to(torch.int32))
         field = torch.empty_like(acc)
         L.reassemble_finalize(acc, cnt, field)
         return field, cnt
@@ -365,13 +405,13 @@ class TrainStep:
     CONV = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
 
     def __init__(self, cfg: StepConfig, params: dict, hops: int, device, rank=0, world=1, group=None,
-                 optimizer="sgd", lr=1e-3):
+                 optimizer="sgd", lr=1e-3, comm=None):
         import dataclasses
         assert cfg.dtype == L.F32, "the training step runs in F32 mode"
         cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops)
         conv = dict(params["conv"])
         conv.setdefault("W_root", np.zeros((cfg.d, cfg.d), np.float32))  # identity root: unused
-        self.hp = HotPath(cfg, conv, device, rank, world, group)
+        self.hp = HotPath(cfg, conv, device, rank, world, group, comm=comm)
         self.dev, self.hops, self.opt, self.lr = device, hops, optimizer, lr
         T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32).to(device)
         self.enc = [T(x) for Wl, bl in params["enc"] for x in (Wl, bl)]
@@ -438,9 +478,8 @@ class TrainStep:
         # loss: MSE of the last decoded values on owned rows, over all ranks
         count = sum(sd.n_own for sd in subs) * n_attr
         if hp.world > 1:
-            import torch.distributed as dist
-            ct = torch.tensor([float(count)], dtype=torch.float64, device=self.dev)
-            dist.all_reduce(ct, group=hp.group)
+            ct = torch.tensor([float(count)], dtype=torch.float32, device=self.dev)  # < 2^24 rows: exact
+            hp.comm.allreduce_sum_f32(ct)
             count = int(ct.item())
         sse = torch.zeros(1, device=self.dev)
         du = []
@@ -485,15 +524,16 @@ class TrainStep:
             x_, h1, h2 = enc_cache[q]
             L.mlp3_bwd(self.enc, x_, h1, h2, dvL_in[q], None, self.g_enc)
         if hp.world > 1:
-            import torch.distributed as dist
             flat = torch.cat([t.reshape(-1) for t in self.g_enc + self.g_dec + [hp.grads[n] for n in self.CONV]]
                              + [sse])
-            dist.all_reduce(flat, group=hp.group)
+            hp.comm.allreduce_sum_f32(flat)
             off = 0
             for t in self.g_enc + self.g_dec + [hp.grads[n] for n in self.CONV] + [sse]:
                 t.copy_(flat[off:off + t.numel()].view_as(t))
                 off += t.numel()
-        loss = float(sse.item()) / count
+        loss_t = torch.empty(1, dtype=torch.float32, device=self.dev)
+        L.mse_mean(sse, count, loss_t)
+        loss = float(loss_t.item())
         return loss, dict(enc=self.g_enc, dec=self.g_dec, conv=hp.grads)
 
     def _params(self):

@@ -9,7 +9,24 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdsmpnn.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu", "train.cu"]
+
+def _nccl_dir():
+    """The NCCL that torch loads (the venv's nvidia-nccl wheel, 2.28): the
+    library links it by soname, so one copy is mapped per process."""
+    try:
+        import nvidia.nccl as nn
+        d = os.path.dirname(nn.__file__) if nn.__file__ else list(nn.__path__)[0]
+    except ImportError:
+        return None
+    return d if os.path.exists(os.path.join(d, "include", "nccl.h")) else None
+
+
+NCCL = _nccl_dir()
+NCCL_INC = ["-I", os.path.join(NCCL, "include")] if NCCL else []
+NCCL_LINK = (["-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
+             if NCCL else ["-lnccl"])
+
+SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu", "train.cu", "comm.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]
@@ -33,7 +50,7 @@ def build(force=False, verbose=False):
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     for src in SOURCES:
         obj = os.path.join(HERE, "build", src.replace(".cu", ".o"))
-        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj, "-I", CSRC] + [f for f in FLAGS if f != "-shared"]
+        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj, "-I", CSRC] + NCCL_INC + [f for f in FLAGS if f != "-shared"]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -49,7 +66,7 @@ def build(force=False, verbose=False):
         for src, out in failed:
             sys.stderr.write(f"--- nvcc failed on {src}\n{out}\n")
         raise RuntimeError("libdsmpnn build failed: " + ", ".join(s for s, _ in failed))
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + ["-lcudart", "-lcuda"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB] + objs + NCCL_LINK + ["-lcudart", "-lcuda"]
     subprocess.run(cmd, check=True)
     return LIB
 

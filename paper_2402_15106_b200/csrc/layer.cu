@@ -11,6 +11,9 @@
 // This file holds the API entry points, the fp32 (F32 mode) kernels and the
 // shared node-level epilogues.  The bf16 tcgen05 kernels live in
 // layer_bf16.cu.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "layer_bf16.cuh"
 #include "simt.cuh"
@@ -265,6 +268,66 @@ static dsmpnn_status edge_range(const int64_t *row_ptr, const int64_t *row_ptr_h
   return DSMPNN_OK;
 }
 
+// ------------------------------------------------------- CSR validation ----
+// BF16 edge tiles hold whole destination rows of at most kMaxRowEdgesBf16
+// edges (edge_fwd2.cuh walk_tile); a longer row is UNSUPPORTED, checked here
+// before any launch.  With DSMPNN_DEBUG set in the environment, every call
+// also validates the CSR (row_ptr non-decreasing, 0 <= col < n_loc) and
+// returns ERR_INDEX instead of reading out of bounds.
+constexpr int kMaxRowEdgesBf16 = 128;
+
+// flags[0] = max degree of rows [rb, re); flags[1] = number of bad entries
+__global__ void csr_scan_kernel(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rb,
+                                int64_t re, int64_t n_loc, int check_cols, int *flags) {
+  int mx = 0, bad = 0;
+  for (int64_t i = rb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < re; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = row_ptr[i], b = row_ptr[i + 1];
+    if (b < a) { ++bad; continue; }
+    const int64_t dg = b - a;
+    mx = max(mx, dg > (1 << 30) ? (1 << 30) : (int)dg);
+    if (check_cols)
+      for (int64_t p = a; p < b; ++p) {
+        const int32_t j = col[p];
+        bad += (j < 0 || (n_loc >= 0 && j >= n_loc));
+      }
+  }
+  if (mx) atomicMax(&flags[0], mx);
+  if (bad) atomicAdd(&flags[1], bad);
+}
+
+static bool debug_checks() {
+  static const bool on = getenv("DSMPNN_DEBUG") != nullptr;
+  return on;
+}
+
+static dsmpnn_status check_rows(const dsmpnn_layer_desc &d, const int64_t *row_ptr, const int64_t *row_ptr_host,
+                                const int32_t *col, int64_t rb, int64_t re, int64_t n_loc, cudaStream_t s) {
+  const bool dbg = debug_checks();
+  const bool need_deg = d.dtype == DSMPNN_BF16;
+  if (!dbg && !need_deg) return DSMPNN_OK;
+  int64_t maxdeg = 0;
+  if (row_ptr_host && !dbg) {
+    for (int64_t i = rb; i < re; ++i) maxdeg = std::max<int64_t>(maxdeg, row_ptr_host[i + 1] - row_ptr_host[i]);
+  } else {
+    int *flags = nullptr, h[2] = {0, 0};
+    DS_CUDA(cudaMallocAsync((void **)&flags, 2 * sizeof(int), s));
+    DS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(re - rb, 256), kNumSMs * 4));
+    csr_scan_kernel<<<blocks, 256, 0, s>>>(row_ptr, col, rb, re, n_loc, dbg ? 1 : 0, flags);
+    DS_LAUNCH_CHECK();
+    DS_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
+    DS_CUDA(cudaFreeAsync(flags, s));
+    DS_CUDA(cudaStreamSynchronize(s));
+    DS_CHECK_ARG(h[1] == 0, DSMPNN_ERR_INDEX, "layer: CSR has %d invalid entries (row_ptr decreasing or col out of "
+                 "range) in rows [%lld, %lld)", h[1], (long long)rb, (long long)re);
+    maxdeg = h[0];
+  }
+  DS_CHECK_ARG(!need_deg || maxdeg <= kMaxRowEdgesBf16, DSMPNN_ERR_UNSUPPORTED,
+               "layer BF16: a destination row has %lld edges; the fused edge kernels take rows of at most %d "
+               "edges (cap the graph with n_e <= %d)", (long long)maxdeg, kMaxRowEdgesBf16, kMaxRowEdgesBf16);
+  return DSMPNN_OK;
+}
+
 // ------------------------------------------------------------ F32 fwd ----
 static dsmpnn_status fwd_f32(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, const float *v, const float *e,
                              const int64_t *row_ptr, const int32_t *col, int64_t n_dst, int64_t E, int64_t rb,
@@ -465,6 +528,7 @@ dsmpnn_status dsmpnn_layer_fwd(const dsmpnn_layer_desc *desc, const dsmpnn_weigh
   cudaStream_t s = as_stream(stream);
   if (row_end == row_begin) return DSMPNN_OK;
   int64_t eb, ee, E;
+  DS_TRY(check_rows(*desc, row_ptr, row_ptr_host, col_idx, row_begin, row_end, -1, s));
   DS_TRY(edge_range(row_ptr, row_ptr_host, row_begin, row_end, &eb, &ee, s));
   if (row_ptr_host) E = row_ptr_host[n_dst];
   else {
@@ -496,6 +560,7 @@ dsmpnn_status dsmpnn_layer_bwd(const dsmpnn_layer_desc *desc, const dsmpnn_weigh
   cudaStream_t s = as_stream(stream);
   if (row_end == row_begin) return DSMPNN_OK;
   int64_t eb, ee, E;
+  DS_TRY(check_rows(*desc, row_ptr, row_ptr_host, col_idx, row_begin, row_end, n_loc, s));
   DS_TRY(edge_range(row_ptr, row_ptr_host, row_begin, row_end, &eb, &ee, s));
   if (row_ptr_host) E = row_ptr_host[n_dst];
   else {

@@ -315,11 +315,8 @@ static dsmpnn_status launch_dz1w1(const Packed &pw, const __nv_bfloat16 *dZ2, co
   DS_TRY(make_tmap_bf16(&tW1, pw.W1, 16, KH, 16, 16, 128));
   DS_TRY(make_tmap_bf16(&tDZ, dZ2, KH, nE, KH, 64, 128));
   DS_TRY(make_tmap_bf16(&tE, e, 16, nE, 16, 16, 128));
-  static bool attr_set = false;
-  if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(dz1w1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZ1C::SMEM));
-    attr_set = true;
-  }
+  // set on every launch: the attribute belongs to the current device's context
+  DS_CUDA(cudaFuncSetAttribute(dz1w1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DZ1C::SMEM));
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
   {
     ProbeScope probe(DSMPNN_PROBE_BF16_DZ1W1, s);
@@ -340,11 +337,8 @@ static dsmpnn_status launch_dw2(const Packed &pw, const __nv_bfloat16 *dZ2, cons
   DS_TRY(make_tmap_bf16(&tW1, pw.W1, 16, KH, 16, 16, 128));
   DS_TRY(make_tmap_bf16(&tDZ, dZ2, KH, nE, KH, 64, 128));
   DS_TRY(make_tmap_bf16(&tE, e, 16, nE, 16, 16, 128));
-  static bool attr_set = false;
-  if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(dw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DW2C::SMEM));
-    attr_set = true;
-  }
+  // set on every launch: the attribute belongs to the current device's context
+  DS_CUDA(cudaFuncSetAttribute(dw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DW2C::SMEM));
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
   {
     ProbeScope probe(DSMPNN_PROBE_BF16_DW2, s);

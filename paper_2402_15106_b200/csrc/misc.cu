@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "halo.cuh"
 
 namespace dsmpnn {
 
@@ -28,6 +29,16 @@ __global__ void gather_rows_kernel(const T *__restrict__ in, const int64_t *__re
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = t / row_elems, c = t - r * row_elems;
     out[t] = in[rows[r] * row_elems + c];
+  }
+}
+
+// fp32 rows -> bf16 rows (round to nearest even): the BF16 mode's layer-0 operand
+__global__ void gather_rows_bf16_kernel(const float *__restrict__ in, const int64_t *__restrict__ rows,
+                                        int64_t n_rows, int64_t row_elems, __nv_bfloat16 *__restrict__ out) {
+  int64_t total = n_rows * row_elems;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / row_elems, c = t - r * row_elems;
+    out[t] = __float2bfloat16_rn(in[(rows ? rows[r] : r) * row_elems + c]);
   }
 }
 
@@ -104,27 +115,6 @@ __global__ void halo_gather_kernel(const T *__restrict__ v, const int32_t *__res
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = t / width, c = t - r * width;
     out[t] = v[(int64_t)rows[r] * width + c];
-  }
-}
-
-// all same-device halo copies of one refresh in one launch: job j = blockIdx.y
-// copies rows src[rows[r]] -> dst[r] of `row16` 16-byte chunks each
-struct HaloJobs {
-  static constexpr int kMax = 64;
-  const uint4 *src[kMax];
-  const int32_t *rows[kMax];
-  uint4 *dst[kMax];
-  int64_t n_rows[kMax];
-};
-__global__ void halo_gather_jobs_kernel(const __grid_constant__ HaloJobs jobs, int row16) {
-  const int j = blockIdx.y;
-  const int64_t total = jobs.n_rows[j] * row16;
-  const uint4 *__restrict__ src = jobs.src[j];
-  const int32_t *__restrict__ rows = jobs.rows[j];
-  uint4 *__restrict__ dst = jobs.dst[j];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t / row16, c = t - r * row16;
-    dst[t] = src[(int64_t)rows[r] * row16 + c];
   }
 }
 
@@ -250,6 +240,16 @@ dsmpnn_status dsmpnn_gather_rows(const void *in, const int64_t *rows, int64_t n_
     gather_rows_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t *)in, rows, n_rows, row_elems, (uint16_t *)out);
   else
     DS_CHECK_ARG(false, DSMPNN_ERR_INVALID_ARG, "gather_rows: elem_bytes must be 2, 4 or 8");
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
+dsmpnn_status dsmpnn_gather_rows_bf16(const float *in, const int64_t *rows, int64_t n_rows, int64_t row_elems,
+                                      void *out, void *stream) {
+  DS_CHECK_ARG(n_rows >= 0 && row_elems >= 0, DSMPNN_ERR_INVALID_ARG, "gather_rows_bf16: negative size");
+  if (n_rows == 0 || row_elems == 0) return DSMPNN_OK;
+  gather_rows_bf16_kernel<<<grid_for(n_rows * row_elems), 256, 0, as_stream(stream)>>>(in, rows, n_rows, row_elems,
+                                                                                     (__nv_bfloat16 *)out);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

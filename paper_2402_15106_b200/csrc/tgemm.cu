@@ -373,11 +373,8 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (!B_MN) DS_TRY(make_tmap_bf16(&tb, a.B, a.K, a.N, a.ldb, 64, BN));
   else DS_TRY(make_tmap_bf16(&tb, a.B, a.N, a.K, a.ldb, T::B_INNER, 64));
   auto kern = tgemm_kernel<BN, A_MN, B_MN, E16, BRES>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
-    attr_set = true;
-  }
+  // set on every launch: the attribute belongs to the current device's context
+  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
   int64_t nkb = (a.K + 63) / 64;
   int splits = a.splits < 1 ? 1 : a.splits;
   int kbps = (int)ceil_div(nkb, splits);

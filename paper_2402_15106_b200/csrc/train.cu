@@ -182,6 +182,17 @@ dsmpnn_status dsmpnn_mse(const float *pred, const float *target, int64_t n_elems
   return DSMPNN_OK;
 }
 
+__global__ void mse_mean_kernel(const float *__restrict__ sse, double count, float *__restrict__ loss) {
+  loss[0] = (float)((double)sse[0] / count);
+}
+
+dsmpnn_status dsmpnn_mse_mean(const float *sse, int64_t count, float *loss, void *stream) {
+  DS_CHECK_ARG(sse && loss && count > 0, DSMPNN_ERR_INVALID_ARG, "mse_mean: arguments");
+  mse_mean_kernel<<<1, 1, 0, as_stream(stream)>>>(sse, (double)count, loss);
+  DS_LAUNCH_CHECK();
+  return DSMPNN_OK;
+}
+
 dsmpnn_status dsmpnn_sgd(float *w, const float *g, int64_t n, float lr, void *stream) {
   DS_CHECK_ARG(n >= 0, DSMPNN_ERR_INVALID_ARG, "sgd: n");
   if (n == 0) return DSMPNN_OK;

@@ -182,102 +182,11 @@ def halo_reverse_loopback(subs, grads):
                                 [s.send_idx for s in subs])
 
 
-def halo_reverse_mixed(subs, grads, proc_of, my_proc, group=None, scatter_add=None):
-    """REVERSE_ADD when sub-domains are spread over processes: the halo slice
-    of q received from p is sent back to p's process (NCCL send/recv, issued in
-    (destination, source) order on both sides), then every owner adds the
-    slices into its send rows with q ascending (the oracle's order).  fp32.
-    `scatter_add(inp, rows, values)` defaults to the library kernel."""
-    import torch.distributed as dist
-    if scatter_add is None:
-        scatter_add = L.halo_scatter_add
-    local = {sd.rank: (sd, g) for sd, g in zip(subs, grads)}
-    nparts = subs[0].nparts
-    ops, recv = [], {}
-    for p_id in range(nparts):          # owner of the rows
-        for q_id in range(nparts):      # holder of the halo copy
-            if p_id == q_id:
-                continue
-            own_local, halo_local = p_id in local, q_id in local
-            if own_local and not halo_local:
-                psd, _ = local[p_id]
-                s0, s1 = psd.send_ptr[q_id], psd.send_ptr[q_id + 1]
-                if s1 > s0:
-                    buf = torch.empty((s1 - s0, grads[0].shape[1]), dtype=torch.float32, device=grads[0].device)
-                    recv[(p_id, q_id)] = buf
-                    ops.append(dist.P2POp(dist.irecv, buf, proc_of[q_id], group))
-            elif halo_local and not own_local:
-                qsd, qg = local[q_id]
-                a, b = qsd.halo_ptr[p_id], qsd.halo_ptr[p_id + 1]
-                if b > a:
-                    ops.append(dist.P2POp(dist.isend, qg[a:b].contiguous(), proc_of[p_id], group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    for p_id in range(nparts):
-        if p_id not in local:
-            continue
-        psd, pg = local[p_id]
-        for q_id in range(nparts):
-            if q_id == p_id:
-                continue
-            s0, s1 = psd.send_ptr[q_id], psd.send_ptr[q_id + 1]
-            if s1 <= s0:
-                continue
-            if q_id in local:
-                qsd, qg = local[q_id]
-                a, b = qsd.halo_ptr[p_id], qsd.halo_ptr[p_id + 1]
-                src = qg[a:b]
-            else:
-                src = recv[(p_id, q_id)]
-            scatter_add(src, psd.send_idx[s0:s1], pg)
-
-
-def halo_exchange_mixed(subs, values, dtype, proc_of, my_proc, group=None, gather=None, stream=None):
-    """FORWARD halo refresh when sub-domains are spread over processes.
-
-    subs/values: this process's sub-domains and their [n_loc x width] arrays.
-    proc_of[p]: process holding sub-domain p.  A peer on the same process is a
-    device gather straight into the halo slice; a peer on another process is
-    a contiguous send buffer + NCCL send/recv (torch.distributed
-    batch_isend_irecv).  Receive slices are contiguous halo rows, so they land
-    in place.  Messages between two processes are issued in (source
-    sub-domain, destination sub-domain) order on both sides, which is how
-    NCCL matches them.  `gather(values, rows, out)` defaults to the library's
-    halo gather kernel."""
-    import torch.distributed as dist
-    if gather is None:
-        def gather(vals, rows, out):
-            L.halo_gather(vals, rows, out, dtype, stream=stream)
-    local = {sd.rank: (sd, v) for sd, v in zip(subs, values)}
-    nparts = subs[0].nparts
-    ops = []
-    keep = []
-    for s_id in range(nparts):
-        for t_id in range(nparts):
-            if s_id == t_id:
-                continue
-            src_local, dst_local = s_id in local, t_id in local
-            if src_local and dst_local:
-                ssd, sv = local[s_id]
-                tsd, tv = local[t_id]
-                s0, s1 = ssd.send_ptr[t_id], ssd.send_ptr[t_id + 1]
-                a, b = tsd.halo_ptr[s_id], tsd.halo_ptr[s_id + 1]
-                if b > a:
-                    gather(sv, ssd.send_idx[s0:s1], tv[a:b])
-            elif src_local:
-                ssd, sv = local[s_id]
-                s0, s1 = ssd.send_ptr[t_id], ssd.send_ptr[t_id + 1]
-                if s1 > s0:
-                    buf = torch.empty((s1 - s0, sv.shape[1]), dtype=sv.dtype, device=sv.device)
-                    gather(sv, ssd.send_idx[s0:s1], buf)
-                    keep.append(buf)
-                    ops.append(dist.P2POp(dist.isend, buf, proc_of[t_id], group))
-            elif dst_local:
-                tsd, tv = local[t_id]
-                a, b = tsd.halo_ptr[s_id], tsd.halo_ptr[s_id + 1]
-                if b > a:
-                    ops.append(dist.P2POp(dist.irecv, tv[a:b], proc_of[s_id], group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+def halo_exchange_comm(comm, subs, values, dtype, proc_of, direction, flags=0, stream=None):
+    """Halo refresh (FORWARD) or gradient return (REVERSE_ADD, fp32) of this
+    process's sub-domains through the library's NCCL context
+    (dsmpnn_halo_exchange): same-process pairs are device copies, the others
+    ncclSend/ncclRecv; proc_of[p] is the process holding sub-domain p."""
+    comm.halo_exchange(subs[0].nparts, proc_of, [sd.rank for sd in subs], values, [sd.halo_ptr for sd in subs],
+                       [sd.send_ptr for sd in subs], [sd.send_idx for sd in subs], dtype, direction, flags,
+                       stream=stream)

@@ -28,9 +28,10 @@ def lib_path():
 
 def test_header_declares_the_six_calls():
     d = _declared()
+    # the north_star's six calls, plus the communicator context the exchange runs on
     for name in ("dsmpnn_sample", "dsmpnn_radius_graph", "dsmpnn_partition", "dsmpnn_layer_fwd",
-                 "dsmpnn_layer_bwd", "dsmpnn_halo_exchange_loopback", "dsmpnn_halo_gather",
-                 "dsmpnn_halo_scatter_add"):
+                 "dsmpnn_layer_bwd", "dsmpnn_halo_exchange", "dsmpnn_ctx_create", "dsmpnn_ctx_destroy",
+                 "dsmpnn_comm_unique_id", "dsmpnn_allreduce_sum_f32", "dsmpnn_ctx_sync"):
         assert name in d
 
 
@@ -57,6 +58,13 @@ def test_error_path_without_gpu(lib_path):
     with pytest.raises(_lib.DsmpnnError) as ei:
         _lib._call("layer_workspace_size", ctypes.byref(d), 10, 10, ctypes.byref(sz))
     assert ei.value.status == -2
+
+
+def test_library_links_nccl(lib_path):
+    # the halo exchange is NCCL inside the library, not torch.distributed
+    import subprocess
+    out = subprocess.run(["ldd", lib_path], capture_output=True, text=True).stdout
+    assert "libnccl.so" in out, out
 
 
 def test_no_oracle_import_in_product():

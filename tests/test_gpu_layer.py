@@ -300,3 +300,7 @@ def test_fwd_bf16_darcy_full_size_sampled(L):
     v, e16, W16 = _to_dtype_inputs(p, 1)
     ref, _ = layer.layer_fwd(LayerDesc(3, cfg.d, cfg.d, cfg.k, 2, 1, "bf16"), W16, v, e16, rp, col, rows=rows)
     assert nerr(got["out"][rows], ref) <= TOL[1]
+    # and against the plain fp64 definition (no operand or activation rounding):
+    # the BF16 mode's whole rounding budget is inside the same 2e-2 bar
+    plain, _ = layer.layer_fwd(LayerDesc(3, cfg.d, cfg.d, cfg.k, 2, 1, "none"), W, p["v"], e, rp, col, rows=rows)
+    assert nerr(got["out"][rows], plain) <= TOL[1]

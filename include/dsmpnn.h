@@ -202,7 +202,8 @@ dsmpnn_status dsmpnn_pack_weights(const dsmpnn_layer_desc *desc, const dsmpnn_we
  *   out_lowp bf16[n_dst x d_out] copy of out, or NULL
  *   ws       saved activations for dsmpnn_layer_bwd, sized by
  *            dsmpnn_layer_workspace_size(desc, n_dst, E); pass the same ws to bwd.
- * Errors: SHAPE for ROOT_IDENTITY with d_in != d_out or BF16 with d_e > 16;
+ * Errors: SHAPE for ROOT_IDENTITY with d_in != d_out or BF16 with d_e > 13 (the
+ * padded edge columns 13..15 carry the first kappa layer bias, layer_bf16.cu);
  * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64} and k = 256,
  * and for a BF16 call whose rows [row_begin, row_end) include a row of more
  * than 128 edges (the fused edge kernels tile whole rows; checked on the host

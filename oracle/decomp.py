@@ -9,6 +9,14 @@ overlap from the neighbours' interiors after every hop.  Used by tests to pin
 import numpy as np
 
 from . import features, graph, halo, layer, partition, sample
+from .precision import round_bf16
+
+
+def _layer_input(desc, v):
+    """The value a layer consumes: in the BF16 mode (act_round="bf16") every
+    layer's input v is a bf16 operand (reading R18: the layer
+    output is stored as the next layer's bf16 operand), else v itself."""
+    return round_bf16(v) if desc.act_round == "bf16" else v
 
 
 def build_local(coords, gid, attr, nparts, overlap_l, r, n_e, seed, edge_mode):
@@ -33,6 +41,7 @@ def ds_forward(desc, W, ranks, v_global_rows, n_layers):
     vals = [np.asarray(v_global_rows(q["local_rows"]), dtype=np.float64) for q in ranks]
     outs = None
     for _ in range(n_layers):
+        vals = [_layer_input(desc, v) for v in vals]
         outs = []
         for q, v in zip(ranks, vals):
             out, _ = layer.layer_fwd(desc, W, v, q["e"], q["row_ptr"], q["col_idx"])
@@ -63,7 +72,7 @@ def ds_forward_backward(desc, W, ranks, v_global_rows, G_global_rows, n_layers, 
     G_global_rows(rows) -> dL/dout of the last layer for those sampled rows
     (owned rows are used).  Returns the weight gradients summed over ranks
     (Alg. 1 :418)."""
-    vals = [np.asarray(v_global_rows(q["local_rows"]), dtype=np.float64) for q in ranks]
+    vals = [_layer_input(desc, np.asarray(v_global_rows(q["local_rows"]), dtype=np.float64)) for q in ranks]
     acts = [vals]
     for _ in range(n_layers):
         outs = [layer.layer_fwd(desc, W, v, q["e"], q["row_ptr"], q["col_idx"])[0] for q, v in zip(ranks, vals)]
@@ -72,7 +81,7 @@ def ds_forward_backward(desc, W, ranks, v_global_rows, G_global_rows, n_layers, 
             nv = v.copy()
             nv[: len(o)] = o
             new_vals.append(nv)
-        vals = halo.halo_forward(ranks, new_vals)
+        vals = [_layer_input(desc, v) for v in halo.halo_forward(ranks, new_vals)]
         acts.append(vals)
     grads = None
     gouts = [np.asarray(G_global_rows(q["local_rows"][: len(q["row_ptr"]) - 1]), dtype=np.float64) for q in ranks]

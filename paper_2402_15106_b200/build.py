@@ -6,7 +6,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libdsmpnn.so")
+LIB = os.environ.get("DSMPNN_BUILD_OUT") or os.path.join(HERE, "libdsmpnn.so")
+# DSMPNN_BUILD_DEFINES="-DDSMPNN_TIMELINE": a development build (clock64 timelines),
+# written to DSMPNN_BUILD_OUT in its own object directory
+DEFINES = os.environ.get("DSMPNN_BUILD_DEFINES", "").split()
+OBJDIR = os.path.join(HERE, "build" + ("_dev" if DEFINES else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -47,10 +51,10 @@ def build(force=False, verbose=False):
         return LIB
     objs = []
     procs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
     for src in SOURCES:
-        obj = os.path.join(HERE, "build", src.replace(".cu", ".o"))
-        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj, "-I", CSRC] + NCCL_INC + [f for f in FLAGS if f != "-shared"]
+        obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj, "-I", CSRC] + NCCL_INC + DEFINES + [f for f in FLAGS if f != "-shared"]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -151,6 +151,16 @@ __global__ void gather_rows_any_kernel(const T *__restrict__ v, const int32_t *_
   }
 }
 
+// spins for `ns` nanoseconds of the global timer (test hook, see below)
+__global__ void stall_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(100000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 struct Gather {
   const char *src;
   const int32_t *rows;
@@ -302,8 +312,8 @@ dsmpnn_status dsmpnn_halo_exchange(dsmpnn_ctx c, int32_t nparts, const int32_t *
                                    const int32_t *local_parts, void *const *values, const int64_t *const *halo_ptr,
                                    const int64_t *const *send_ptr, const int32_t *const *send_idx, int32_t width,
                                    int32_t dtype, int32_t direction, int32_t flags, void *stream) {
-  DS_CHECK_ARG(c && c->comm, DSMPNN_ERR_INVALID_ARG, "halo_exchange: no context");
-  DS_CHECK_ARG(!c->aborted, DSMPNN_ERR_NCCL, "halo_exchange: the communicator was aborted");
+  DS_CHECK_ARG(c, DSMPNN_ERR_INVALID_ARG, "halo_exchange: no context");
+  DS_CHECK_ARG(!c->aborted && c->comm, DSMPNN_ERR_NCCL, "halo_exchange: the communicator was aborted");
   DS_CHECK_ARG(part_rank && (n_local == 0 || (local_parts && values && halo_ptr && send_ptr && send_idx)),
                DSMPNN_ERR_INVALID_ARG, "halo_exchange: NULL argument");
   DS_CHECK_ARG(width > 0, DSMPNN_ERR_INVALID_ARG, "halo_exchange: width");
@@ -326,9 +336,14 @@ dsmpnn_status dsmpnn_halo_exchange(dsmpnn_ctx c, int32_t nparts, const int32_t *
   auto L = [&](int part) { return find_local(n_local, local_parts, part); };
   bool any_nccl = false;
   for (const dsmpnn_halo_op &o : c->ops) any_nccl = any_nccl || o.kind != DSMPNN_HALO_OP_LOCAL;
-  // test hook: drop every send, so the matching receives never complete
-  // (exercises the dsmpnn_ctx_sync watchdog; never set in production)
-  static const bool drop_sends = getenv("DSMPNN_TEST_HALO_DROP_SENDS") != nullptr;
+  // test hook: stall the comm stream for DSMPNN_TEST_HALO_STALL_MS ms before
+  // the exchange (a bounded stand-in for a peer that never answers; exercises
+  // the dsmpnn_ctx_sync watchdog; never set in production)
+  static const int stall_ms = getenv("DSMPNN_TEST_HALO_STALL_MS") ? atoi(getenv("DSMPNN_TEST_HALO_STALL_MS")) : 0;
+  if (stall_ms > 0) {
+    stall_kernel<<<1, 1, 0, cs>>>((unsigned long long)stall_ms * 1000000ull);
+    DS_LAUNCH_CHECK();
+  }
   if (direction == DSMPNN_HALO_FORWARD) {
     std::vector<Gather> g;
     for (const dsmpnn_halo_op &o : c->ops) {
@@ -343,11 +358,8 @@ dsmpnn_status dsmpnn_halo_exchange(dsmpnn_ctx c, int32_t nparts, const int32_t *
     if (any_nccl) {
       DS_NCCL(ncclGroupStart());
       for (const dsmpnn_halo_op &o : c->ops) {
-        if (o.kind == DSMPNN_HALO_OP_SEND) {
-          if (!drop_sends)
-            DS_NCCL(ncclSend(stage + (size_t)o.offset * rowb, (size_t)o.rows * rowb, ncclUint8, o.peer_rank, c->comm,
-                             cs));
-        }
+        if (o.kind == DSMPNN_HALO_OP_SEND)
+          DS_NCCL(ncclSend(stage + (size_t)o.offset * rowb, (size_t)o.rows * rowb, ncclUint8, o.peer_rank, c->comm, cs));
         if (o.kind == DSMPNN_HALO_OP_RECV)
           DS_NCCL(ncclRecv((char *)values[L(o.dst_part)] + (size_t)o.offset * rowb, (size_t)o.rows * rowb, ncclUint8,
                            o.peer_rank, c->comm, cs));
@@ -390,8 +402,8 @@ dsmpnn_status dsmpnn_halo_wait(dsmpnn_ctx c, void *stream) {
 }
 
 dsmpnn_status dsmpnn_allreduce_sum_f32(dsmpnn_ctx c, float *buf, int64_t n, void *stream) {
-  DS_CHECK_ARG(c && c->comm, DSMPNN_ERR_INVALID_ARG, "allreduce: no context");
-  DS_CHECK_ARG(!c->aborted, DSMPNN_ERR_NCCL, "allreduce: the communicator was aborted");
+  DS_CHECK_ARG(c, DSMPNN_ERR_INVALID_ARG, "allreduce: no context");
+  DS_CHECK_ARG(!c->aborted && c->comm, DSMPNN_ERR_NCCL, "allreduce: the communicator was aborted");
   DS_CHECK_ARG(n >= 0, DSMPNN_ERR_INVALID_ARG, "allreduce: n < 0");
   cudaStream_t s = as_stream(stream);
   if (n > 0) DS_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclFloat32, ncclSum, c->comm, s));
@@ -400,8 +412,8 @@ dsmpnn_status dsmpnn_allreduce_sum_f32(dsmpnn_ctx c, float *buf, int64_t n, void
 }
 
 dsmpnn_status dsmpnn_ctx_sync(dsmpnn_ctx c, int32_t timeout_ms) {
-  DS_CHECK_ARG(c && c->comm, DSMPNN_ERR_INVALID_ARG, "ctx_sync: no context");
-  DS_CHECK_ARG(!c->aborted, DSMPNN_ERR_NCCL, "ctx_sync: the communicator was aborted");
+  DS_CHECK_ARG(c, DSMPNN_ERR_INVALID_ARG, "ctx_sync: no context");
+  DS_CHECK_ARG(!c->aborted && c->comm, DSMPNN_ERR_NCCL, "ctx_sync: the communicator was aborted");
   const auto t0 = std::chrono::steady_clock::now();
   for (;;) {
     cudaError_t q = cudaEventQuery(c->ev_done);

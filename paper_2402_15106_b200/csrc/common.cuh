@@ -75,4 +75,23 @@ struct ProbeScope {
   ~ProbeScope() { if (on) probe_after(id, s); }
 };
 
+#ifdef DSMPNN_TIMELINE
+// development builds: print the clock64 timeline of CTA 0 (slots relative to
+// the first stamp of tile 0), one line per tile
+static inline void dump_timeline(const char *name, const unsigned long long *dbg, int nslots, cudaStream_t s) {
+  unsigned long long h[32 * 32];
+  cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  unsigned long long t0 = ~0ull;
+  for (int k = 0; k < 32 * 32; ++k)
+    if (h[k] && h[k] < t0) t0 = h[k];
+  fprintf(stderr, "%s timeline (cycles since first stamp), tiles x slots\n", name);
+  for (int t = 0; t < 16; ++t) {
+    fprintf(stderr, "t%02d", t);
+    for (int k = 0; k < nslots; ++k) fprintf(stderr, " %7lld", h[t * 32 + k] ? (long long)(h[t * 32 + k] - t0) : -1ll);
+    fprintf(stderr, "\n");
+  }
+}
+#endif
+
 }  // namespace dsmpnn

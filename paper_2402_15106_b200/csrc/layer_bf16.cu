@@ -1,7 +1,7 @@
 // layer_bf16.cu - BF16 mode of the edge-conditioned convolution on the
 // tcgen05 tensor cores (sm_100a).  Formulation: DESIGN.md §6 ("aggregate
 // first", see layer.cu).  Widths supported: k = 256, d_in = d_out = D in
-// {32, 64}, d_e <= 16 (zero-padded).
+// {32, 64}, d_e <= 13 (zero-padded to 16; columns 13..15 carry the bias b1).
 //
 // Forward of rows [rb, re):
 //   1. fill kernel   : S~_aug[i][k*D + c] = mean_p v_j[c]  (the h~ = 1 row),
@@ -17,26 +17,40 @@
 //   3. node GEMM     : [S~_aug] . [Theta~ ; W_root^T] on tcgen05 (split-K),
 //   4. node epilogue : + b (+ v_i), sigma, out (fp32), out_lowp (bf16), pre.
 #include <cuda.h>
+#include <cstdlib>
 
 #include "layer_bf16.cuh"
 #include "layer_bf16_common.cuh"
 #include "edge_fwd2.cuh"
+#include "edge_fwd3.cuh"
 #include "simt.cuh"
 #include "tc.cuh"
 #include "tgemm.cuh"
 
 namespace dsmpnn {
 
-__global__ void pack_bf16_kernel(const float *__restrict__ W1, const float *__restrict__ W2,
-                                 const float *__restrict__ W3, const float *__restrict__ b3,
-                                 const float *__restrict__ Wr, int root_dense, int k, int de, int di, int dout,
-                                 int64_t kp, Packed p) {
+// W1 packed [k x 16]: columns 0..d_e-1 the weights, columns 13, 14, 15 the
+// bias b1 split into three bf16 terms (their fp32 sum is b1 to ~2^-24
+// relative: the MMA's fp32 accumulation adds it like an fp32 bias add), the
+// rest zero.  The fused edge kernels set e columns 13..15 to 1 in their SMEM
+// copy of the edge tile, so z1 = E W1^T already holds + b1 (edge_fwd3.cuh,
+// edge_bwd3.cuh); every other reader of W1 sees zeros there and adds b1 itself.
+__global__ void pack_bf16_kernel(const float *__restrict__ W1, const float *__restrict__ b1,
+                                 const float *__restrict__ W2, const float *__restrict__ W3,
+                                 const float *__restrict__ b3, const float *__restrict__ Wr, int root_dense, int k,
+                                 int de, int di, int dout, int64_t kp, Packed p) {
   int64_t n1 = (int64_t)k * 16, n2 = (int64_t)k * k, n3 = kp * dout;
   int64_t total = n1 + n2 + n3;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     if (t < n1) {
       int r = (int)(t / 16), c = (int)(t % 16);
-      p.W1[t] = __float2bfloat16_rn(c < de ? W1[(int64_t)r * de + c] : 0.f);
+      float w = c < de ? W1[(int64_t)r * de + c] : 0.f;
+      if (c >= kBiasCol0) {  // b1 = t0 + t1 + t2, each a bf16 value (t2 absorbs the rest to ~2^-24 |b1|)
+        const float t0 = __bfloat162float(__float2bfloat16_rn(b1[r]));
+        const float t1 = __bfloat162float(__float2bfloat16_rn(b1[r] - t0));
+        w = c == kBiasCol0 ? t0 : c == kBiasCol0 + 1 ? t1 : b1[r] - t0 - t1;
+      }
+      p.W1[t] = __float2bfloat16_rn(w);
     } else if (t < n1 + n2) {
       p.W2[t - n1] = __float2bfloat16_rn(W2[t - n1]);
     } else {
@@ -62,7 +76,9 @@ dsmpnn_status bf16_check_desc(const dsmpnn_layer_desc &d) {
   DS_CHECK_ARG(d.k == KH, DSMPNN_ERR_UNSUPPORTED, "layer BF16: k must be %d (got %d)", KH, d.k);
   DS_CHECK_ARG(d.d_in == d.d_out && (d.d_in == 32 || d.d_in == 64), DSMPNN_ERR_UNSUPPORTED,
                "layer BF16: d_in = d_out in {32, 64} (got %d, %d)", d.d_in, d.d_out);
-  DS_CHECK_ARG(d.d_e <= 16, DSMPNN_ERR_SHAPE, "layer BF16: d_e <= 16 (got %d)", d.d_e);
+  DS_CHECK_ARG(d.d_e <= kBiasCol0, DSMPNN_ERR_SHAPE,
+               "layer BF16: d_e <= %d (got %d; columns 13..15 of the padded edge tile carry the kappa bias)",
+               kBiasCol0, d.d_e);
   return DSMPNN_OK;
 }
 
@@ -83,7 +99,7 @@ dsmpnn_status bf16_pack(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, voi
   DS_CUDA(cudaMemsetAsync(p.ThT, 0, (size_t)d.d_out * kp * 2, s));
   int64_t total = (int64_t)d.k * 16 + (int64_t)d.k * d.k + kp * d.d_out;
   pack_bf16_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(
-      w.W1, w.W2, w.W3, w.b3, w.W_root, d.root == DSMPNN_ROOT_DENSE, d.k, d.d_e, d.d_in, d.d_out, kp, p);
+      w.W1, w.b1, w.W2, w.W3, w.b3, w.W_root, d.root == DSMPNN_ROOT_DENSE, d.k, d.d_e, d.d_in, d.d_out, kp, p);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -220,15 +236,33 @@ static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16
                                      const int32_t *col, int64_t rb, int64_t re, int64_t eb, int64_t ee,
                                      const Packed &pw, const float *b1, const float *b2, __nv_bfloat16 *S,
                                      int64_t kp, cudaStream_t s) {
-  using C = EF2<D>;
   CUtensorMap tW2;
   DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
-  auto kern = edge_fwd2_kernel<D>;
-  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_FWD, s);
-  kern<<<grid, 512, C::SMEM, s>>>(tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  // DSMPNN_EDGE_FWD=2 selects the previous design (h through SMEM) for A/B timing
+  static const bool v2 = getenv("DSMPNN_EDGE_FWD") && atoi(getenv("DSMPNN_EDGE_FWD")) == 2;
+  if (v2) {
+    auto kern = edge_fwd2_kernel<D>;
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EF2<D>::SMEM));
+    kern<<<grid, 512, EF2<D>::SMEM, s>>>(tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+  } else {
+    auto kern = edge_fwd3_kernel<D>;
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EF3<D>::SMEM));
+#ifdef DSMPNN_TIMELINE
+    static unsigned long long *dbg = nullptr;
+    if (!dbg) {
+      cudaMalloc(&dbg, 32 * 32 * 8);
+      cudaMemcpyToSymbol(g_tl3, &dbg, sizeof(dbg));
+    }
+    cudaMemsetAsync(dbg, 0, 32 * 32 * 8, s);
+#endif
+    kern<<<grid, 512, EF3<D>::SMEM, s>>>(tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+#ifdef DSMPNN_TIMELINE
+    dump_timeline("edge_fwd3", dbg, 29, s);
+#endif
+  }
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

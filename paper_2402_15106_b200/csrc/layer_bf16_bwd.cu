@@ -20,6 +20,7 @@
 //   B6  dW1 += dz1^T e ; de = dz1 W1              (tgemm)
 //   B7  dv[j] += sum_{p: col(p)=j} u_p            (deterministic CSC scatter)
 #include <cuda.h>
+#include <cstdlib>
 
 #include "layer_bf16.cuh"
 #include "layer_bf16_common.cuh"
@@ -27,6 +28,7 @@
 #include "tc.cuh"
 #include "tgemm.cuh"
 #include "edge_bwd2.cuh"
+#include "edge_bwd3.cuh"
 #include "dz1w1.cuh"
 #include "dw2.cuh"
 
@@ -288,18 +290,38 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
                                      const __nv_bfloat16 *v, const int64_t *row_ptr, const int32_t *col, int64_t n_dst,
                                      int64_t rb, int64_t re, int64_t eb, int64_t ee, const float *b1, const float *b2,
                                      const BBwd &b, bool write_a1, int *grid_out, cudaStream_t s) {
-  using C = EB2<D>;
   CUtensorMap tW2, tDS;
   DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
   DS_TRY(make_tmap_bf16(&tDS, b.dS, D, n_dst * (int64_t)(KH + 1), D, D, KH));
-  auto kern = edge_bwd2_kernel<D>;
-  DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   int64_t tiles = (ee - eb + 127) / 128 + 1;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   *grid_out = grid;
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_BWD, s);
-  kern<<<grid, 512, C::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS,
-                                  write_a1 ? b.A1 : nullptr, b.dZ2, b.U, b.db2_part);
+  // edge_bwd3 (a1 / h in TMEM, W2 resident) unless A1 is wanted (the unfused
+  // backward with the edge-attribute gradient) or DSMPNN_EDGE_BWD=2 (A/B timing)
+  static const bool v2 = getenv("DSMPNN_EDGE_BWD") && atoi(getenv("DSMPNN_EDGE_BWD")) == 2;
+  if (write_a1 || v2) {
+    auto kern = edge_bwd2_kernel<D>;
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EB2<D>::SMEM));
+    kern<<<grid, 512, EB2<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS,
+                                         write_a1 ? b.A1 : nullptr, b.dZ2, b.U, b.db2_part);
+  } else {
+    auto kern = edge_bwd3_kernel<D>;
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EB3<D>::SMEM));
+#ifdef DSMPNN_TIMELINE
+    static unsigned long long *dbg = nullptr;
+    if (!dbg) {
+      cudaMalloc(&dbg, 32 * 32 * 8);
+      cudaMemcpyToSymbol(g_tlb3, &dbg, sizeof(dbg));
+    }
+    cudaMemsetAsync(dbg, 0, 32 * 32 * 8, s);
+#endif
+    kern<<<grid, 512, EB3<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
+                                         b.db2_part);
+#ifdef DSMPNN_TIMELINE
+    dump_timeline("edge_bwd3", dbg, 30, s);
+#endif
+  }
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

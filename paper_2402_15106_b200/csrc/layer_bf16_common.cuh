@@ -9,6 +9,10 @@
 namespace dsmpnn {
 
 constexpr int KH = 256;  // kappa hidden width supported by the BF16 kernels
+// columns of the 16-wide padded edge tile / packed W1 that carry the first
+// kappa layer's bias as three bf16 terms (layer_bf16.cu pack_bf16_kernel):
+// d_e <= 13 in BF16 mode
+constexpr int kBiasCol0 = 13;
 
 static inline int64_t kpad_of(const dsmpnn_layer_desc &d) {
   int64_t kp = (int64_t)(d.k + 2) * d.d_in;

@@ -120,10 +120,11 @@ def test_allreduce_single_rank_is_identity(comm):
 
 
 def test_watchdog_times_out_and_aborts():
-    """A receive whose send never comes (test hook DSMPNN_TEST_HALO_DROP_SENDS)
-    makes dsmpnn_ctx_sync return TIMEOUT after the limit and abort the
-    communicator; later calls fail with NCCL instead of hanging.  Runs in a
-    child process under its own time limit."""
+    """An exchange that does not finish (test hook DSMPNN_TEST_HALO_STALL_MS:
+    the comm stream is held for 12 s before the transfer) makes dsmpnn_ctx_sync
+    return TIMEOUT after its 2 s limit and abort the communicator; later calls
+    fail with NCCL instead of hanging.  Runs in a child process under its own
+    time limit."""
     code = r'''
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
@@ -137,9 +138,9 @@ hp = HotPath(_cfg(c, 0), c["W"], torch.device("cuda:0"))
 hp.build(_T(c["x"]), _T(c["a"]))
 vals = [torch.zeros((sd.n_loc, c["d"]), device="cuda:0") for sd in hp.subs]
 hp.comm = comm
-hp.halo(vals, L.F32, flags=L.HALO_VIA_NCCL | L.HALO_ASYNC)
+hp.halo(vals, L.F32, flags=L.HALO_ASYNC)  # device copies only: no NCCL kernel is left behind the stall
 try:
-    comm.sync(timeout_ms=3000)
+    comm.sync(timeout_ms=2000)
     print("NO_TIMEOUT")
 except L.DsmpnnError as e:
     print("STATUS", e.status)
@@ -149,11 +150,12 @@ try:
 except L.DsmpnnError as e:
     print("AFTER", e.status)
 sys.stdout.flush()
+torch.cuda.synchronize()  # the stall kernel ends by itself
 import os
 os._exit(0)
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DSMPNN_TEST_HALO_DROP_SENDS="1")
+    env = dict(os.environ, DSMPNN_TEST_HALO_STALL_MS="12000")
     p = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=240)
     assert "STATUS -7" in p.stdout, p.stdout + p.stderr
     assert "AFTER -6" in p.stdout, p.stdout + p.stderr

@@ -246,10 +246,14 @@ def test_fwd_bwd_bf16(L, d, dim, mode, root, act):
 @pytest.mark.parametrize("d,dim,mode,root,act,n", [(64, 2, "diff", 2, 1, 700), (32, 3, "concat", 2, 1, 700),
                                                     (64, 2, "diff", 2, 1, 37)])
 def test_fwd_bwd_bf16_no_de(L, d, dim, mode, root, act, n):
-    """Without the edge-attribute gradient the library recomputes a1 from e
-    (B4 in dw2.cuh, the edge kernel skips A1) and fuses B5 and B6 (dz1 stays
-    on chip, dW1 accumulated in TMEM): same oracle bar, and the fused and
-    unfused paths agree closely on dW1, db1 and dW2, exactly elsewhere."""
+    """Without the edge-attribute gradient the library runs the fused edge
+    backward (edge_bwd3.cuh: a1 / h in TMEM, kappa bias through the MMA),
+    recomputes a1 from e (B4 in dw2.cuh) and fuses B5 and B6 (dz1 stays on
+    chip, dW1 accumulated in TMEM); with it, edge_bwd2 writes A1 and GEMMs
+    follow.  Both paths meet the oracle bar; the kappa_phi recomputes differ
+    (bias through the MMA vs an fp32 add), so a few ReLU decisions at the
+    kink may differ between them and only the dense-layer gradients agree to
+    fp32 summation order."""
     p = _problem(n, dim, 0.1 if dim == 2 else 0.2, 40, mode, d, 256, seed=41 + d + n, n_dst=n - 50 if n > 100 else n,
                  isolated=3 if n > 100 else 0)
     _mask_kinks(p, 1, root, act)
@@ -259,14 +263,14 @@ def test_fwd_bwd_bf16_no_de(L, d, dim, mode, root, act, n):
     for nm in GNAMES:
         assert nerr(got["grads"][nm], ref["grads"][nm]) <= TOL[1], nm
     unf = _run_gpu(L, p, 1, root, act, want_de=True)
-    # the unfused path sums bf16-rounded dz1 into db1, the fused one the fp32
-    # values (the oracle's dz1 is unrounded): they differ by ~bf16 resolution
-    for nm in ("W1", "b1"):
-        assert nerr(got["grads"][nm], unf["grads"][nm]) <= 1e-2, nm
-    # dW2: same bf16 operands, another fp32 summation order
-    assert nerr(got["grads"]["W2"], unf["grads"]["W2"]) <= 1e-4
-    for nm in ("b2", "W3", "b3", "W_root", "b"):
-        assert np.array_equal(got["grads"][nm], unf["grads"][nm]), nm
+    # the unfused path (edge_bwd2 + GEMMs, A1 in HBM) against the same oracle
+    assert nerr(unf["dv"], ref["dv"]) <= TOL[1]
+    for nm in GNAMES:
+        assert nerr(unf["grads"][nm], ref["grads"][nm]) <= TOL[1], nm
+    # the dense-layer gradients do not depend on kappa_phi's recompute: the
+    # two paths give the same values up to fp32 summation order
+    for nm in ("W3", "b3", "W_root", "b"):
+        assert nerr(got["grads"][nm], unf["grads"][nm]) <= 1e-5, nm
 
 
 def test_bf16_darcy_full_size_sampled_bwd(L):

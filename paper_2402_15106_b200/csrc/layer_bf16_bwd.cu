@@ -29,6 +29,7 @@
 #include "tgemm.cuh"
 #include "edge_bwd2.cuh"
 #include "edge_bwd3.cuh"
+#include "edge_bwd4.cuh"
 #include "dz1w1.cuh"
 #include "dw2.cuh"
 
@@ -297,10 +298,27 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, tiles));
   *grid_out = grid;
   ProbeScope probe(DSMPNN_PROBE_BF16_EDGE_BWD, s);
-  // edge_bwd3 (a1 / h in TMEM, W2 resident) unless A1 is wanted (the unfused
-  // backward with the edge-attribute gradient) or DSMPNN_EDGE_BWD=2 (A/B timing)
-  static const bool v2 = getenv("DSMPNN_EDGE_BWD") && atoi(getenv("DSMPNN_EDGE_BWD")) == 2;
-  if (write_a1 || v2) {
+  // edge_bwd4 (a1 / h in TMEM, W2 resident, dz2 through the TMA engine) unless
+  // A1 is wanted (the unfused backward with the edge-attribute gradient: edge_bwd2);
+  // DSMPNN_EDGE_BWD=2 / 3 select the earlier designs for A/B timing
+  static const int ver = getenv("DSMPNN_EDGE_BWD") ? atoi(getenv("DSMPNN_EDGE_BWD")) : 4;
+  if (!write_a1 && ver == 4) {
+    auto kern = edge_bwd4_kernel<D>;
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EB4<D>::SMEM));
+#ifdef DSMPNN_TIMELINE
+    static unsigned long long *dbg4 = nullptr;
+    if (!dbg4) {
+      cudaMalloc(&dbg4, 32 * 32 * 8);
+      cudaMemcpyToSymbol(g_tlb4, &dbg4, sizeof(dbg4));
+    }
+    cudaMemsetAsync(dbg4, 0, 32 * 32 * 8, s);
+#endif
+    kern<<<grid, 512, EB4<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
+                                         b.db2_part);
+#ifdef DSMPNN_TIMELINE
+    dump_timeline("edge_bwd4", dbg4, 16, s);
+#endif
+  } else if (write_a1 || ver == 2) {
     auto kern = edge_bwd2_kernel<D>;
     DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, EB2<D>::SMEM));
     kern<<<grid, 512, EB2<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b1, b2, b.dS,

@@ -94,6 +94,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, const void *s
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// 1-D bulk copy shared -> global (bytes a multiple of 16, both 16-byte aligned), bulk-group completion
+__device__ __forceinline__ void bulk_store_1d(void *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(gdst)),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -308,6 +314,19 @@ __device__ __forceinline__ uint32_t pack_bf16_relu(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
+}
+
+// 32 x 32 bit-matrix transpose across a warp: lane i holds row i (bit j);
+// returns column `lane` (bit i = bit `lane` of row i).  Five butterfly rounds.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u
+                                                                                                   : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+  }
+  return x;
 }
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a SW128 atom

@@ -657,7 +657,7 @@ def main():
             achieved = bytes_per_launch / (per_launch_ms / 1e3) / 1e9 if probe_n else 0.0
             tensor_tflops = bwd_flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
             if world == 1 and args.halo_ratio == 1.0:
-                traffic, traffic_src = ncu_traffic("edge_bwd2", args.config)
+                traffic, traffic_src = ncu_traffic("edge_bwd4", args.config)
         else:
             achieved = flops_edge * units_per_launch / (per_launch_ms / 1e3) / 1e12 if probe_n else 0.0
             bytes_per_launch, tensor_tflops = None, None
@@ -680,7 +680,7 @@ def main():
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "traffic_source": traffic_src,
-                         "kernel": {1: "F32 mlp2 sgemm", 5: "bf16 fused edge bwd (edge_bwd2)"}.get(probe_id,
+                         "kernel": {1: "F32 mlp2 sgemm", 5: "bf16 fused edge bwd (edge_bwd4)"}.get(probe_id,
                                                                                                str(probe_id)),
                          "algorithmic_bytes_per_launch": bytes_per_launch,
                          "tensor_tflops_same_launches": tensor_tflops,

@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(512, 1)
             }
           const int ns = (deg + 15) & ~15;
           const uint32_t ta = tZ + lane_off + cg * 128 + s0;
+          if ((warp == 4 || warp == 8) && lane == 0 && g < 2) TLB4(t, 16 + 2 * g + (warp == 8 ? 4 : 0));
           int c0 = 0;
           for (; c0 + 64 <= ns; c0 += 64) acc += dz2_stage<64>(ta + c0, slot_bits(mw, s0 + c0), kap, s0 + c0, stage);
           if (c0 + 32 <= ns) {
@@ -500,6 +501,7 @@ __global__ void __launch_bounds__(512, 1)
             c0 += 32;
           }
           if (c0 < ns) acc += dz2_stage<16>(ta + c0, slot_bits(mw, s0 + c0), kap, s0 + c0, stage);
+          if ((warp == 4 || warp == 8) && lane == 0 && g < 2) TLB4(t, 17 + 2 * g + (warp == 8 ? 4 : 0));
         }
         db2_acc += acc;
       }

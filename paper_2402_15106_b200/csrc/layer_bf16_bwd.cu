@@ -316,7 +316,7 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
     kern<<<grid, 512, EB4<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
                                          b.db2_part);
 #ifdef DSMPNN_TIMELINE
-    dump_timeline("edge_bwd4", dbg4, 16, s);
+    dump_timeline("edge_bwd4", dbg4, 24, s);
 #endif
   } else if (write_a1 || ver == 2) {
     auto kern = edge_bwd2_kernel<D>;

@@ -610,12 +610,16 @@ def main():
     # ---- graph build alone (sample + partition + radius graph + attributes + CSC), for reference
     torch.cuda.synchronize()
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.graph_stats(reset=True)
     g0.record(st)
     for _ in range(args.steps):
         hp.build(devin["coords"], devin["attr"])
     g1.record(st)
     torch.cuda.synchronize()
     graph_ms = g0.elapsed_time(g1) / args.steps
+    graph_tests = L.graph_stats(reset=True) / args.steps  # candidate tests per build (this rank)
+    # SURVEY D.3 a2 algorithmic bytes per sub-domain: n_loc (4 dim + 8) + 8 (n_dst + 1) + 4 E
+    graph_bytes = sum(sd.n_loc * (4 * sc.dim + 8) + 8 * (sd.n_own + 1) + 4 * sd.n_edges for sd in hp.subs)
 
     stats = torch.tensor([ms, e2e_ms, layer_ms, layer_ms_nocomm, float(E_local)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -695,6 +699,13 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "graph_ms": graph_ms,
+            "graph": {"ms": graph_ms, "candidate_tests": graph_tests,
+                      "candidate_tests_per_s": graph_tests / (graph_ms / 1e3),
+                      "scan_GBps": graph_tests * 16 / (graph_ms / 1e3) / 1e9,
+                      "algorithmic_GBps": graph_bytes / (graph_ms / 1e3) / 1e9,
+                      "what": "whole build (sample + partition + radius graph + attributes + CSC) on rank 0; "
+                              "candidate tests = fp32 predicate evaluations of the radius-graph search (first pass), "
+                              "16 B (cell-ordered float4) read per test; algorithmic bytes per SURVEY D.3 a2"},
             "layers_only": {"ms": layer_ms, "value": E_tot * sc.L / (layer_ms / 1e3),
                             "ms_no_comm": layer_ms_nocomm,
                             "exposed_comm_ms": layer_ms - layer_ms_nocomm if sc.halo else None,

@@ -106,6 +106,12 @@ dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64
                                   int32_t *col_idx, int64_t col_capacity, int64_t *n_edges /*host*/,
                                   void *ws, size_t ws_bytes, void *stream);
 
+/* Diagnostics of the radius-graph search: the number of candidate tests (fp32
+ * predicate evaluations) of dsmpnn_radius_graph calls since the last reset,
+ * summed over calls and devices' default context (synchronising read).
+ * candidate_tests: host uint64 out (may be NULL); reset != 0 zeroes the counter. */
+dsmpnn_status dsmpnn_graph_stats(uint64_t *candidate_tests /*host*/, int32_t reset);
+
 /* Candidate counts |C_i| (pre-cap) per destination row; same search as above.
  * counts int32[n_dst].  Used for diagnostics and tests. */
 dsmpnn_status dsmpnn_radius_counts(const float *coords, int64_t n_loc, int64_t n_dst, int dim, float r,

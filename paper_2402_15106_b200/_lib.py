@@ -81,6 +81,7 @@ _f = {
     "radius_graph_workspace_size": _sig("radius_graph_workspace_size", I64, I64, C.c_int, C.POINTER(SZ)),
     "radius_graph": _sig("radius_graph", P, P, I64, I64, C.c_int, F, I32, U64, P, P, I64, C.POINTER(I64), P, SZ, P),
     "radius_counts": _sig("radius_counts", P, I64, I64, C.c_int, F, P, P, SZ, P),
+    "graph_stats": _sig("graph_stats", C.POINTER(U64), I32),
     "csc_workspace_size": _sig("csc_workspace_size", I64, I64, C.POINTER(SZ)),
     "csc": _sig("csc", P, I64, I64, P, P, P, SZ, P),
     "partition_workspace_size": _sig("partition_workspace_size", I64, C.c_int, C.c_int, C.POINTER(SZ)),
@@ -201,6 +202,13 @@ def radius_counts(coords, n_dst, r, counts, stream=None):
     ws = _ws(radius_graph_workspace_size(n_loc, n_dst, dim), coords.device)
     _call("radius_counts", _p(coords), n_loc, n_dst, dim, float(r), _p(counts), _p(ws), ws.numel(), _stream(stream))
     return counts
+
+
+def graph_stats(reset=False):
+    """Candidate tests of the radius-graph search since the last reset."""
+    v = U64(0)
+    _call("graph_stats", C.byref(v), int(bool(reset)))
+    return int(v.value)
 
 
 def csc_workspace_size(n_edges, n_loc):

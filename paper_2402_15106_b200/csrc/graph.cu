@@ -17,6 +17,8 @@
 // A row whose boundary bin overflows the per-warp buffer (not expected for
 // hash keys) is finished by the general most-significant-digit radix select
 // (select_kernel, 8-bit digits over the full 128-bit (key, gid) composite).
+// Large sub-domains use the one-pass kernel graph1 instead (see below); the
+// candidate coordinates and gids are loaded together (scan_sorted_g).
 #include <cub/cub.cuh>
 #include <cstdlib>
 
@@ -341,13 +343,54 @@ __device__ __forceinline__ void scan_sorted(int64_t i, const float *__restrict__
     }
 }
 
+// As scan_sorted, with the candidate's gid loaded together with its
+// coordinates (both loads in flight before the predicate): F(t, j, ok, g).
+template <typename F>
+__device__ __forceinline__ void scan_sorted_g(int64_t i, const float *__restrict__ x, int dim, float r2,
+                                              const GridParams &p, const int32_t *__restrict__ start,
+                                              const float4 *__restrict__ xs, const int64_t *__restrict__ gs, F &&f) {
+  const int lane = threadIdx.x & 31;
+  float xi[3] = {0.f, 0.f, 0.f};
+  for (int d = 0; d < dim; ++d) xi[d] = x[i * dim + d];
+  int c[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) c[d] = cell_coord(xi[d], p.lo[d], p.inv_h, p.n[d]);
+  const int R = p.reach;
+  const int z0 = dim == 3 ? max(c[2] - R, 0) : 0, z1 = dim == 3 ? min(c[2] + R, p.n[2] - 1) : 0;
+  const int y0 = max(c[1] - R, 0), y1 = min(c[1] + R, p.n[1] - 1);
+  const int x0 = max(c[0] - R, 0), x1 = min(c[0] + R, p.n[0] - 1);
+  for (int cz = z0; cz <= z1; ++cz)
+    for (int cy = y0; cy <= y1; ++cy) {
+      const int base = (cz * p.n[1] + cy) * p.n[0];
+      const int a = start[base + x0], b = start[base + x1 + 1];
+      for (int t0 = a; t0 < b; t0 += 64) {
+        const int ta = t0 + lane, tb = t0 + 32 + lane;
+        const float4 pa = ta < b ? xs[ta] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        const float4 pb = tb < b ? xs[tb] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        const int64_t ga = ta < b ? __ldg(gs + ta) : 0, gb = tb < b ? __ldg(gs + tb) : 0;
+        {
+          const int j = __float_as_int(pa.w);
+          const float xj[3] = {pa.x, pa.y, pa.z};
+          f(ta, j, ta < b && j != i && within(xi, xj, dim, r2), ga);
+        }
+        if (t0 + 32 < b) {
+          const int j = __float_as_int(pb.w);
+          const float xj[3] = {pb.x, pb.y, pb.z};
+          f(tb, j, tb < b && j != i && within(xi, xj, dim, r2), gb);
+        }
+      }
+    }
+}
+
+__device__ unsigned long long g_graph_tests;  // candidate tests (fp32 predicate evaluations), dsmpnn_graph_stats
+
 // pass 1: counts, deg = min(count, n_e), and for capped rows the boundary
 // bin b* of the top-kHB key bits and the number `take` kept from it
 template <bool HIST>
 __global__ void __launch_bounds__(kGWarps * 32) count2_kernel(
     const float *__restrict__ x, const int64_t *__restrict__ gs, const int64_t *__restrict__ gid, int64_t n_dst,
     int dim, float r, int32_t n_e, uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
-    const float4 *__restrict__ xs, int32_t *__restrict__ counts, int64_t *__restrict__ deg, int2 *__restrict__ bnd) {
+    const float4 *__restrict__ xs, int32_t *__restrict__ counts, int64_t *__restrict__ deg, int2 *__restrict__ bnd,
+    int64_t n_loc = 0, int cell_order = 0) {
   __shared__ uint32_t hist_all[HIST ? kGWarps : 1][HIST ? kHBins : 1];
   const GridParams p = *gp;
   const float r2 = __fmul_rn(r, r);
@@ -358,12 +401,17 @@ __global__ void __launch_bounds__(kGWarps * 32) count2_kernel(
   __syncwarp();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n_dst; i += nwarps) {
+  unsigned long long nscan = 0;
+  const int64_t n_iter = cell_order ? n_loc : n_dst;
+  for (int64_t tt = warp; tt < n_iter; tt += nwarps) {
+    const int64_t i = cell_order ? (int64_t)__float_as_int(xs[tt].w) : tt;  // rows in cell order: L1 reuse
+    if (i >= n_dst) continue;
     const uint64_t si = HIST ? smx(s0 ^ (uint64_t)gid[i]) : 0;
     int cnt = 0;
-    scan_sorted(i, x, dim, r2, p, start, xs, [&](int t, int, bool ok) {
-      if (HIST && ok) atomicAdd(&hist[key_edge(si, (uint64_t)gs[t]) >> (64 - kHB)], 1u);
+    scan_sorted_g(i, x, dim, r2, p, start, xs, gs, [&](int, int jj, bool ok, int64_t gt) {
+      if (HIST && ok) atomicAdd(&hist[key_edge(si, (uint64_t)gt) >> (64 - kHB)], 1u);
       cnt += __popc(__ballot_sync(0xffffffffu, ok));
+      nscan += jj >= 0;
     });
     if (lane == 0) {
       if (counts) counts[i] = cnt;
@@ -398,6 +446,7 @@ __global__ void __launch_bounds__(kGWarps * 32) count2_kernel(
       __syncwarp();
     }
   }
+  if (HIST && nscan) atomicAdd(&g_graph_tests, nscan);
 }
 
 // pass 2 (capped rows select from the boundary bin; uncapped rows keep all)
@@ -406,7 +455,7 @@ __global__ void __launch_bounds__(kGWarps * 32) select2_kernel(
     int dim, float r, int32_t n_e, uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
     const float4 *__restrict__ xs, const int32_t *__restrict__ counts, const int2 *__restrict__ bnd,
     const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col, int32_t *__restrict__ fl_rows,
-    int32_t *__restrict__ fl_n, int force_fallback) {
+    int32_t *__restrict__ fl_n, int force_fallback, int64_t n_loc = 0, int cell_order = 0) {
   __shared__ int32_t Lt[kGWarps][kMaxNe];
   __shared__ int64_t Lg[kGWarps][kMaxNe];
   __shared__ uint64_t Bk[kGWarps][kCapB];
@@ -417,17 +466,20 @@ __global__ void __launch_bounds__(kGWarps * 32) select2_kernel(
   const uint32_t lt = (1u << lane) - 1u;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n_dst; i += nwarps) {
+  const int64_t n_iter = cell_order ? n_loc : n_dst;
+  for (int64_t tt = warp; tt < n_iter; tt += nwarps) {
+    const int64_t i = cell_order ? (int64_t)__float_as_int(xs[tt].w) : tt;
+    if (i >= n_dst) continue;
     const int cnt = counts[i];
     const bool capped = cnt > n_e;
     const int2 bt = capped ? bnd[i] : make_int2(kHBins, 0);
     const uint64_t si = smx(s0 ^ (uint64_t)gid[i]);
     int nl = 0, nb = 0;
-    scan_sorted(i, x, dim, r2, p, start, xs, [&](int t, int, bool ok) {
+    scan_sorted_g(i, x, dim, r2, p, start, xs, gs, [&](int t, int, bool ok, int64_t gt) {
       uint32_t top = 0;
       uint64_t key = 0;
       if (ok && capped) {
-        key = key_edge(si, (uint64_t)gs[t]);
+        key = key_edge(si, (uint64_t)gt);
         top = (uint32_t)(key >> (64 - kHB));
       }
       const bool inL = ok && (!capped || (int)top < bt.x);
@@ -481,6 +533,215 @@ __global__ void __launch_bounds__(kGWarps * 32) select2_kernel(
   }
 }
 
+// ------------------------------------------------------ one-pass path --
+// graph1_kernel: the candidate scan of each row runs ONCE.  Besides the
+// count and the histogram of the top kHB key bits, the warp keeps the
+// candidates whose bin is <= T in a shared list, where T is the boundary bin
+// of the histogram so far: the final boundary bin b* can only be lower (bins
+// only gain counts), so no candidate the selection needs is ever dropped.
+// When the list fills up, T is recomputed and the list compacted.  At the end
+// of the row the kept set (all candidates of an uncapped row; bins < b* plus
+// the `take` smallest (key, gid) of bin b* of a capped row) is ordered by gid
+// (rank sort) and written to the row's n_e-wide slot of `tmp`; after the
+// exclusive scan of the degrees a copy kernel packs the slots into col.  A
+// list overflow (many equal top bits, not expected for hash keys) flags the
+// row for the general radix select (select_kernel), as before.
+constexpr int kG1Warps = 4;
+
+__device__ __forceinline__ int warp_boundary_bin(const uint32_t *hist, int lane, int n_e, int *below) {
+  // bin b with (count in bins < b) < n_e <= (count in bins <= b); lane owns 32 consecutive bins
+  constexpr int PER = kHBins / 32;
+  uint32_t sum = 0;
+  for (int q = 0; q < PER; ++q) sum += hist[lane * PER + q];
+  uint32_t incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t excl = incl - sum;
+  int found = -1, bl = 0;
+  if ((int)excl < n_e && n_e <= (int)incl) {
+    uint32_t c0 = excl;
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t hq = hist[lane * PER + q];
+      if ((int)(c0 + hq) >= n_e) {
+        found = lane * PER + q;
+        bl = (int)c0;
+        break;
+      }
+      c0 += hq;
+    }
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, found >= 0);
+  const int src = m ? __ffs(m) - 1 : 0;
+  found = __shfl_sync(0xffffffffu, found, src);
+  bl = __shfl_sync(0xffffffffu, bl, src);
+  *below = bl;
+  return found;
+}
+
+template <int kCap1>  // shared candidate list per warp
+__global__ void __launch_bounds__(kG1Warps * 32, 6) graph1_kernel(
+    const float *__restrict__ x, const int64_t *__restrict__ gs, const int64_t *__restrict__ gid, int64_t n_loc,
+    int64_t n_dst,
+    int dim, float r, int32_t n_e, uint64_t s0, const GridParams *__restrict__ gp, const int32_t *__restrict__ start,
+    const float4 *__restrict__ xs, int32_t *__restrict__ counts, int64_t *__restrict__ deg, int32_t *__restrict__ tmp,
+    int32_t *__restrict__ fl_rows, int32_t *__restrict__ fl_n, int force_fallback, unsigned long long *scanned,
+    int cell_order) {
+  __shared__ uint32_t hist_all[kG1Warps][kHBins];
+  __shared__ int32_t lt_all[kG1Warps][kCap1];
+  __shared__ uint64_t lk_all[kG1Warps][kCap1];
+  __shared__ int32_t kj_all[kG1Warps][kMaxNe];
+  __shared__ int64_t kg_all[kG1Warps][kMaxNe];
+  const GridParams p = *gp;
+  const float r2 = __fmul_rn(r, r);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t *hist = hist_all[w];
+  int32_t *lt = lt_all[w];
+  uint64_t *lk = lk_all[w];
+  int32_t *kj = kj_all[w];
+  int64_t *kg = kg_all[w];
+  unsigned long long nscan = 0;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // rows in cell order: the warps of a block (and neighbouring blocks) scan
+  // overlapping cells, so candidate loads hit in L1; halo points are skipped
+  const int64_t n_iter = cell_order ? n_loc : n_dst;
+  for (int64_t tt = warp; tt < n_iter; tt += nwarps) {
+    const int64_t i = cell_order ? (int64_t)__float_as_int(xs[tt].w) : tt;
+    if (i >= n_dst) continue;
+    for (int q = lane; q < kHBins; q += 32) hist[q] = 0;
+    __syncwarp();
+    const uint64_t si = smx(s0 ^ (uint64_t)gid[i]);
+    int cnt = 0, ns = 0, T = kHBins - 1;
+    bool overflow = false;
+    scan_sorted_g(i, x, dim, r2, p, start, xs, gs, [&](int t, int jj, bool ok, int64_t gt) {
+      uint64_t key = 0;
+      int bin = kHBins;
+      if (ok) {
+        key = key_edge(si, (uint64_t)gt);
+        bin = (int)(key >> (64 - kHB));
+        // bins above T can no longer hold b*: their counts are never needed
+        if (bin <= T) atomicAdd(&hist[bin], 1u);
+      }
+      nscan += jj >= 0;
+      cnt += __popc(__ballot_sync(0xffffffffu, ok));
+      const bool keep = ok && bin <= T;
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int q = ns + __popc(m & lt_mask);
+        if (q < kCap1) {
+          lt[q] = t;
+          lk[q] = key;
+        }
+      }
+      ns += __popc(m);
+      if (ns > kCap1 - 64 && !overflow) {  // lower T to the boundary bin so far and compact the list
+        __syncwarp();
+        if (cnt > n_e) {
+          int below;
+          T = warp_boundary_bin(hist, lane, n_e, &below);
+          int nk = 0;
+          const int n0 = min(ns, kCap1);
+          for (int a0 = 0; a0 < n0; a0 += 32) {
+            const int a = a0 + lane;
+            int ta = 0;
+            uint64_t ka = 0;
+            bool k2 = false;
+            if (a < n0) {
+              ta = lt[a];
+              ka = lk[a];
+              k2 = (int)(ka >> (64 - kHB)) <= T;
+            }
+            __syncwarp();
+            const uint32_t m2 = __ballot_sync(0xffffffffu, k2);
+            if (k2) {
+              const int q = nk + __popc(m2 & lt_mask);
+              lt[q] = ta;
+              lk[q] = ka;
+            }
+            nk += __popc(m2);
+            __syncwarp();
+          }
+          ns = nk;
+        }
+        if (ns > kCap1 - 64) overflow = true;  // keep counting; the general select finishes the row
+      }
+    });
+    __syncwarp();
+    if (lane == 0) {
+      counts[i] = cnt;
+      deg[i] = cnt < n_e ? cnt : n_e;
+    }
+    if (overflow || ns > kCap1 || (force_fallback && cnt > n_e)) {
+      if (lane == 0) fl_rows[atomicAdd(fl_n, 1)] = (int32_t)i;
+      __syncwarp();
+      continue;
+    }
+    // the kept set: everything (uncapped), or bins < b* plus the `take` smallest (key, gid) of bin b*
+    int bstar = kHBins, take = 0;
+    if (cnt > n_e) {
+      int below;
+      bstar = warp_boundary_bin(hist, lane, n_e, &below);
+      take = n_e - below;
+    }
+    int nk = 0;
+    for (int a0 = 0; a0 < ns; a0 += 32) {
+      const int a = a0 + lane;
+      bool keep = false;
+      int ta = 0;
+      if (a < ns) {
+        ta = lt[a];
+        const uint64_t ka = lk[a];
+        const int ba = (int)(ka >> (64 - kHB));
+        if (ba < bstar) {
+          keep = true;
+        } else if (ba == bstar) {
+          const uint64_t ga = (uint64_t)gs[ta];
+          int rank = 0;
+          for (int b = 0; b < ns; ++b) {
+            const uint64_t kb = lk[b];
+            if ((int)(kb >> (64 - kHB)) != bstar) continue;
+            rank += kb < ka || (kb == ka && (uint64_t)gs[lt[b]] < ga);
+          }
+          keep = rank < take;
+        }
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int q = nk + __popc(m & lt_mask);
+        kj[q] = __float_as_int(xs[ta].w);
+        kg[q] = gs[ta];
+      }
+      nk += __popc(m);
+    }
+    __syncwarp();
+    // order the row by gid (R11): rank sort, write the row's slot of tmp
+    for (int a = lane; a < nk; a += 32) {
+      const int64_t g = kg[a];
+      int rank = 0;
+      for (int b = 0; b < nk; ++b) rank += kg[b] < g;
+      tmp[i * (int64_t)n_e + rank] = kj[a];
+    }
+    __syncwarp();
+  }
+  if (nscan) atomicAdd(scanned ? scanned : &g_graph_tests, nscan);  // candidate tests (predicate evaluations)
+}
+
+// col[row_ptr[i] + k] = tmp[i * n_e + k], k < deg_i (rows finished by the general select are skipped)
+__global__ void pack_rows_kernel(const int32_t *__restrict__ tmp, const int64_t *__restrict__ row_ptr,
+                                 const int32_t *__restrict__ counts, int64_t n_dst, int32_t n_e,
+                                 int32_t *__restrict__ col) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = warp; i < n_dst; i += nwarps) {
+    const int64_t a = row_ptr[i], d = row_ptr[i + 1] - a;
+    for (int k = lane; k < d; k += 32) col[a + k] = tmp[i * (int64_t)n_e + k];
+  }
+}
+
 static int64_t max_cells_for(int64_t n_loc) { return std::max<int64_t>(4 * n_loc, 4096); }
 
 static size_t graph_ws(int64_t n_loc, int64_t n_dst, size_t *sort_tmp, size_t *scan_tmp) {
@@ -500,6 +761,8 @@ static size_t graph_ws(int64_t n_loc, int64_t n_dst, size_t *sort_tmp, size_t *s
   c.take<int32_t>(n_dst + 1);
   c.take<char>(*sort_tmp);
   c.take<char>(*scan_tmp);
+  c.take<int32_t>(n_dst * (int64_t)kMaxNe);  // one-pass row slots
+  c.take<unsigned long long>(2);
   return c.used();
 }
 
@@ -513,6 +776,8 @@ struct GraphState {
   int32_t *fl;  // [0] = count, [1..] = rows
   void *scan_tmp;
   size_t scan_bytes;
+  int32_t *tmp;                  // [n_dst x n_e] row slots of the one-pass kernel
+  unsigned long long *scanned;   // candidate tests of the last build (diagnostics)
 };
 
 static dsmpnn_status build_cells(const float *coords, const int64_t *gid, int64_t n_loc, int64_t n_dst, int dim,
@@ -537,6 +802,8 @@ static dsmpnn_status build_cells(const float *coords, const int64_t *gid, int64_
   void *t1 = c.take<char>(sort_tmp);
   st.scan_tmp = c.take<char>(scan_tmp);
   st.scan_bytes = scan_tmp;
+  st.tmp = c.take<int32_t>(n_dst * (int64_t)kMaxNe);
+  st.scanned = c.take<unsigned long long>(2);
   bbox_kernel<<<1, 1024, 0, s>>>(coords, n_loc, dim, bb);
   // cell edge r(1+2^-8)/kReach: kReach cells on each side cover r with a margin
   // for the rounding of the cell index; smaller cells scan less area per row
@@ -563,6 +830,17 @@ static dsmpnn_status build_cells(const float *coords, const int64_t *gid, int64_
 using namespace dsmpnn;
 
 extern "C" {
+
+dsmpnn_status dsmpnn_graph_stats(uint64_t *candidate_tests, int32_t reset) {
+  unsigned long long v = 0;
+  DS_CUDA(cudaMemcpyFromSymbol(&v, g_graph_tests, sizeof(v)));
+  if (candidate_tests) *candidate_tests = v;
+  if (reset) {
+    const unsigned long long z = 0;
+    DS_CUDA(cudaMemcpyToSymbol(g_graph_tests, &z, sizeof(z)));
+  }
+  return DSMPNN_OK;
+}
 
 dsmpnn_status dsmpnn_radius_graph_workspace_size(int64_t n_loc, int64_t n_dst, int dim, size_t *bytes) {
   DS_CHECK_ARG(n_loc >= 0 && n_dst >= 0 && n_dst <= n_loc && n_loc < (1ll << 31), DSMPNN_ERR_INVALID_ARG,
@@ -608,12 +886,36 @@ dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64
   GraphState st;
   DS_TRY(build_cells(coords, gid, n_loc, n_dst, dim, r, ws, ws_bytes, s, st));
   const uint64_t s0 = smx(seed);
+  const bool force_fb = getenv("DSMPNN_TEST_GRAPH_FALLBACK") != nullptr;
+  // One pass (graph1, rows in cell order) or two passes (count2 + select2,
+  // rows in index order).  Measured per Darcy sub-domain (4.1k rows, index
+  // order already spatially coherent): two passes 441 us, one pass 618 us;
+  // airfoil (25k rows per sub-domain, unordered cloud, up to 12k candidates
+  // per row): one pass 14.4 ms, two passes 22 ms per build of 8; step: 2.95 vs
+  // 3.3 ms.  Both give the same graph bit for bit; the choice is by size.
+  // DSMPNN_GRAPH_TWO_PASS=0|1 forces one (A/B timing).
+  static const int force_tp = getenv("DSMPNN_GRAPH_TWO_PASS") ? atoi(getenv("DSMPNN_GRAPH_TWO_PASS")) : -1;
+  const bool two_pass = force_tp >= 0 ? force_tp != 0 : n_dst < 16384;
   int blocks = (int)std::min<int64_t>(ceil_div(n_dst, kGWarps), 148 * 16);
-  count2_kernel<true><<<blocks, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start,
-                                                      st.xs, st.counts, st.deg, st.bnd);
-  DS_LAUNCH_CHECK();
+  // rows of the two-pass kernels in index order (cell order with DSMPNN_GRAPH_ROWORDER=1)
+  static const int roworder2 = getenv("DSMPNN_GRAPH_ROWORDER") ? atoi(getenv("DSMPNN_GRAPH_ROWORDER")) : 0;
+  const int roworder = 1;
+  const int blocks2 = (int)std::min<int64_t>(ceil_div(roworder2 ? n_loc : n_dst, kGWarps), 148 * 16);
   DS_CUDA(cudaMemsetAsync(st.fl, 0, sizeof(int32_t), s));
   DS_CUDA(cudaMemsetAsync(st.deg + n_dst, 0, sizeof(int64_t), s));
+  if (!two_pass) {
+    const int blocks1 = (int)std::min<int64_t>(ceil_div(n_loc, kG1Warps), 148 * 32);
+    static const int cap = getenv("DSMPNN_GRAPH_CAP") ? atoi(getenv("DSMPNN_GRAPH_CAP")) : 320;
+    auto k1 = cap >= 512 ? graph1_kernel<512> : graph1_kernel<320>;
+    k1<<<blocks1, kG1Warps * 32, 0, s>>>(coords, st.gs, gid, n_loc, n_dst, dim, r, n_e, s0, st.gp, st.start,
+                                                   st.xs,
+                                                   st.counts, st.deg, st.tmp, st.fl + 1, st.fl, force_fb ? 1 : 0,
+                                                   nullptr, roworder);
+  } else {
+    count2_kernel<true><<<blocks2, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start,
+                                                         st.xs, st.counts, st.deg, st.bnd, n_loc, roworder2);
+  }
+  DS_LAUNCH_CHECK();
   size_t sb = st.scan_bytes;
   DS_CUDA(cub::DeviceScan::ExclusiveSum(st.scan_tmp, sb, st.deg, row_ptr, (int)(n_dst + 1), s));
   if (n_edges) {
@@ -624,9 +926,14 @@ dsmpnn_status dsmpnn_radius_graph(const float *coords, const int64_t *gid, int64
       return DSMPNN_ERR_CAPACITY;
     }
   }
-  select2_kernel<<<blocks, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start, st.xs,
-                                                st.counts, st.bnd, row_ptr, col_idx, st.fl + 1, st.fl,
-                                                getenv("DSMPNN_TEST_GRAPH_FALLBACK") != nullptr);
+  if (!two_pass) {
+    pack_rows_kernel<<<(int)std::min<int64_t>(ceil_div(n_dst, 8), 148 * 16), 256, 0, s>>>(st.tmp, row_ptr, st.counts,
+                                                                                         n_dst, n_e, col_idx);
+  } else {
+    select2_kernel<<<blocks2, kGWarps * 32, 0, s>>>(coords, st.gs, gid, n_dst, dim, r, n_e, s0, st.gp, st.start, st.xs,
+                                                   st.counts, st.bnd, row_ptr, col_idx, st.fl + 1, st.fl, force_fb, n_loc,
+                                                   roworder2);
+  }
   DS_LAUNCH_CHECK();
   // rows whose boundary bin overflowed (row list on the device; usually empty)
   select_kernel<<<148, kSelWarps * 32, 0, s>>>(coords, gid, n_dst, dim, r, n_e, s0, st.gp, st.start, st.sorted_idx,

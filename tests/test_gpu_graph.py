@@ -252,3 +252,20 @@ def test_csc_view(L):
     want_perm = np.lexsort((np.arange(E), col))
     assert np.array_equal(N(perm), want_perm)
     assert np.array_equal(N(ptr), np.searchsorted(col[want_perm], np.arange(501), side="left"))
+
+
+@pytest.mark.parametrize("mode", ["0", "1"], ids=["one-pass", "two-pass"])
+def test_graph_parity_with_each_radius_kernel(mode):
+    """The radius graph has two kernels with the same output bit for bit: the
+    one-pass graph1 (chosen for sub-domains of >= 16384 rows) and count2 +
+    select2 (smaller ones).  The graph parity tests of this file rerun in a
+    child process with DSMPNN_GRAPH_TWO_PASS forcing each."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DSMPNN_GRAPH_TWO_PASS=mode)
+    p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_graph.py"), "-m", "gpu", "-q",
+                        "-p", "no:cacheprovider", "-k", "not each_radius_kernel"], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]

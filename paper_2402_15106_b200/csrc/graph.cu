@@ -446,7 +446,10 @@ __global__ void __launch_bounds__(kGWarps * 32) count2_kernel(
       __syncwarp();
     }
   }
-  if (HIST && nscan) atomicAdd(&g_graph_tests, nscan);
+  if (HIST) {  // one atomic per warp
+    const unsigned int wsum = __reduce_add_sync(0xffffffffu, (unsigned int)nscan);
+    if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&g_graph_tests, (unsigned long long)wsum);
+  }
 }
 
 // pass 2 (capped rows select from the boundary bin; uncapped rows keep all)
@@ -726,7 +729,10 @@ __global__ void __launch_bounds__(kG1Warps * 32, 6) graph1_kernel(
     }
     __syncwarp();
   }
-  if (nscan) atomicAdd(scanned ? scanned : &g_graph_tests, nscan);  // candidate tests (predicate evaluations)
+  {  // candidate tests (predicate evaluations), one atomic per warp
+    const unsigned int wsum = __reduce_add_sync(0xffffffffu, (unsigned int)nscan);
+    if (lane == 0 && wsum) atomicAdd(scanned ? scanned : &g_graph_tests, (unsigned long long)wsum);
+  }
 }
 
 // col[row_ptr[i] + k] = tmp[i * n_e + k], k < deg_i (rows finished by the general select are skipped)

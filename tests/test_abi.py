@@ -72,3 +72,24 @@ def test_no_oracle_import_in_product():
     for f in glob.glob(os.path.join(ROOT, "paper_2402_15106_b200", "**", "*.py"), recursive=True):
         src = open(f).read()
         assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), f
+
+
+def test_bench_gpus_n_spawns_n_ranks(monkeypatch):
+    """`python bench.py --gpus N` outside torchrun starts N ranks itself
+    (torch.distributed.run on 127.0.0.1) instead of timing one rank."""
+    import subprocess
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    calls = []
+    monkeypatch.setattr(subprocess, "call", lambda cmd, *a, **k: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3"])
+    assert bench.main() == 0
+    assert len(calls) == 1
+    cmd = calls[0]
+    assert "torch.distributed.run" in cmd and "--nproc-per-node=2" in cmd and "127.0.0.1" in cmd
+    assert cmd[cmd.index("--gpus") + 1] == "2"
+    # under torchrun with a mismatching WORLD_SIZE the bench refuses
+    monkeypatch.setenv("WORLD_SIZE", "3")
+    assert bench.main() == 2

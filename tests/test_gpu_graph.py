@@ -269,3 +269,23 @@ def test_graph_parity_with_each_radius_kernel(mode):
                         "-p", "no:cacheprovider", "-k", "not each_radius_kernel"], env=env, capture_output=True,
                        text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+def test_radius_graph_airfoil_full_size_dense_rows(L):
+    """BASELINE configs[2] at full size (200k points, r = 0.05, n_e = 64): the
+    whole cloud as one sub-domain (the one-pass kernel), checked on rows
+    with more than 5k candidates (the boundary layer),
+    chosen by the oracle's own candidate counts."""
+    cfg = synth.CONFIGS["airfoil"]
+    coords, _ = synth.points(cfg)
+    x = coords.astype(np.float32)
+    n = len(x)
+    gid = np.arange(n, dtype=np.int64)
+    seedc = synth.BASE_SEED + synth.SEED_CAPPING
+    rp, col, E = _graph_gpu(L, x, gid, n, cfg.r, cfg.n_e, seedc)
+    probe = hash_rows(n, 1500, salt=3)
+    dense = [int(i) for i in probe if graph.candidate_count(x, int(i), cfg.r) > 5000][:12]
+    assert len(dense) >= 4
+    ref = graph.radius_graph_rows(x, gid, dense, cfg.r, cfg.n_e, seedc)
+    for i, want in zip(dense, ref):
+        assert np.array_equal(col[rp[i]:rp[i + 1]], want), i

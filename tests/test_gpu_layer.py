@@ -308,3 +308,67 @@ def test_fwd_bf16_darcy_full_size_sampled(L):
     # the BF16 mode's whole rounding budget is inside the same 2e-2 bar
     plain, _ = layer.layer_fwd(LayerDesc(3, cfg.d, cfg.d, cfg.k, 2, 1, "none"), W, p["v"], e, rp, col, rows=rows)
     assert nerr(got["out"][rows], plain) <= TOL[1]
+
+
+def test_bf16_rows_longer_than_128_edges_are_unsupported(L):
+    """The fused BF16 edge kernels tile whole rows of at most 128 edges; a
+    longer row is rejected with UNSUPPORTED before any launch (with and
+    without the host copy of row_ptr), and the context stays usable."""
+    n, d, k = 300, 64, 256
+    rp = np.array([0, 129, 131], np.int64)
+    col = np.arange(131, dtype=np.int32) % n
+    W = synth.weights(3, d, d, k, salt=5)
+    desc = L.make_desc(3, d, d, k, L.BF16, L.ROOT_DENSE, L.ACT_RELU)
+    Wd = {nm: T(W[nm]) for nm in GNAMES}
+    packed = torch.empty(L.packed_weights_size(desc), dtype=torch.uint8, device=cuda())
+    L.pack_weights(desc, Wd, packed)
+    v = T(synth.node_features(n, d)).to(torch.bfloat16)
+    e = torch.zeros((131, 16), dtype=torch.bfloat16, device=cuda())
+    out = torch.empty((2, d), device=cuda())
+    ws = torch.empty(L.layer_workspace_size(desc, 2, 131), dtype=torch.uint8, device=cuda())
+    for host in (torch.from_numpy(rp), None):
+        with pytest.raises(L.DsmpnnError) as ei:
+            L.layer_fwd(desc, Wd, packed, v, e, T(rp), T(col), 2, 0, 2, out, None, ws, row_ptr_host=host)
+        assert ei.value.status == -8
+    # row 1 alone (2 edges) is fine
+    L.layer_fwd(desc, Wd, packed, v, e, T(rp), T(col), 2, 1, 2, out, None, ws, row_ptr_host=torch.from_numpy(rp))
+    torch.cuda.synchronize()
+    assert torch.isfinite(out[1]).all()
+
+
+def test_debug_index_validation_returns_index_error():
+    """With DSMPNN_DEBUG set, a CSR with a column index out of range gives
+    ERR_INDEX instead of an out-of-bounds read (child process: the switch is
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2402_15106_b200 import _lib as L, synth
+n, d, k = 50, 16, 32
+W = synth.weights(3, d, d, k, salt=1)
+desc = L.make_desc(3, d, d, k, L.F32, L.ROOT_DENSE, L.ACT_RELU)
+Wd = {nm: torch.from_numpy(np.ascontiguousarray(W[nm])).cuda() for nm in W}
+packed = torch.empty(L.packed_weights_size(desc), dtype=torch.uint8, device="cuda")
+L.pack_weights(desc, Wd, packed)
+rp = torch.tensor([0, 2, 3], dtype=torch.int64, device="cuda")
+col = torch.tensor([1, 7, 10**6], dtype=torch.int32, device="cuda")
+v = torch.randn(n, d, device="cuda"); e = torch.zeros(3, 3, device="cuda")
+out = torch.empty(2, d, device="cuda")
+ws = torch.empty(L.layer_workspace_size(desc, 2, 3), dtype=torch.uint8, device="cuda")
+G = torch.randn(2, d, device="cuda"); gv = torch.zeros(n, d, device="cuda")
+perm = torch.empty(3, dtype=torch.int32, device="cuda"); cptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+grads = {nm: torch.zeros_like(t) for nm, t in Wd.items()}
+bws = torch.empty(L.layer_bwd_workspace_size(desc, 2, n, 3), dtype=torch.uint8, device="cuda")
+try:
+    L.layer_bwd(desc, Wd, packed, v, e, rp, col, perm, cptr, 2, n, 0, 2, G, gv, None, grads, ws, bws)
+    print("NO_ERROR")
+except L.DsmpnnError as ex:
+    print("STATUS", ex.status)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code, root], env=dict(os.environ, DSMPNN_DEBUG="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert "STATUS -3" in p.stdout, p.stdout + p.stderr

@@ -26,6 +26,7 @@ import numpy as np
 
 from . import features, halo, layer
 from .layer import LayerDesc, ROOT_IDENTITY, ACT_IDENTITY
+from .precision import round_bf16
 
 
 def mlp_fwd(P, x):
@@ -62,24 +63,32 @@ def _refresh(x, u, row_ptr, col_idx):
     return np.concatenate([x[dst] - x[ci], u[dst] - u[ci]], axis=1)
 
 
-def conv_desc(d_e, d, k):
-    return LayerDesc(d_e, d, d, k, ROOT_IDENTITY, ACT_IDENTITY)
+def conv_desc(d_e, d, k, act_round="none"):
+    return LayerDesc(d_e, d, d, k, ROOT_IDENTITY, ACT_IDENTITY, act_round)
 
 
-def ds_train_grads(params, ranks, v0_rows, Y_rows, hops, dim, n_attr, x_rows):
+def ds_train_grads(params, ranks, v0_rows, Y_rows, hops, dim, n_attr, x_rows, bf16=False):
     """Loss and weight gradients of one DS-MPNN step on the decomposed ranks.
 
     params: dict enc=[(W,b)]*3, dec=[(W,b)]*3, conv=layer weight dict.
     v0_rows(rows) -> initial node values [x, a] of sampled rows; Y_rows(rows)
     -> targets [n_attr]; x_rows(rows) -> coordinates.  Returns (loss, grads)
-    with grads in the same structure (summed over ranks, Alg. 1 :418)."""
+    with grads in the same structure (summed over ranks, Alg. 1 :418).
+    bf16=True: the BF16 mode's rounding points of the convolution (R18, R27):
+    its weights W1, W2, W3, b3, every hop's input v_L and edge attributes e
+    are bf16 operands and a1, h are rounded (act_round); the encoder, the
+    decoder, the latent values and all arithmetic stay fp64."""
     enc, dec = params["enc"], params["dec"]
     d = enc[2][0].shape[0]
     W = dict(params["conv"])
     W.setdefault("W_root", np.zeros((d, d)))  # identity root: unused
     k = W["W1"].shape[0]
     d_e = dim + n_attr
-    desc = conv_desc(d_e, d, k)
+    desc = conv_desc(d_e, d, k, "bf16" if bf16 else "none")
+    rnd = round_bf16 if bf16 else (lambda a: a)
+    if bf16:
+        for nm in ("W1", "W2", "W3", "b3"):
+            W[nm] = round_bf16(W[nm])
     R = len(ranks)
     n_own = [len(q["row_ptr"]) - 1 for q in ranks]
     xs = [np.asarray(x_rows(q["local_rows"]), np.float32) for q in ranks]
@@ -91,10 +100,11 @@ def ds_train_grads(params, ranks, v0_rows, Y_rows, hops, dim, n_attr, x_rows):
         y, cache = mlp_fwd(enc, v0[q])
         enc_cache.append(cache)
         vL.append(y)
-        e.append(ranks[q]["e"])  # e^0 from the initial values (R21 diff)
+        e.append(rnd(ranks[q]["e"]))  # e^0 from the initial values (R21 diff)
     hist = []
     for hop in range(hops):
-        outs = [layer.layer_fwd(desc, W, vL[q], e[q], ranks[q]["row_ptr"], ranks[q]["col_idx"])[0]
+        vin = [rnd(v) for v in vL]  # the convolution's operand
+        outs = [layer.layer_fwd(desc, W, vin[q], e[q], ranks[q]["row_ptr"], ranks[q]["col_idx"])[0]
                 for q in range(R)]
         new = []
         for q in range(R):
@@ -104,8 +114,8 @@ def ds_train_grads(params, ranks, v0_rows, Y_rows, hops, dim, n_attr, x_rows):
         new = halo.halo_forward(ranks, new)
         dec_out = [mlp_fwd(dec, new[q]) for q in range(R)]
         u = [o[0] for o in dec_out]
-        e_next = [_refresh(xs[q], u[q], ranks[q]["row_ptr"], ranks[q]["col_idx"]) for q in range(R)]
-        hist.append(dict(vin=vL, e=e, vout=new, dec_cache=[o[1] for o in dec_out], u=u))
+        e_next = [rnd(_refresh(xs[q], u[q], ranks[q]["row_ptr"], ranks[q]["col_idx"])) for q in range(R)]
+        hist.append(dict(vin=vin, e=e, vout=new, dec_cache=[o[1] for o in dec_out], u=u))
         vL, e = new, e_next
     count = sum(n_own) * n_attr
     u_last = hist[-1]["u"]

@@ -397,7 +397,10 @@ class TrainStep:
     refresh (iv) e_ij = (x_i - x_j, u_i - u_j)}; MSE of the last decoded values
     on owned rows; backward with received values detached (R16); gradient sum
     over processes; SGD (Alg. 1 :419) or Adam.  The oracle is
-    oracle/train.py (O9).
+    oracle/train.py (O9).  F32 or BF16 mode (cfg.dtype): in BF16 the latent
+    values, the decoder and the optimiser stay fp32, and each hop's
+    convolution reads a bf16 copy of its input and the bf16 edge attributes
+    (the tensor-core kernels; reading R27), as oracle.train's bf16 mode.
 
     params: dict enc=[(W, b)] * 3, dec=[(W, b)] * 3 (PyTorch [out, in]),
     conv=layer weights (W1, b1, W2, b2, W3, b3, b)."""
@@ -407,7 +410,6 @@ class TrainStep:
     def __init__(self, cfg: StepConfig, params: dict, hops: int, device, rank=0, world=1, group=None,
                  optimizer="sgd", lr=1e-3, comm=None):
         import dataclasses
-        assert cfg.dtype == L.F32, "the training step runs in F32 mode"
         cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops)
         conv = dict(params["conv"])
         conv.setdefault("W_root", np.zeros((cfg.d, cfg.d), np.float32))  # identity root: unused
@@ -435,6 +437,14 @@ class TrainStep:
         L.mlp3_fwd(Wb, x, h1, h2, y)
         return y, (x, h1, h2)
 
+    def _conv_input(self, v):
+        """The convolution's operand: v itself (F32) or its bf16 copy (BF16)."""
+        if self.hp.cfg.dtype == L.F32:
+            return v
+        vb = torch.empty(v.shape, dtype=torch.bfloat16, device=self.dev)
+        L.gather_rows_bf16(v, None, vb)
+        return vb
+
     def loss_and_grads(self, v0_global, Y_global):
         """v0_global [N x (dim + n_attr)] initial node values, Y_global
         [N x n_attr] targets (rows = point ids).  Returns (loss, grads) with
@@ -452,14 +462,15 @@ class TrainStep:
             y, cache = self._mlp(self.enc, v0)
             enc_cache.append(cache)
             vL.append(y)
-            e.append(sd.e32)
+            e.append(sd.e32 if c.dtype == L.F32 else sd.e16)
         hist = []
         for hop in range(self.hops):
-            new = []
+            new, vin = [], []
             for q, sd in enumerate(subs):
                 ws = hp._ws(("fwd", hop, q), L.layer_workspace_size(desc, sd.n_own, sd.n_edges))
                 out = torch.empty((sd.n_own, c.d), device=self.dev)
-                L.layer_fwd(desc, hp.W, hp.packed, vL[q], e[q], sd.row_ptr, sd.col_idx, sd.n_own, 0, sd.n_own, out,
+                vin.append(self._conv_input(vL[q]))
+                L.layer_fwd(desc, hp.W, hp.packed, vin[q], e[q], sd.row_ptr, sd.col_idx, sd.n_own, 0, sd.n_own, out,
                             None, ws, row_ptr_host=sd.row_ptr_host)
                 nv = vL[q].clone()
                 nv[: sd.n_own].copy_(out)
@@ -470,10 +481,14 @@ class TrainStep:
                 uq, cache = self._mlp(self.dec, new[q])
                 dec_cache.append(cache)
                 u.append(uq)
-                en = torch.empty((max(sd.n_edges, 1), dim + n_attr), device=self.dev)
-                L.edge_features(L.EDGE_DIFF, sd.coords, uq, sd.row_ptr, sd.col_idx, sd.n_own, e32=en)
+                if c.dtype == L.F32:
+                    en = torch.empty((max(sd.n_edges, 1), dim + n_attr), device=self.dev)
+                    L.edge_features(L.EDGE_DIFF, sd.coords, uq, sd.row_ptr, sd.col_idx, sd.n_own, e32=en)
+                else:
+                    en = torch.empty((max(sd.n_edges, 1), 16), dtype=torch.bfloat16, device=self.dev)
+                    L.edge_features(L.EDGE_DIFF, sd.coords, uq, sd.row_ptr, sd.col_idx, sd.n_own, e16=en)
                 e_next.append(en)
-            hist.append(dict(vin=vL, e=e, vout=new, dec_cache=dec_cache, u=u))
+            hist.append(dict(vin=vin, e=e, vout=new, dec_cache=dec_cache, u=u))
             vL, e = new, e_next
         # loss: MSE of the last decoded values on owned rows, over all ranks
         count = sum(sd.n_own for sd in subs) * n_attr

@@ -34,12 +34,12 @@ def _case(seed=91, n=500, P=4, hops=2, d=16, k=32, hid=24, r=0.12, n_e=12):
     return dict(x=x, a=a, params=params, v0=v0, Y=Y, n=n, P=P, hops=hops, d=d, k=k, r=r, n_e=n_e)
 
 
-def _step(c, optimizer="sgd", lr=1e-2, update=False):
+def _step(c, optimizer="sgd", lr=1e-2, update=False, dtype=0):
     from paper_2402_15106_b200 import _lib as L
     from paper_2402_15106_b200.api import StepConfig, TrainStep
     l = c["r"] * (1 + 2 ** -12)
     sc = StepConfig(n_points=c["n"], s=c["n"], dim=2, n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l, n_e=c["n_e"],
-                    d=c["d"], k=c["k"], L=c["hops"], edge_mode=L.EDGE_DIFF, dtype=L.F32, seed_sampling=3,
+                    d=c["d"], k=c["k"], L=c["hops"], edge_mode=L.EDGE_DIFF, dtype=dtype, seed_sampling=3,
                     seed_capping=5)
     ts = TrainStep(sc, c["params"], c["hops"], cuda(), optimizer=optimizer, lr=lr)
     T = lambda arr: torch.from_numpy(np.ascontiguousarray(arr)).to(cuda())
@@ -53,7 +53,7 @@ def _step(c, optimizer="sgd", lr=1e-2, update=False):
     return loss, g, ts
 
 
-def _oracle(c):
+def _oracle(c, bf16=False):
     ids = sample.sample(c["n"], c["n"], 3).astype(np.int64)
     l = c["r"] * (1 + 2 ** -12)
     _, _, _, ranks = decomp.build_local(c["x"][ids], ids, c["a"][ids], c["P"], l, c["r"], c["n_e"], 5, "diff")
@@ -62,7 +62,7 @@ def _oracle(c):
                conv={k: v.astype(np.float64) for k, v in c["params"]["conv"].items()})
     v0, Y, x = c["v0"][ids], c["Y"][ids], c["x"][ids]
     return train.ds_train_grads(p64, ranks, lambda rows: v0[rows], lambda rows: Y[rows], c["hops"], 2, 1,
-                                lambda rows: x[rows])
+                                lambda rows: x[rows], bf16=bf16)
 
 
 def test_train_step_loss_and_gradients(lib):
@@ -99,3 +99,23 @@ def test_train_step_update(lib, opt):
             ref, _, _ = train.adam(w0, gr, np.zeros_like(w0), np.zeros_like(w0), 1, lr)
         # the update moves each weight by at most lr; compare the moved weights
         assert np.allclose(w_gpu.cpu().numpy(), ref, rtol=0, atol=1e-5 * max(1.0, np.abs(w0).max()) + 2e-4 * lr)
+
+
+def test_train_step_bf16_loss_and_gradients(lib):
+    """The training step in BF16 mode (the tensor-core convolution of the
+    benchmark inside the full hop loop: encoder, 2 residual hops with halo
+    refresh, decoder, edge refresh (iv), MSE, DETACH backward through the
+    unfused BF16 backward that returns the edge-attribute gradient) against
+    oracle.train's bf16 rounding points (R18, R27) at the north_star's 2e-2."""
+    c = _case(seed=93, d=32, k=256)
+    loss, g, _ = _step(c, dtype=1)
+    w_loss, wg = _oracle(c, bf16=True)
+    assert abs(loss - w_loss) <= 2e-2 * abs(w_loss)
+    errs = {}
+    for part in ("enc", "dec"):
+        for l_ in range(3):
+            for j in range(2):
+                errs[(part, l_, j)] = nerr(g[part][2 * l_ + j].cpu().numpy(), wg[part][l_][j])
+    for nm in ("W1", "b1", "W2", "b2", "W3", "b3", "b"):
+        errs[nm] = nerr(g["conv"][nm].cpu().numpy(), wg["conv"][nm])
+    assert max(errs.values()) <= 2e-2, errs

@@ -278,6 +278,52 @@ dsmpnn_status dsmpnn_halo_reverse_add_loopback(int32_t nparts, float *const *val
                                                const int64_t *const *send_ptr, const int32_t *const *send_idx,
                                                int32_t width, void *stream);
 
+/* ------------------------------------------------------------------ a8 --- */
+/* Sub-domain batch: the P sub-domains one process holds as ONE disjoint-union
+ * graph, so a layer (a4 + a5 + a7) runs once over all of them.
+ * places one sub-domain on each GPU; with more sub-domains than processes the
+ * local graphs are independent between two halo refreshes (Alg. 1 :404-411),
+ * and the union gives the same per-row results as P separate calls (reading
+ * R31).  Union node order: owned rows of part 0..P-1, then halo rows of part
+ * 0..P-1 (N_own = sum n_own, N_loc = sum n_loc); own row i of part q is union
+ * row own_off_q + i, halo row n_own_q + h of part q is union row halo_off_q + h.
+ * Union edges: the parts' edges concatenated (edge_off_q = sum of earlier E).
+ * Every part whose halo rows source another part must have that part in the
+ * batch (a process-local batch: all P parts).  1 <= P <= 16.
+ *
+ * parts: host array of P descriptors (device pointers inside, except the host
+ * halo_ptr / send_ptr: int64[P+1] each, the plan of dsmpnn_partition_all).
+ * Outputs (device, caller-allocated; any may be NULL to skip it):
+ *   row_ptr  int64[N_own+1]   union CSR (row_ptr[N_own] = E_tot)
+ *   col_idx  int32[E_tot]     union column ids
+ *   e        E_tot x e_row_bytes bytes: the parts' edge attribute rows
+ *   csc_perm int32[E_tot], csc_ptr int64[N_loc+1]: the union CSC view; each
+ *            union column's list is its part's list (order kept) + edge_off_q
+ *   rows     int64[N_loc]     the parts' `rows` entries in union order
+ *   halo_src int32[N_loc-N_own] union row each union halo row is copied from:
+ *            a FORWARD halo refresh is dsmpnn_halo_gather(values, halo_src,
+ *            N_loc - N_own, width, dtype, values + N_own * width)
+ * ws: sized by dsmpnn_batch_workspace_size.  Errors: P out of range ->
+ * UNSUPPORTED; inconsistent halo / send plans -> SHAPE; union sizes >= 2^31 ->
+ * UNSUPPORTED; missing inputs for a requested output -> INVALID_ARG. */
+typedef struct {
+  int64_t n_own, n_loc, n_edges;
+  const int64_t *row_ptr;   /* int64[n_own+1] */
+  const int32_t *col_idx;   /* int32[n_edges], local ids < n_loc */
+  const void *e;            /* n_edges x e_row_bytes (or NULL when e is not requested) */
+  const int32_t *csc_perm;  /* int32[n_edges] (dsmpnn_csc) */
+  const int64_t *csc_ptr;   /* int64[n_loc+1] */
+  const int64_t *rows;      /* int64[n_loc] per-row payload (e.g. sampled-set rows), or NULL */
+  const int64_t *halo_ptr;  /* host int64[P+1]: halo rows from part p are [halo_ptr[p], halo_ptr[p+1]) */
+  const int64_t *send_ptr;  /* host int64[P+1]: rows sent to part q are send_idx[send_ptr[q] ..] */
+  const int32_t *send_idx;  /* int32[n_send] local own rows */
+} dsmpnn_batch_part;
+dsmpnn_status dsmpnn_batch_workspace_size(int32_t nparts, size_t *bytes);
+dsmpnn_status dsmpnn_batch_subdomains(int32_t nparts, const dsmpnn_batch_part *parts, int32_t e_row_bytes,
+                                      int64_t *row_ptr, int32_t *col_idx, void *e, int32_t *csc_perm,
+                                      int64_t *csc_ptr, int64_t *rows, int32_t *halo_src, void *ws, size_t ws_bytes,
+                                      void *stream);
+
 /* ------------------------------------------------------- a6 over NCCL --- */
 /* The halo exchange between processes ("the overlap area of a
  * given domain is updated from the neighboring domains' interiors"; Alg. 1

@@ -60,6 +60,12 @@ class Grads(C.Structure):
     _fields_ = [("W1", P), ("b1", P), ("W2", P), ("b2", P), ("W3", P), ("b3", P), ("W_root", P), ("b", P)]
 
 
+class BatchPart(C.Structure):
+    _fields_ = [("n_own", I64), ("n_loc", I64), ("n_edges", I64), ("row_ptr", P), ("col_idx", P), ("e", P),
+                ("csc_perm", P), ("csc_ptr", P), ("rows", P), ("halo_ptr", C.POINTER(I64)),
+                ("send_ptr", C.POINTER(I64)), ("send_idx", P)]
+
+
 class HaloOp(C.Structure):
     _fields_ = [("kind", I32), ("peer_rank", I32), ("src_part", I32), ("dst_part", I32), ("rows", I64),
                 ("offset", I64)]
@@ -99,6 +105,8 @@ _f = {
     "layer_bwd": _sig("layer_bwd", C.POINTER(LayerDesc), C.POINTER(Weights), P, P, P, P, P, P, P, I64, I64, I64, I64,
                       P, P, P, C.POINTER(Grads), P, P, SZ, P),
     "halo_gather": _sig("halo_gather", P, P, I64, I32, I32, P, P),
+    "batch_workspace_size": _sig("batch_workspace_size", I32, C.POINTER(SZ)),
+    "batch_subdomains": _sig("batch_subdomains", I32, C.POINTER(BatchPart), I32, P, P, P, P, P, P, P, P, SZ, P),
     "halo_scatter_add": _sig("halo_scatter_add", P, P, I64, I32, P, P),
     "accumulate_f32": _sig("accumulate_f32", P, P, I64, P),
     "halo_exchange_loopback": _sig("halo_exchange_loopback", I32, C.POINTER(P), C.POINTER(C.POINTER(I64)),
@@ -337,6 +345,29 @@ def layer_bwd(desc, W, packed, v, e, row_ptr, col_idx, csc_perm, csc_ptr, n_dst,
 def halo_gather(values, rows, out, dtype, stream=None):
     width = values.shape[1]
     _call("halo_gather", _p(values), _p(rows), rows.numel(), width, dtype, _p(out), _stream(stream))
+
+
+def batch_subdomains(parts, e_row_bytes, row_ptr, col_idx, e, csc_perm, csc_ptr, rows, halo_src, ws=None,
+                     stream=None):
+    """a8: the union graph of P local sub-domains.  parts: list of dicts with
+    n_own, n_loc, n_edges (ints), row_ptr, col_idx, e, csc_perm, csc_ptr, rows,
+    send_idx (device tensors or None) and halo_ptr, send_ptr (int lists)."""
+    P_ = len(parts)
+    keep = []
+    arr = (BatchPart * P_)()
+    for q, d in enumerate(parts):
+        hp = (I64 * (P_ + 1))(*[int(x) for x in d["halo_ptr"]])
+        sp = (I64 * (P_ + 1))(*[int(x) for x in d["send_ptr"]])
+        keep += [hp, sp]
+        arr[q] = BatchPart(int(d["n_own"]), int(d["n_loc"]), int(d["n_edges"]), _p(d["row_ptr"]), _p(d["col_idx"]),
+                           _p(d.get("e")), _p(d.get("csc_perm")), _p(d.get("csc_ptr")), _p(d.get("rows")),
+                           C.cast(hp, C.POINTER(I64)), C.cast(sp, C.POINTER(I64)), _p(d.get("send_idx")))
+    sz = SZ()
+    _call("batch_workspace_size", P_, C.byref(sz))
+    dev = parts[0]["row_ptr"].device
+    ws = ws if ws is not None and ws.numel() >= sz.value else _ws(sz.value, dev)
+    _call("batch_subdomains", P_, arr, int(e_row_bytes), _p(row_ptr), _p(col_idx), _p(e), _p(csc_perm), _p(csc_ptr),
+          _p(rows), _p(halo_src), _p(ws), ws.numel(), _stream(stream))
 
 
 def accumulate_f32(dst, src, stream=None):

@@ -51,6 +51,7 @@ class StepConfig:
     streams: int = 2  # CUDA streams the local sub-domains' layer work is spread over (1: one stream)
     halo: int = 1  # 0: skip the per-layer halo refresh (bench --no-comm: measures the exposed exchange time)
     halo_flags: int = 0  # extra dsmpnn_halo_exchange flags (L.HALO_VIA_NCCL: same-process pairs through NCCL too)
+    batch: int = -1  # 1/-1: without a communicator, run the local sub-domains as one union graph (a8, R31); 0: per part
 
 
 def parts_of_process(nparts, world, rank):
@@ -111,7 +112,14 @@ class HotPath:
         pipeline.build_graphs(self.subs, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
                               want_bf16=(c.dtype == L.BF16), streams=self._side_streams(),
                               ws_cache=self.ws.setdefault("graph", {}))
+        self.bat = pipeline.batch_subdomains(self.subs) if self._batched() else None
         return self
+
+    def _batched(self):
+        """Union-graph mode (a8): every sub-domain is on this device (no
+        communicator), more than one of them, and no deep-row overlap asked for."""
+        c = self.cfg
+        return (c.batch != 0 and self.comm is None and 1 < len(self.subs) <= 16 and c.overlap_halo != 1)
 
     @property
     def n_edges(self):
@@ -187,6 +195,8 @@ class HotPath:
         v0: [s x d] initial latent of the sampled nodes (sampled order).
         Returns (acts, outs): every layer's input per sub-domain (local order)
         and the last layer's fp32 outputs of each sub-domain's owned rows."""
+        if getattr(self, "bat", None) is not None:
+            return self._forward_batch(v0)
         c, desc = self.cfg, self.desc
         lowp = c.dtype == L.BF16
         vdt = torch.bfloat16 if lowp else torch.float32
@@ -267,6 +277,8 @@ class HotPath:
         lowp = c.dtype == L.BF16
         for g in self.grads.values():
             g.zero_()
+        if getattr(self, "bat", None) is not None:
+            return self._forward_backward_batch(v0, G)
         acts, _ = self.forward(v0)
         # backward: DETACH or REVERSE_ADD halo rows (R16, f2)
         gouts = []
@@ -326,6 +338,56 @@ class HotPath:
                 gouts = [gv[: sd.n_own] for gv, sd in zip(new_g, self.subs)]
         if self.world > 1:
             self._allreduce_grads()
+        return self.grads
+
+    # ------------------------------------------------ union-graph mode (a8) --
+    def _forward_batch(self, v0):
+        """forward() over the union graph: one layer call per layer for all
+        local sub-domains, then one gather refreshes every halo row.  Returns
+        (acts, outs) with acts[l] the union layer inputs and outs the per-part
+        views of the last layer's fp32 outputs."""
+        c, desc, b = self.cfg, self.desc, self.bat
+        lowp = c.dtype == L.BF16
+        vdt = torch.bfloat16 if lowp else torch.float32
+        v = torch.empty((b.n_loc, c.d), dtype=vdt, device=self.dev)
+        if lowp:
+            L.gather_rows_bf16(v0, b.local_rows, v)
+        else:
+            L.gather_rows(v0, b.local_rows, v)
+        acts = [v]
+        out = self._ws(("out", "B"), b.n_own * c.d * 4).view(torch.float32)[: b.n_own * c.d].view(b.n_own, c.d)
+        e = b.e16 if lowp else b.e32
+        for layer in range(c.L):
+            nv = torch.empty((b.n_loc, c.d), dtype=vdt, device=self.dev)
+            ws = self._ws(("fwd", layer, "B"), L.layer_workspace_size(desc, b.n_own, b.n_edges))
+            L.layer_fwd(desc, self.W, self.packed, acts[-1], e, b.row_ptr, b.col_idx, b.n_own, 0, b.n_own, out,
+                        nv[: b.n_own] if lowp else None, ws, row_ptr_host=b.row_ptr_host)
+            if not lowp:
+                nv[: b.n_own].copy_(out)
+            if c.halo:
+                pipeline.batch_halo(b, nv, L.BF16 if lowp else L.F32)
+            acts.append(nv)
+        outs = [out[o:o + sd.n_own] for o, sd in zip(b.own_off, self.subs)]
+        return acts, outs
+
+    def _forward_backward_batch(self, v0, G):
+        c, desc, b = self.cfg, self.desc, self.bat
+        lowp = c.dtype == L.BF16
+        acts, _ = self._forward_batch(v0)
+        g = torch.empty((b.n_own, c.d), dtype=torch.float32, device=self.dev)
+        L.gather_rows(G, b.local_rows[: b.n_own], g)
+        bws = self._ws(("bwd", "B"), L.layer_bwd_workspace_size(desc, b.n_own, b.n_loc, b.n_edges))
+        e = b.e16 if lowp else b.e32
+        for layer in reversed(range(c.L)):
+            # the input gradient of the first layer is not needed (no scatter / root term)
+            gv = torch.zeros((b.n_loc, c.d), dtype=torch.float32, device=self.dev) if layer > 0 else None
+            L.layer_bwd(desc, self.W, self.packed, acts[layer], e, b.row_ptr, b.col_idx, b.csc_perm, b.csc_ptr,
+                        b.n_own, b.n_loc, 0, b.n_own, g, gv, None, self.grads, self.ws[("fwd", layer, "B")], bws,
+                        row_ptr_host=b.row_ptr_host)
+            if gv is not None:
+                if c.grad_mode == REVERSE_ADD:
+                    pipeline.batch_halo_reverse(b, gv)
+                g = gv[: b.n_own]
         return self.grads
 
     def _ws_grads(self, k):
@@ -410,7 +472,7 @@ class TrainStep:
     def __init__(self, cfg: StepConfig, params: dict, hops: int, device, rank=0, world=1, group=None,
                  optimizer="sgd", lr=1e-3, comm=None):
         import dataclasses
-        cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops)
+        cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops, batch=0)
         conv = dict(params["conv"])
         conv.setdefault("W_root", np.zeros((cfg.d, cfg.d), np.float32))  # identity root: unused
         self.hp = HotPath(cfg, conv, device, rank, world, group, comm=comm)

@@ -30,7 +30,7 @@ NCCL_INC = ["-I", os.path.join(NCCL, "include")] if NCCL else []
 NCCL_LINK = (["-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
              if NCCL else ["-lnccl"])
 
-SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu", "train.cu", "comm.cu"]
+SOURCES = ["misc.cu", "sample.cu", "graph.cu", "partition.cu", "simt.cu", "tgemm.cu", "layer.cu", "layer_bf16.cu", "layer_bf16_bwd.cu", "gcn.cu", "train.cu", "comm.cu", "batch.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "--extended-lambda", "-Xcompiler", "-fPIC", "-shared",
          "-Xptxas", "-warn-spills"]

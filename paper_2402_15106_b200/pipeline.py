@@ -190,3 +190,88 @@ def halo_exchange_comm(comm, subs, values, dtype, proc_of, direction, flags=0, s
     comm.halo_exchange(subs[0].nparts, proc_of, [sd.rank for sd in subs], values, [sd.halo_ptr for sd in subs],
                        [sd.send_ptr for sd in subs], [sd.send_idx for sd in subs], dtype, direction, flags,
                        stream=stream)
+
+
+@dataclass
+class Batch:
+    """The local sub-domains as one disjoint-union graph (dsmpnn_batch_subdomains,
+    reading R31): owned rows of every part first, then every part's halo rows."""
+    subs: list
+    n_own: int
+    n_loc: int
+    n_edges: int
+    own_off: list                   # union row of part q's row 0
+    halo_off: list                  # union row of part q's first halo row
+    row_ptr: torch.Tensor
+    row_ptr_host: torch.Tensor
+    col_idx: torch.Tensor
+    e32: torch.Tensor
+    e16: torch.Tensor
+    csc_perm: torch.Tensor
+    csc_ptr: torch.Tensor
+    local_rows: torch.Tensor        # int64 [n_loc] sampled-set rows in union order
+    halo_src: torch.Tensor          # int32 [n_loc - n_own]
+
+
+def batch_subdomains(subs, ws=None):
+    """Union graph of `subs` (every sub-domain of the plan, all on this device)."""
+    dev = subs[0].coords.device
+    n_own = sum(sd.n_own for sd in subs)
+    n_loc = sum(sd.n_loc for sd in subs)
+    E = sum(sd.n_edges for sd in subs)
+    own_off, halo_off, a, h = [], [], 0, n_own
+    for sd in subs:
+        own_off.append(a)
+        halo_off.append(h)
+        a += sd.n_own
+        h += sd.n_halo
+    # host copy of the union row_ptr (the layer calls read edge ranges from it)
+    parts_h, eoff = [], 0
+    for sd in subs:
+        parts_h.append(sd.row_ptr_host[:-1] + eoff)
+        eoff += sd.n_edges
+    parts_h.append(torch.tensor([E], dtype=torch.int64))
+    rph = torch.cat(parts_h)
+    e_arr = subs[0].e16 if subs[0].e16 is not None else subs[0].e32
+    e_row_bytes = e_arr.shape[1] * e_arr.element_size()
+    b = Batch(subs, n_own, n_loc, E, own_off, halo_off,
+              row_ptr=torch.empty(n_own + 1, dtype=torch.int64, device=dev), row_ptr_host=rph,
+              col_idx=torch.empty(max(E, 1), dtype=torch.int32, device=dev), e32=None, e16=None,
+              csc_perm=torch.empty(max(E, 1), dtype=torch.int32, device=dev),
+              csc_ptr=torch.empty(n_loc + 1, dtype=torch.int64, device=dev),
+              local_rows=torch.empty(n_loc, dtype=torch.int64, device=dev),
+              halo_src=torch.empty(max(n_loc - n_own, 1), dtype=torch.int32, device=dev))
+    e_out = torch.empty((max(E, 1), e_arr.shape[1]), dtype=e_arr.dtype, device=dev)
+    if subs[0].e16 is not None:
+        b.e16 = e_out
+    else:
+        b.e32 = e_out
+    parts = [dict(n_own=sd.n_own, n_loc=sd.n_loc, n_edges=sd.n_edges, row_ptr=sd.row_ptr, col_idx=sd.col_idx,
+                  e=sd.e16 if sd.e16 is not None else sd.e32, csc_perm=sd.csc_perm, csc_ptr=sd.csc_ptr,
+                  rows=sd.local_rows, halo_ptr=sd.halo_ptr, send_ptr=sd.send_ptr, send_idx=sd.send_idx)
+             for sd in subs]
+    L.batch_subdomains(parts, e_row_bytes, b.row_ptr, b.col_idx, e_out, b.csc_perm, b.csc_ptr, b.local_rows,
+                       b.halo_src, ws=ws)
+    return b
+
+
+def batch_halo(b, values, dtype, stream=None):
+    """FORWARD halo refresh of a union value array [n_loc x width]: one gather."""
+    if b.n_loc > b.n_own:
+        L.halo_gather(values, b.halo_src[: b.n_loc - b.n_own], values[b.n_own:], dtype, stream=stream)
+
+
+def batch_halo_reverse(b, grads):
+    """REVERSE_ADD of a union fp32 gradient array, pair by pair in the order of
+    dsmpnn_halo_reverse_add_loopback (bitwise the same sums)."""
+    subs = b.subs
+    for p, sp in enumerate(subs):
+        for q, sq in enumerate(subs):
+            if q == p:
+                continue
+            s0, s1 = sp.send_ptr[q], sp.send_ptr[q + 1]
+            a, z = sq.halo_ptr[p], sq.halo_ptr[p + 1]
+            if z == a:
+                continue
+            h0 = b.halo_off[q] + (a - sq.n_own)
+            L.halo_scatter_add(grads[h0:h0 + (z - a)], sp.send_idx[s0:s1], grads[b.own_off[p]:])

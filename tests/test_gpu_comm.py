@@ -39,7 +39,7 @@ def _cfg(c, dtype, **kw):
     l = c["r"] * (1 + 2 ** -12)
     sc = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
                     n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
-                    seed_sampling=3, seed_capping=5, streams=1)
+                    seed_sampling=3, seed_capping=5, streams=1, batch=0)
     return dataclasses.replace(sc, **kw)
 
 

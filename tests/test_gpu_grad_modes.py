@@ -27,13 +27,14 @@ def _case(seed=61, n=600, dim=2, d=16, k=32, L=3, P=4, r=0.11, n_e=16):
     return dict(x=x, a=a, W=W, v0=v0, G=G, n=n, dim=dim, d=d, k=k, L=L, P=P, r=r, n_e=n_e)
 
 
-def _gpu(c, mode, dtype, streams=2, nparts=None, root=2, act=1, G=None):
+def _gpu(c, mode, dtype, streams=2, nparts=None, root=2, act=1, G=None, batch=0):
     from paper_2402_15106_b200 import _lib as Lib
     from paper_2402_15106_b200.api import HotPath, StepConfig
     l = c["r"] * (1 + 2 ** -12)
     sc = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=nparts or c["P"], r=c["r"],
                     overlap_l=l, n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
-                    seed_sampling=3, seed_capping=5, grad_mode=mode, streams=streams, root=root, act=act)
+                    seed_sampling=3, seed_capping=5, grad_mode=mode, streams=streams, root=root, act=act,
+                    batch=batch)
     dev = cuda()
     hp = HotPath(sc, c["W"], dev)
     ids = sample.sample(c["n"], c["n"], 3)  # identity sample (s = N), sampled order = id order
@@ -75,22 +76,24 @@ def lib():
     build.build()
 
 
+@pytest.mark.parametrize("batch", [0, 1], ids=["per-part", "union"])
 @pytest.mark.parametrize("mode", [decomp.DETACH, decomp.REVERSE_ADD], ids=["detach", "reverse_add"])
-def test_step_gradients_match_oracle_f32(lib, mode):
+def test_step_gradients_match_oracle_f32(lib, mode, batch):
     c = _case()
-    got = _gpu(c, mode, 0)
+    got = _gpu(c, mode, 0, batch=batch)
     want = _oracle(c, mode)
     for n in NAMES:
         assert nerr(got[n], want[n]) <= 1e-5, n
 
 
-def test_reverse_add_equals_undecomposed_and_detach_does_not(lib):
+@pytest.mark.parametrize("batch", [0, 1], ids=["per-part", "union"])
+def test_reverse_add_equals_undecomposed_and_detach_does_not(lib, batch):
     c = _case(seed=62)
-    got = _gpu(c, decomp.REVERSE_ADD, 0)
+    got = _gpu(c, decomp.REVERSE_ADD, 0, batch=batch)
     single = _oracle(c, decomp.REVERSE_ADD, P=1)
     for n in NAMES:
         assert nerr(got[n], single[n]) <= 1e-5, n
-    det = _gpu(c, decomp.DETACH, 0)
+    det = _gpu(c, decomp.DETACH, 0, batch=batch)
     assert max(nerr(det[n], single[n]) for n in NAMES) > 1e-3
 
 
@@ -106,7 +109,7 @@ def test_overlapped_halo_refresh_is_bitwise_identical(lib, dtype):
     l = c["r"] * (1 + 2 ** -12)
     base = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
                       n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
-                      seed_sampling=3, seed_capping=5, overlap_halo=0)
+                      seed_sampling=3, seed_capping=5, overlap_halo=0, batch=0)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda())
     res = []
     for ov in (0, 1):
@@ -131,7 +134,7 @@ def test_two_stream_schedule(lib, dtype):
     l = c["r"] * (1 + 2 ** -12)
     base = StepConfig(n_points=c["n"], s=c["n"], dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
                       n_e=c["n_e"], d=c["d"], k=c["k"], L=c["L"], edge_mode=Lib.EDGE_DIFF, dtype=dtype,
-                      seed_sampling=3, seed_capping=5)
+                      seed_sampling=3, seed_capping=5, batch=0)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda())
     outs, grads = [], []
     for streams in (1, 2, 2):
@@ -149,8 +152,9 @@ def test_two_stream_schedule(lib, dtype):
         assert np.array_equal(grads[1][n], grads[2][n]), n
 
 
+@pytest.mark.parametrize("batch", [0, 1], ids=["per-part", "union"])
 @pytest.mark.parametrize("mode", [decomp.DETACH, decomp.REVERSE_ADD], ids=["detach", "reverse_add"])
-def test_step_gradients_match_oracle_bf16_paper_form(lib, mode):
+def test_step_gradients_match_oracle_bf16_paper_form(lib, mode, batch):
     """The benchmarked machinery (BF16 tensor-core mode, 4 sub-domains,
     sub-domains on 2 CUDA streams in DETACH, d = 64, k = 256, 3 layers with a
     halo refresh after each) in the paper's form of the layer (Eq. (ii) with
@@ -161,14 +165,15 @@ def test_step_gradients_match_oracle_bf16_paper_form(lib, mode):
     ReLU decisions are those inside kappa_phi, which both sides take on the
     same rounded operands."""
     c = _case(seed=65, n=700, d=64, k=256, L=3, n_e=24, r=0.1)
-    got = _gpu(c, mode, 1, streams=2, root=1, act=0)
+    got = _gpu(c, mode, 1, streams=2, root=1, act=0, batch=batch)
     want = _oracle(c, mode, bf16=True, root=1, act=0)
     errs = {n: nerr(got[n], want[n]) for n in NAMES if n != "W_root"}
     assert max(errs.values()) <= 2e-2, errs
 
 
+@pytest.mark.parametrize("batch", [0, 1], ids=["per-part", "union"])
 @pytest.mark.parametrize("mode", [decomp.DETACH, decomp.REVERSE_ADD], ids=["detach", "reverse_add"])
-def test_step_gradients_match_oracle_bf16_gno_one_layer(lib, mode):
+def test_step_gradients_match_oracle_bf16_gno_one_layer(lib, mode, batch):
     """GNO form (dense root, ReLU sigma; the benchmark's form), 4 sub-domains
     on 2 streams, one layer: the upstream gradient is zeroed where the
     oracle's pre-activation lies within 2% of its spread from the ReLU kink
@@ -183,7 +188,7 @@ def test_step_gradients_match_oracle_bf16_gno_one_layer(lib, mode):
     sub = Gm[ids]
     sub[np.abs(pre) < 2e-2 * pre.std()] = 0.0
     Gm[ids] = sub
-    got = _gpu(c, mode, 1, streams=2, G=Gm)
+    got = _gpu(c, mode, 1, streams=2, G=Gm, batch=batch)
     want = _oracle(c, mode, bf16=True, G=Gm)
     errs = {n: nerr(got[n], want[n]) for n in NAMES}
     assert max(errs.values()) <= 2e-2, errs

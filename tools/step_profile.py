@@ -1,6 +1,6 @@
 """Kernel times of the bench step in situ (2 streams, warm caches): CUPTI via
 torch.profiler over a few steps; per-kernel totals per step and the share of
-the step.  Development tool.  python tools/step_profile.py [config] [steps]"""
+the step.  Development tool.  python tools/step_profile.py [config] [steps] [streams]"""
 import collections
 import sys
 
@@ -17,6 +17,9 @@ cname = sys.argv[1] if len(sys.argv) > 1 else "darcy"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 dev = torch.device("cuda:0")
 cfg, sc, coords, attr = bench.step_config(cname, 1, "bf16")
+if len(sys.argv) > 3:
+    import dataclasses
+    sc = dataclasses.replace(sc, streams=int(sys.argv[3]))
 d_e = (sc.dim + sc.n_attr) * (1 if sc.edge_mode == 0 else 2)
 W = synth.weights(d_e, sc.d, sc.d, sc.k)
 T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)

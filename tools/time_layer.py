@@ -1,7 +1,7 @@
 """One Darcy sub-domain (BASELINE configs[1] shapes), BF16 layer forward and
 backward: per-kernel times of the fused edge kernels (library probe: CUDA
 events on the launching stream) and whole-call times, median over reps.
-Development tool (not on the product path).  python tools/time_layer.py [reps] [config]"""
+Development tool (not on the product path).  python tools/time_layer.py [reps] [config] [P]"""
 import statistics
 import sys
 
@@ -21,7 +21,7 @@ s = cfg.s or n
 ids = pipeline.sample_nodes(n, s, synth.BASE_SEED + 3, dev).long()
 cs = torch.from_numpy(coords).to(dev)[ids].contiguous()
 at = torch.from_numpy(attr).to(dev)[ids].contiguous()
-P = max(cfg.P, 1)
+P = int(sys.argv[3]) if len(sys.argv) > 3 else max(cfg.P, 1)
 subs, _ = pipeline.decompose(cs, ids, at, P, cfg.r, cfg.r, [0])
 mode = L.EDGE_DIFF if cfg.edge_mode == "diff" else L.EDGE_CONCAT
 sd = pipeline.build_graph(subs[0], cfg.r, cfg.n_e, 7, mode, want_f32=False)

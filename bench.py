@@ -50,6 +50,8 @@ def parse():
                     help="skip every halo refresh (PAPER.md:209 no-communication ablation; halos stay stale)")
     ap.add_argument("--halo-ratio", type=float, default=1.0, help="overlap length l = ratio * r (Table 4 sweep)")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the timed run")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="build each step's graph inside the step (no prefetch of the next step's graph)")
     return ap.parse_args()
 
 
@@ -281,7 +283,8 @@ def oracle_parity(hp, sc, cfg_name, world, n_rows=96):
       * partition (a3): the local order of this rank's first sub-domain, bit-exact;
       * radius graph (a2): n_rows hash-selected destination rows, bit-exact;
       * layer forward (a4 + a5): layer 0 of that sub-domain on those rows,
-        re-run through the same HotPath.forward the timed steps use;
+        re-run through the same HotPath.forward the timed steps use (the
+        union graph of all local sub-domains when the step runs that way);
       * layer backward (a7): layer 0 with the upstream gradient restricted to
         those rows (masked upstream), all weight gradients and dv;
     within the north_star's tolerance (1e-5 F32, 2e-2 BF16, normwise-inf)."""
@@ -336,7 +339,18 @@ def oracle_parity(hp, sc, cfg_name, world, n_rows=96):
     dev = hp.dev
     v0_d = torch.from_numpy(np.ascontiguousarray(v0_all)).to(dev)
     acts, _ = hp.forward(v0_d)
-    out_g = acts[1][0][: sd.n_own].float().cpu().numpy()[rows]
+    # union-graph mode (a8): sub-domain 0's owned rows are union rows [0, n_own)
+    # and its halo rows start at bat.halo_off[0]
+    bat = getattr(hp, "bat", None)
+    if bat is not None:
+        v_in, a_out, ws_f, bkey = acts[0], acts[1], hp.ws[("fwd", 0, "B")], ("bwd", "B")
+        gsrc = bat
+        loc_map = np.concatenate([np.arange(sd.n_own), bat.halo_off[0] + np.arange(sd.n_halo)])
+    else:
+        v_in, a_out, ws_f, bkey = acts[0][0], acts[1][0], hp.ws[("fwd", 0, 0)], ("bwd", 0)
+        gsrc = sd
+        loc_map = np.arange(sd.n_loc)
+    out_g = a_out[: sd.n_own].float().cpu().numpy()[rows]
     res["fwd_err"] = _nerr(out_g, out_o)
     # masked-upstream backward of layer 0 (kinks within 2% of the spread masked, as in the tests)
     Gm = G_all[lr][rows].copy()
@@ -345,17 +359,17 @@ def oracle_parity(hp, sc, cfg_name, world, n_rows=96):
     dv_o, _, g_o = layer.layer_bwd(desc, Wo, vloc, eo, rp, col + m, Gm, want_de=False)
     dv_o_full = dv_o[m:].copy()
     dv_o_full[rows] += dv_o[:m]
-    Gd = torch.zeros((sd.n_own, sc.d), dtype=torch.float32, device=dev)
+    Gd = torch.zeros((gsrc.n_own, sc.d), dtype=torch.float32, device=dev)
     Gd[torch.from_numpy(rows).to(dev)] = torch.from_numpy(Gm.astype(np.float32)).to(dev)
-    gv = torch.zeros((sd.n_loc, sc.d), dtype=torch.float32, device=dev)
+    gv = torch.zeros((gsrc.n_loc, sc.d), dtype=torch.float32, device=dev)
     grads = {n: torch.zeros_like(t) for n, t in hp.W.items()}
-    ein = sd.e16 if bf16 else sd.e32
-    bws = hp._ws(("bwd", 0), L.layer_bwd_workspace_size(hp.desc, sd.n_own, sd.n_loc, sd.n_edges))
-    L.layer_bwd(hp.desc, hp.W, hp.packed, acts[0][0], ein, sd.row_ptr, sd.col_idx, sd.csc_perm, sd.csc_ptr,
-                sd.n_own, sd.n_loc, 0, sd.n_own, Gd, gv, None, grads, hp.ws[("fwd", 0, 0)], bws,
-                row_ptr_host=sd.row_ptr_host)
+    ein = gsrc.e16 if bf16 else gsrc.e32
+    bws = hp._ws(bkey, L.layer_bwd_workspace_size(hp.desc, gsrc.n_own, gsrc.n_loc, gsrc.n_edges))
+    L.layer_bwd(hp.desc, hp.W, hp.packed, v_in, ein, gsrc.row_ptr, gsrc.col_idx, gsrc.csc_perm, gsrc.csc_ptr,
+                gsrc.n_own, gsrc.n_loc, 0, gsrc.n_own, Gd, gv, None, grads, ws_f, bws,
+                row_ptr_host=gsrc.row_ptr_host)
     torch.cuda.synchronize()
-    errs = {"dv": _nerr(gv.cpu().numpy(), dv_o_full)}
+    errs = {"dv": _nerr(gv.cpu().numpy()[loc_map], dv_o_full)}
     for nm, t in grads.items():
         errs[nm] = _nerr(t.cpu().numpy(), g_o[nm])
     res["bwd_err_max"] = max(errs.values())
@@ -461,18 +475,32 @@ def main():
     hp = HotPath(sc, W, dev, rank, world)  # world > 1: the library NCCL context (dsmpnn_ctx_create)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def step(inp):
-        flush.zero_()
-        return hp.step(inp["coords"], inp["attr"], inp["v0"], inp["G"])
+    pipelined = not args.no_pipeline
 
-    for _ in range(args.warmup):
-        step(devin)
+    def step(inp, nxt=None, ready=None, serial=False):
+        """One step.  Pipelined (default): the graph of this step was built
+        during the previous step (HotPath.step_pipelined) and, if `nxt` is
+        given, the next step's graph is built while this step's layers run.
+        A run of K pipelined steps does K builds and K layer passes."""
+        flush.zero_()
+        if serial or not pipelined:
+            return hp.step(inp["coords"], inp["attr"], inp["v0"], inp["G"])
+        return hp.step_pipelined(inp["coords"], inp["attr"], inp["v0"], inp["G"],
+                                 next_inputs=(nxt["coords"], nxt["attr"]) if nxt is not None else None,
+                                 next_ready=ready)
+
+    def run_steps(n, marks=None):
+        for k_ in range(n):
+            step(devin, devin if k_ + 1 < n else None)
+            if marks is not None and k_ < n - 1:
+                marks[k_].record(torch.cuda.current_stream())
+
+    run_steps(args.warmup)
     # settle: at least 8 untimed steps in all (W + extra) before timing; with
     # fewer, the first timed steps of a fresh process were occasionally 10-30 %
     # slow (two-stream schedule not yet steady); reported as warmup_extra
     warmup_extra = max(0, 8 - args.warmup)
-    for _ in range(warmup_extra):
-        step(devin)
+    run_steps(warmup_extra)
     torch.cuda.synchronize()
     E_local = hp.n_edges
     # dominant kernel of the step: the fused edge backward (BF16), the kappa-MLP
@@ -502,10 +530,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     e0.record(st)
-    for k_ in range(args.steps):
-        step(devin)
-        if k_ < args.steps - 1:
-            marks[k_].record(st)
+    run_steps(args.steps, marks)
     e1.record(st)
     torch.cuda.synchronize()
     bounds = [e0] + marks + [e1]
@@ -542,13 +567,14 @@ def main():
         load_inputs(0)
         for s_ in range(n_steps):
             i = s_ % 2
+            last = s_ + 1 == n_steps
+            if not last:  # the next step's inputs (its graph is built from them during this step)
+                load_inputs(1 - i, after=used[1 - i] if s_ >= 1 else None)
             st.wait_event(loaded[i])
-            grads = step(dbuf[i])
+            grads = step(dbuf[i], None if last else dbuf[1 - i], None if last else loaded[1 - i])
             for n, t in grads.items():
                 gstage[i][n].copy_(t, non_blocking=True)
             used[i].record(st)
-            if s_ + 1 < n_steps:
-                load_inputs(1 - i, after=used[1 - i] if s_ >= 1 else None)
             with torch.cuda.stream(cpy):
                 cpy.wait_event(used[i])
                 for n, t in gstage[i].items():
@@ -592,20 +618,26 @@ def main():
     # roofline probe of the dominant kernel with the sub-domains on one stream:
     # with 2 streams its launches overlap other kernels, so their event
     # durations measure the schedule, not the kernel (both are reported)
+    # (with the pipeline, the next step's graph build overlaps it the same way)
     probe_ms_step, probe_n_step = probe_ms, probe_n
-    if sc.streams > 1:
+    serial_ms = None
+    if sc.streams > 1 or pipelined:
         hp.cfg = dataclasses.replace(hp.cfg, streams=1)
-        step(devin)
+        step(devin, serial=True)
         torch.cuda.synchronize()
         L.probe_begin(probe_id, 64 * args.steps * sc.L * len(hp.subs) + 64)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(st)
         for _ in range(args.steps):
-            step(devin)
+            step(devin, serial=True)
+        s1.record(st)
         torch.cuda.synchronize()
         probe_ms, probe_n = L.probe_end()
+        serial_ms = s0.elapsed_time(s1) / args.steps
         hp.cfg = dataclasses.replace(hp.cfg, streams=sc.streams)
     # kernels of one step (CUPTI trace); after the timed regions so that no
     # profiler state is live while they run
-    launches, lib_other = count_our_launches(lambda: step(devin))
+    launches, lib_other = count_our_launches(lambda: step(devin, serial=True))
 
     # ---- graph build alone (sample + partition + radius graph + attributes + CSC), for reference
     torch.cuda.synchronize()
@@ -679,6 +711,9 @@ def main():
                        "l2": "256 MB buffer zeroed at the start of every step, inside the timed region",
                        "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd",
                        "streams": sc.streams,
+                       "pipeline": ("the graph of step t+1 is built on a second stream while step t's layers run "
+                                    "(Alg. 1 builds graphs ahead of the training loop); K steps = K builds + K "
+                                    "layer passes" if pipelined else "off: each step builds its graph first"),
                        "comm": "library NCCL context (dsmpnn_halo_exchange)" if world > 1 else
                                "sub-domains on one device: halo = device copies"},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
@@ -692,9 +727,10 @@ def main():
                                          if tensor_tflops else None),
                          "per_launch_ms": per_launch_ms, "launches": probe_n,
                          "share_of_step": probe_ms / (ms * args.steps), "peak_source": src,
-                         "probe": ("separate pass of the same steps with the sub-domains on one stream "
-                                   "(the kernel alone); in the timed 2-stream region its launches overlap "
-                                   "other kernels" if sc.streams > 1 else "timed region"),
+                         "probe": ("separate pass of the same steps, unpipelined, sub-domains on one stream "
+                                   "(the kernel alone); in the timed region its launches overlap the next "
+                                   "step's graph build / other streams" if (sc.streams > 1 or pipelined)
+                                   else "timed region"),
                          "per_launch_ms_in_timed_region": probe_ms_step / max(1, probe_n_step)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
@@ -712,6 +748,7 @@ def main():
                             "what": "L x (fwd + halo) + L x bwd on the built graphs (SURVEY D.1 t_iter), "
                                     "max over ranks; no-comm = the same with every halo refresh skipped"},
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
+            "ms_per_step_unpipelined": serial_ms,
             "gpu_launches": launches * args.steps,
             "warmup_extra": warmup_extra,
             "gpu_launches_cub": lib_other * args.steps,

@@ -449,6 +449,81 @@ class HotPath:
         self.build(coords, attr)
         return self.forward_backward(v0, G)
 
+    # ------------------------------------------------------ pipelined steps --
+    # Alg. 1 builds every sample's graph (lines 391-397) in a loop of its own,
+    # ahead of the training loop (the trainloader).  step_pipelined keeps that
+    # order within a run of steps: while the layers of step t run on the
+    # current stream, the host builds the graph of step t+1 on a separate
+    # high-priority stream, so the build's host synchronisations (plan sizes,
+    # edge counts) wait for the build's own kernels only and its kernels fill
+    # the SMs the layer kernels leave idle.  Every step still does its full
+    # build and its full layer work.
+    def _build_stream(self):
+        if getattr(self, "_bstream", None) is None:
+            _, hi = torch.cuda.Stream.priority_range()
+            self._bstream = torch.cuda.Stream(self.dev, priority=hi)
+        return self._bstream
+
+    def _graph_state(self):
+        return (self.subs, getattr(self, "bat", None), getattr(self, "ids", None), getattr(self, "plan", None))
+
+    def _set_graph_state(self, st):
+        self.subs, self.bat, self.ids, self.plan = st
+
+    @staticmethod
+    def _state_tensors(st):
+        subs, bat, ids, plan = st
+        objs = list(subs) + ([bat] if bat is not None else [])
+        out = [ids] + (list(plan.values()) if plan else [])
+        for o in objs:
+            out += [v for v in vars(o).values() if isinstance(v, torch.Tensor) and v.is_cuda]
+        return [t for t in out if isinstance(t, torch.Tensor) and t.is_cuda]
+
+    def prefetch(self, coords, attr, after=()):
+        """Enqueue the graph build of the next step on the build stream (it
+        first waits for the events in `after`, e.g. the inputs' copy); the
+        host returns when the build's host-side work is done.  The next
+        step_pipelined call adopts the result."""
+        bs = self._build_stream()
+        for ev in after:
+            if ev is not None:
+                bs.wait_event(ev)
+        coords.record_stream(bs)
+        attr.record_stream(bs)
+        cur = self._graph_state()
+        try:
+            with torch.cuda.stream(bs):
+                self.build(coords, attr)
+                done = torch.cuda.Event()
+                done.record(bs)
+            self._next = (self._graph_state(), done)
+        finally:
+            self._set_graph_state(cur)
+
+    def step_pipelined(self, coords, attr, v0, G, next_inputs=None, next_ready=None):
+        """One step (build + forward_backward) whose graph was prefetched by
+        the previous call, or is built now; then, if next_inputs = (coords,
+        attr) is given, the next step's graph is built on the build stream
+        (after next_ready, an event, if given) while this step's layers run.
+        Returns the gradients as forward_backward does."""
+        main = torch.cuda.current_stream(self.dev)
+        nxt = getattr(self, "_next", None)
+        if nxt is not None:
+            st, done = nxt
+            self._next = None
+            main.wait_event(done)
+            for t in self._state_tensors(st):  # used on this stream from now on
+                t.record_stream(main)
+            self._set_graph_state(st)
+        else:
+            self.build(coords, attr)
+        fence = torch.cuda.Event()
+        fence.record(main)  # the next build may reuse the graph workspaces once this step's build is done
+        grads = self.forward_backward(v0, G)
+        if next_inputs is not None:
+            self.prefetch(next_inputs[0], next_inputs[1], after=(fence, next_ready))
+        return grads
+
 
 class TrainStep:
     """one DS-MPNN training step (PAPER.md eqs. (i)-(iv),

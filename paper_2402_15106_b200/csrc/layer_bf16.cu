@@ -203,6 +203,17 @@ constexpr int kMaxSplitsFwd = 16;
 // whose last round is fullest (fewest idle SMs), ties to fewer splits
 static int node_gemm_splits(int64_t nR, int64_t kp, int *real_out) {
   const int64_t mt = ceil_div(nR, 128), nkb = ceil_div(kp, 64);
+  // enough row tiles to occupy most SMs: one CTA streams a tile's whole K
+  // (no partial sums to write and re-read; the S~ stream runs at the rate of
+  // the B1 GEMM, which has the same shape transposed)
+  static const int64_t min_tiles = [] {
+    const char *e = getenv("DSMPNN_NODE_GEMM_NOSPLIT_TILES");
+    return e ? atoll(e) : (int64_t)(kNumSMs * 3 / 4);
+  }();
+  if (mt >= min_tiles) {
+    *real_out = 1;
+    return 1;
+  }
   int best = 4, best_real = 4;
   double best_eff = -1.0;
   for (int sp = 4; sp <= kMaxSplitsFwd; ++sp) {

@@ -67,11 +67,18 @@ struct TG {
   // BRES: the whole B (N <= BN, K <= NKB_RES * BK) stays in SMEM for every
   // tile; only A streams through the stages
   static constexpr int NKB_RES = 4;
-  static constexpr int STAGES = BRES ? 2 : (BN >= 256 ? (E16 ? 3 : 4) : (BN >= 128 ? 5 : 6));
+  // epilogue warps: 4 (one per TMEM lane quarter); the streaming bf16
+  // epilogue (E16 without a resident B) uses 8 -- two per lane quarter taking
+  // alternate 64-column chunks -- as one warp per scheduler cannot hide the
+  // latency of its TMEM-load / convert / store chain (the B2 GEMM of the
+  // backward is bound by that chain, not by HBM or the tensor pipe)
+  static constexpr int EPI = (E16 && !BRES) ? 8 : 4;
+  static constexpr int THREADS = 64 + 32 * EPI;
+  static constexpr int STAGES = BRES ? 2 : (BN >= 256 ? (E16 ? 2 : 4) : (BN >= 128 ? (E16 ? 3 : 5) : (E16 ? 4 : 6)));
   static constexpr int B_STAGE_BYTES = BRES ? 0 : B_BYTES;
   static constexpr int B_RES_BYTES = BRES ? NKB_RES * B_BYTES : 0;
   // bf16 epilogue staging per epilogue warp: 2 output buffers + 2 mask buffers (32 rows x 128 B each)
-  static constexpr int STG_BYTES = E16 ? 4 * 4 * 4096 : 0;
+  static constexpr int STG_BYTES = E16 ? EPI * 4 * 4096 : 0;
   static constexpr int B_INNER = B_MN ? (BN < 64 ? BN : 64) : 64;  // box inner elements for B
   static constexpr int B_ROW = B_INNER * 2;                          // bytes per smem row of B (MN-major)
   static constexpr uint32_t ACC_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
@@ -84,7 +91,7 @@ struct TG {
 // 2..5 = epilogue; the accumulator is double-buffered in TMEM so the epilogue
 // of tile i overlaps the mainloop of tile i+1.
 template <int BN, bool A_MN, bool B_MN, bool E16, bool BRES>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(TG<BN, A_MN, B_MN, E16, BRES>::THREADS, 1)
     tgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                  const __grid_constant__ CUtensorMap tout, const __grid_constant__ CUtensorMap tmask, int64_t M,
                  int64_t N, int64_t K, int kb_per_split, const TgemmArgs ep, int splits) {
@@ -98,8 +105,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t *empty = full + T::STAGES;
   uint64_t *tfull = empty + T::STAGES;   // [2]
   uint64_t *tempty = tfull + 2;          // [2]
-  uint64_t *mbar = tempty + 2;           // [4][2] mask loads, two buffers per epilogue warp
-  uint64_t *bres = mbar + 8;             // resident B loaded (BRES)
+  uint64_t *mbar = tempty + 2;           // [EPI][2] mask loads, two buffers per epilogue warp
+  uint64_t *bres = mbar + 2 * T::EPI;    // resident B loaded (BRES)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,9 +121,9 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 4);
+      tc::mbar_init(&tempty[a], T::EPI);
     }
-    for (int a = 0; a < 8; ++a) tc::mbar_init(&mbar[a], 1);
+    for (int a = 0; a < 2 * T::EPI; ++a) tc::mbar_init(&mbar[a], 1);
     tc::mbar_init(bres, 1);
     tc::fence_mbar_init();
     tc::tma_prefetch(&ta);
@@ -227,6 +234,9 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int g = warp & 3;  // TMEM lane group accessible to this warp
+    const int ew = warp - 2;                    // epilogue warp index: staging buffers, mask barriers
+    constexpr int CSTEP = T::EPI / 4;           // 64-column chunks: this warp takes h, h + CSTEP, ...
+    const int h = ew / 4;
     uint32_t li = 0, ocount = 0;
     float csum[BN / 64 > 0 ? BN / 64 : 1][2] = {};
     // mask tiles are prefetched one 64-column chunk ahead (two buffers)
@@ -236,11 +246,11 @@ __global__ void __launch_bounds__(192, 1)
       int nkb_, z_;
       tile_coords(t, m0, n0, kb0, nkb_, z_);
       if (n0 + c64 * 64 >= N) return;
-      tc::mbar_expect_tx(&mbar[g * 2 + (q & 1)], 4096);
-      tc::tma_load_2d(sStg + (g * 4 + 2 + (q & 1)) * 4096, &tmask, &mbar[g * 2 + (q & 1)],
+      tc::mbar_expect_tx(&mbar[ew * 2 + (q & 1)], 4096);
+      tc::tma_load_2d(sStg + (ew * 4 + 2 + (q & 1)) * 4096, &tmask, &mbar[ew * 2 + (q & 1)],
                       (int32_t)(n0 + c64 * 64), (int32_t)(m0 + g * 32));
     };
-    mask_load(blockIdx.x, 0, 0);
+    mask_load(blockIdx.x, h, 0);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
       int64_t m0, n0, kb0;
       int nkb, z;
@@ -284,13 +294,13 @@ __global__ void __launch_bounds__(192, 1)
         const float sc = (ep.row_scale && row < M) ? ep.row_scale[row] : 1.f;
         const int nch = (int)((N - n0 + 63) / 64) < BN / 64 ? (int)((N - n0 + 63) / 64) : BN / 64;
 #pragma unroll 1
-        for (int c64 = 0; c64 < nch; ++c64) {
+        for (int c64 = h; c64 < nch; c64 += CSTEP) {
           const int64_t ncol = n0 + c64 * 64;
-          uint8_t *ost = sStg + (g * 4 + (ocount & 1)) * 4096;
-          uint8_t *mst = sStg + (g * 4 + 2 + (ocount & 1)) * 4096;
-          // prefetch the next chunk's mask (this tile's next chunk, else the next tile's first)
-          if (c64 + 1 < nch) mask_load(t, c64 + 1, ocount + 1);
-          else mask_load(t + gridDim.x, 0, ocount + 1);
+          uint8_t *ost = sStg + (ew * 4 + (ocount & 1)) * 4096;
+          uint8_t *mst = sStg + (ew * 4 + 2 + (ocount & 1)) * 4096;
+          // prefetch this warp's next chunk's mask (this tile's, else the next tile's first)
+          if (c64 + CSTEP < nch) mask_load(t, c64 + CSTEP, ocount + 1);
+          else mask_load(t + gridDim.x, h, ocount + 1);
           uint32_t v[64];
           tc::tmem_ld32(dcol + (uint32_t)(c64 * 64), *reinterpret_cast<uint32_t (*)[32]>(&v[0]));
           tc::tmem_ld32(dcol + (uint32_t)(c64 * 64 + 32), *reinterpret_cast<uint32_t (*)[32]>(&v[32]));
@@ -299,7 +309,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = (nkb > 0 && row < M) ? __uint_as_float(v[j]) * sc : 0.f;
           if (ep.mask16) {
-            tc::mbar_wait(&mbar[g * 2 + (ocount & 1)], (ocount >> 1) & 1);
+            tc::mbar_wait(&mbar[ew * 2 + (ocount & 1)], (ocount >> 1) & 1);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const uint4 mv = *reinterpret_cast<const uint4 *>(mst + tc::sw128_off(lane, c));
@@ -386,7 +396,9 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   if (per_sm > 2) per_sm = 2;
   if (per_sm * T::TMEM_COLS > 512) per_sm = 512 / T::TMEM_COLS;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm));
-  kern<<<grid, 192, T::SMEM, s>>>(ta, tb, tout, tmask, a.M, a.N, a.K, kbps, a, splits);
+  DS_CHECK_ARG(T::EPI == 4 || a.colsum_part == nullptr, DSMPNN_ERR_UNSUPPORTED,
+               "tgemm: column sums need the resident-B bf16 epilogue");
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(ta, tb, tout, tmask, a.M, a.N, a.K, kbps, a, splits);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

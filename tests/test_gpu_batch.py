@@ -163,3 +163,35 @@ def test_union_step_matches_per_part(L, dtype, mode):
     assert nerr(o1, o0) <= 1e-5
     for n in NAMES:
         assert nerr(g1[n], g0[n]) <= 1e-5, n
+
+
+@pytest.mark.parametrize("batch", [0, 1], ids=["per-part", "union"])
+def test_pipelined_steps_match_serial_steps(L, batch):
+    """HotPath.step_pipelined (the next step's graph built on the build
+    stream while this step's layers run) gives, step by step, bitwise the
+    gradients of HotPath.step on the same inputs -- also when consecutive
+    steps have different point clouds (the prefetched graph is the next
+    step's, not the current one's)."""
+    from paper_2402_15106_b200 import _lib as Lib
+    from paper_2402_15106_b200.api import HotPath, StepConfig
+    from test_gpu_grad_modes import _case
+    cs = [_case(seed=91 + i, d=64, k=256) for i in range(3)]
+    c = cs[0]
+    l = c["r"] * (1 + 2 ** -12)
+    sc = StepConfig(n_points=c["n"], s=c["n"] - 50, dim=c["dim"], n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l,
+                    n_e=c["n_e"], d=c["d"], k=c["k"], L=2, edge_mode=Lib.EDGE_DIFF, dtype=Lib.BF16,
+                    seed_sampling=3, seed_capping=5, batch=batch)
+    inp = [[T(x[n]) for n in ("x", "a", "v0", "G")] for x in (cs[0], cs[1], cs[2], cs[1])]
+    hs = HotPath(sc, c["W"], cuda())
+    want = []
+    for x in inp:
+        g = hs.step(*x)
+        want.append({n: N(g[n]).copy() for n in NAMES})
+    hp = HotPath(sc, c["W"], cuda())
+    for i, x in enumerate(inp):
+        nxt = inp[i + 1][:2] if i + 1 < len(inp) else None
+        g = hp.step_pipelined(*x, next_inputs=nxt)
+        got = {n: N(g[n]).copy() for n in NAMES}
+        for n in NAMES:
+            assert np.array_equal(got[n], want[i][n]), (i, n)
+    assert getattr(hp, "_next", None) is None

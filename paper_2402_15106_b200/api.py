@@ -545,13 +545,19 @@ class TrainStep:
     CONV = ("W1", "b1", "W2", "b2", "W3", "b3", "W_root", "b")
 
     def __init__(self, cfg: StepConfig, params: dict, hops: int, device, rank=0, world=1, group=None,
-                 optimizer="sgd", lr=1e-3, comm=None):
+                 optimizer="sgd", lr=1e-3, comm=None, decoded_exchange=True):
+        """decoded_exchange: after every hop's decoder, also refresh the halo
+        rows of the decoded values from their owners (Alg. 1 :412, the second
+        per-hop Comm); the values equal the local decode of the refreshed
+        latent rows bit for bit (reading R26), so this models the paper's
+        communication, not a different result."""
         import dataclasses
         cfg = dataclasses.replace(cfg, root=L.ROOT_IDENTITY, act=L.ACT_IDENTITY, grad_mode=DETACH, L=hops, batch=0)
         conv = dict(params["conv"])
         conv.setdefault("W_root", np.zeros((cfg.d, cfg.d), np.float32))  # identity root: unused
         self.hp = HotPath(cfg, conv, device, rank, world, group, comm=comm)
         self.dev, self.hops, self.opt, self.lr = device, hops, optimizer, lr
+        self.decoded_exchange = decoded_exchange
         T = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32).to(device)
         self.enc = [T(x) for Wl, bl in params["enc"] for x in (Wl, bl)]
         self.dec = [T(x) for Wl, bl in params["dec"] for x in (Wl, bl)]
@@ -618,6 +624,10 @@ class TrainStep:
                 uq, cache = self._mlp(self.dec, new[q])
                 dec_cache.append(cache)
                 u.append(uq)
+            if self.decoded_exchange:  # Alg. 1 :412 v^l <- Comm(i_b, Omega, v^l)
+                hp.halo(u, L.F32)
+            for q, sd in enumerate(subs):
+                uq = u[q]
                 if c.dtype == L.F32:
                     en = torch.empty((max(sd.n_edges, 1), dim + n_attr), device=self.dev)
                     L.edge_features(L.EDGE_DIFF, sd.coords, uq, sd.row_ptr, sd.col_idx, sd.n_own, e32=en)

@@ -34,14 +34,14 @@ def _case(seed=91, n=500, P=4, hops=2, d=16, k=32, hid=24, r=0.12, n_e=12):
     return dict(x=x, a=a, params=params, v0=v0, Y=Y, n=n, P=P, hops=hops, d=d, k=k, r=r, n_e=n_e)
 
 
-def _step(c, optimizer="sgd", lr=1e-2, update=False, dtype=0):
+def _step(c, optimizer="sgd", lr=1e-2, update=False, dtype=0, decoded_exchange=True):
     from paper_2402_15106_b200 import _lib as L
     from paper_2402_15106_b200.api import StepConfig, TrainStep
     l = c["r"] * (1 + 2 ** -12)
     sc = StepConfig(n_points=c["n"], s=c["n"], dim=2, n_attr=1, nparts=c["P"], r=c["r"], overlap_l=l, n_e=c["n_e"],
                     d=c["d"], k=c["k"], L=c["hops"], edge_mode=L.EDGE_DIFF, dtype=dtype, seed_sampling=3,
                     seed_capping=5)
-    ts = TrainStep(sc, c["params"], c["hops"], cuda(), optimizer=optimizer, lr=lr)
+    ts = TrainStep(sc, c["params"], c["hops"], cuda(), optimizer=optimizer, lr=lr, decoded_exchange=decoded_exchange)
     T = lambda arr: torch.from_numpy(np.ascontiguousarray(arr)).to(cuda())
     ts.build(T(c["x"]), T(c["a"]))
     if update:
@@ -119,3 +119,19 @@ def test_train_step_bf16_loss_and_gradients(lib):
     for nm in ("W1", "b1", "W2", "b2", "W3", "b3", "b"):
         errs[nm] = nerr(g["conv"][nm].cpu().numpy(), wg["conv"][nm])
     assert max(errs.values()) <= 2e-2, errs
+
+
+@pytest.mark.parametrize("dtype", [0, 1], ids=["f32", "bf16"])
+def test_decoded_value_exchange_is_bitwise_the_local_decode(lib, dtype):
+    """Alg. 1 :412 (v^l <- Comm(i_b, Omega, v^l)): exchanging the decoded
+    halo values after each hop gives bitwise the loss and gradients of
+    decoding the refreshed latent halo rows locally (reading R26)."""
+    c = _case(seed=95) if dtype == 0 else _case(seed=95, d=64, k=256)
+    l0, g0, _ = _step(c, dtype=dtype, decoded_exchange=False)
+    l1, g1, _ = _step(c, dtype=dtype, decoded_exchange=True)
+    assert l0 == l1
+    for part in ("enc", "dec"):
+        for a, b in zip(g0[part], g1[part]):
+            assert torch.equal(a, b)
+    for n in g0["conv"]:
+        assert torch.equal(g0["conv"][n], g1["conv"][n]), n

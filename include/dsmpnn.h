@@ -210,8 +210,10 @@ dsmpnn_status dsmpnn_pack_weights(const dsmpnn_layer_desc *desc, const dsmpnn_we
  *            dsmpnn_layer_workspace_size(desc, n_dst, E); pass the same ws to bwd.
  * Errors: SHAPE for ROOT_IDENTITY with d_in != d_out or BF16 with d_e > 13 (the
  * padded edge columns 13..15 carry the first kappa layer bias, layer_bf16.cu);
- * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64} and k = 256,
- * and for a BF16 call whose rows [row_begin, row_end) include a row of more
+ * UNSUPPORTED for BF16 widths other than d_in = d_out in {32, 64} and k <= 256
+ * (the BF16 kernels run k = 256; a smaller k is zero-padded to 256 by
+ * dsmpnn_pack_weights: the padded units are exact zeros, the results and
+ * gradients are those of width k, the cost that of width 256), and for a BF16 call whose rows [row_begin, row_end) include a row of more
  * than 128 edges (the fused edge kernels tile whole rows; checked on the host
  * from row_ptr_host, else from row_ptr with a synchronising scan).
  * With DSMPNN_DEBUG set in the environment, layer_fwd / layer_bwd also

@@ -1,7 +1,8 @@
 // layer_bf16.cu - BF16 mode of the edge-conditioned convolution on the
 // tcgen05 tensor cores (sm_100a).  Formulation: DESIGN.md §6 ("aggregate
-// first", see layer.cu).  Widths supported: k = 256, d_in = d_out = D in
-// {32, 64}, d_e <= 13 (zero-padded to 16; columns 13..15 carry the bias b1).
+// first", see layer.cu).  Widths supported: k <= 256 (k < 256 zero-padded
+// to 256: same results, the k = 256 cost), d_in = d_out = D in {32, 64},
+// d_e <= 13 (zero-padded to 16; columns 13..15 carry the bias b1).
 //
 // Forward of rows [rb, re):
 //   1. fill kernel   : S~_aug[i][k*D + c] = mean_p v_j[c]  (the h~ = 1 row),
@@ -29,51 +30,62 @@
 
 namespace dsmpnn {
 
-// W1 packed [k x 16]: columns 0..d_e-1 the weights, columns 13, 14, 15 the
+// W1 packed [KH x 16]: columns 0..d_e-1 the weights, columns 13, 14, 15 the
 // bias b1 split into three bf16 terms (their fp32 sum is b1 to ~2^-24
 // relative: the MMA's fp32 accumulation adds it like an fp32 bias add), the
 // rest zero.  The fused edge kernels set e columns 13..15 to 1 in their SMEM
 // copy of the edge tile, so z1 = E W1^T already holds + b1 (edge_fwd3.cuh,
 // edge_bwd3.cuh); every other reader of W1 sees zeros there and adds b1 itself.
+// k < KH: units k..KH-1 get zero weights and biases (W1 rows, W2 rows and
+// columns, Theta~ rows), so their a1 and h are exactly 0 and they add exact
+// zeros to every product: the results are those of the width-k MLP.
 __global__ void pack_bf16_kernel(const float *__restrict__ W1, const float *__restrict__ b1,
-                                 const float *__restrict__ W2, const float *__restrict__ W3,
-                                 const float *__restrict__ b3, const float *__restrict__ Wr, int root_dense, int k,
-                                 int de, int di, int dout, int64_t kp, Packed p) {
-  int64_t n1 = (int64_t)k * 16, n2 = (int64_t)k * k, n3 = kp * dout;
-  int64_t total = n1 + n2 + n3;
+                                 const float *__restrict__ W2, const float *__restrict__ b2,
+                                 const float *__restrict__ W3, const float *__restrict__ b3,
+                                 const float *__restrict__ Wr, int root_dense, int k, int de, int di, int dout,
+                                 int64_t kp, Packed p) {
+  int64_t n1 = (int64_t)KH * 16, n2 = (int64_t)KH * KH, n3 = kp * dout;
+  int64_t total = n1 + n2 + n3 + 2 * KH;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     if (t < n1) {
       int r = (int)(t / 16), c = (int)(t % 16);
-      float w = c < de ? W1[(int64_t)r * de + c] : 0.f;
+      float w = (r < k && c < de) ? W1[(int64_t)r * de + c] : 0.f;
       if (c >= kBiasCol0) {  // b1 = t0 + t1 + t2, each a bf16 value (t2 absorbs the rest to ~2^-24 |b1|)
-        const float t0 = __bfloat162float(__float2bfloat16_rn(b1[r]));
-        const float t1 = __bfloat162float(__float2bfloat16_rn(b1[r] - t0));
-        w = c == kBiasCol0 ? t0 : c == kBiasCol0 + 1 ? t1 : b1[r] - t0 - t1;
+        const float bb = r < k ? b1[r] : 0.f;
+        const float t0 = __bfloat162float(__float2bfloat16_rn(bb));
+        const float t1 = __bfloat162float(__float2bfloat16_rn(bb - t0));
+        w = c == kBiasCol0 ? t0 : c == kBiasCol0 + 1 ? t1 : bb - t0 - t1;
       }
       p.W1[t] = __float2bfloat16_rn(w);
     } else if (t < n1 + n2) {
-      p.W2[t - n1] = __float2bfloat16_rn(W2[t - n1]);
-    } else {
+      const int64_t u = t - n1;
+      const int r = (int)(u / KH), c = (int)(u % KH);
+      p.W2[u] = __float2bfloat16_rn((r < k && c < k) ? W2[(int64_t)r * k + c] : 0.f);
+    } else if (t < n1 + n2 + n3) {
       int64_t u = t - n1 - n2;
       int64_t row = u / dout;  // Theta~_aug row
       int o = (int)(u - row * dout);
       int kap = (int)(row / di), c = (int)(row - (int64_t)kap * di);
       float val = 0.f;
       if (kap < k) val = W3[((int64_t)c * dout + o) * k + kap];
-      else if (kap == k) val = b3[(int64_t)c * dout + o];
-      else if (kap == k + 1 && root_dense) val = Wr[(int64_t)o * di + c];
+      else if (kap == KH) val = b3[(int64_t)c * dout + o];
+      else if (kap == KH + 1 && root_dense) val = Wr[(int64_t)o * di + c];
       __nv_bfloat16 bv = __float2bfloat16_rn(val);
       p.Th[row * dout + o] = bv;
-      // the forward S~ rows store the kappa < k block as [c][kappa]: K index
-      // c*k + kappa (edge kernel EPI_B); the bias and root blocks keep k*d_in + c
-      const int64_t kk = kap < k ? (int64_t)c * k + kap : row;
+      // the forward S~ rows store the kappa < KH block as [c][kappa]: K index
+      // c*KH + kappa (edge kernel EPI_B); the bias and root blocks keep KH*d_in + c
+      const int64_t kk = kap < KH ? (int64_t)c * KH + kap : row;
       p.ThT[(int64_t)o * kp + kk] = bv;
+    } else {
+      const int u = (int)(t - n1 - n2 - n3);
+      if (u < KH) p.b1[u] = u < k ? b1[u] : 0.f;
+      else p.b2[u - KH] = u - KH < k ? b2[u - KH] : 0.f;
     }
   }
 }
 
 dsmpnn_status bf16_check_desc(const dsmpnn_layer_desc &d) {
-  DS_CHECK_ARG(d.k == KH, DSMPNN_ERR_UNSUPPORTED, "layer BF16: k must be %d (got %d)", KH, d.k);
+  DS_CHECK_ARG(d.k >= 1 && d.k <= KH, DSMPNN_ERR_UNSUPPORTED, "layer BF16: 1 <= k <= %d (got %d)", KH, d.k);
   DS_CHECK_ARG(d.d_in == d.d_out && (d.d_in == 32 || d.d_in == 64), DSMPNN_ERR_UNSUPPORTED,
                "layer BF16: d_in = d_out in {32, 64} (got %d, %d)", d.d_in, d.d_out);
   DS_CHECK_ARG(d.d_e <= kBiasCol0, DSMPNN_ERR_SHAPE,
@@ -85,10 +97,12 @@ dsmpnn_status bf16_check_desc(const dsmpnn_layer_desc &d) {
 size_t bf16_packed_bytes(const dsmpnn_layer_desc &d) {
   Carver c(nullptr, 0);
   int64_t kp = kpad_of(d);
-  c.take<__nv_bfloat16>((int64_t)d.k * 16);
-  c.take<__nv_bfloat16>((int64_t)d.k * d.k);
+  c.take<__nv_bfloat16>((int64_t)KH * 16);
+  c.take<__nv_bfloat16>((int64_t)KH * KH);
   c.take<__nv_bfloat16>((int64_t)d.d_out * kp);
   c.take<__nv_bfloat16>(kp * d.d_out);
+  c.take<float>(KH);
+  c.take<float>(KH);
   return c.used();
 }
 
@@ -97,9 +111,11 @@ dsmpnn_status bf16_pack(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, voi
   Packed p = carve_packed(d, packed);
   int64_t kp = kpad_of(d);
   DS_CUDA(cudaMemsetAsync(p.ThT, 0, (size_t)d.d_out * kp * 2, s));
-  int64_t total = (int64_t)d.k * 16 + (int64_t)d.k * d.k + kp * d.d_out;
+  DS_CHECK_ARG(w.W1 && w.b1 && w.W2 && w.b2 && w.W3 && w.b3, DSMPNN_ERR_INVALID_ARG, "pack: a kappa weight is NULL");
+  int64_t total = (int64_t)KH * 16 + (int64_t)KH * KH + kp * d.d_out + 2 * KH;
   pack_bf16_kernel<<<(int)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(
-      w.W1, w.b1, w.W2, w.W3, w.b3, w.W_root, d.root == DSMPNN_ROOT_DENSE, d.k, d.d_e, d.d_in, d.d_out, kp, p);
+      w.W1, w.b1, w.W2, w.b2, w.W3, w.b3, w.W_root, d.root == DSMPNN_ROOT_DENSE, d.k, d.d_e, d.d_in, d.d_out, kp,
+      p);
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -298,8 +314,8 @@ dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   }
   // 2. fused kappa MLP + S formation
   if (ee > eb) {
-    if (D == 64) DS_TRY(launch_edge_fwd<64>(e, v, row_ptr, col, rb, re, eb, ee, pw, w.b1, w.b2, f.S, kp, s));
-    else DS_TRY(launch_edge_fwd<32>(e, v, row_ptr, col, rb, re, eb, ee, pw, w.b1, w.b2, f.S, kp, s));
+    if (D == 64) DS_TRY(launch_edge_fwd<64>(e, v, row_ptr, col, rb, re, eb, ee, pw, pw.b1, pw.b2, f.S, kp, s));
+    else DS_TRY(launch_edge_fwd<32>(e, v, row_ptr, col, rb, re, eb, ee, pw, pw.b1, pw.b2, f.S, kp, s));
   }
   // 3. node GEMM [S~_aug] . [Theta~_aug]  (split-K partials)
   int real = 1;

@@ -142,6 +142,17 @@ __global__ void unpack_bias_root_kernel(const float *__restrict__ dT, int k, int
   }
 }
 
+// dst[r * ld_dst + c] += src[r * ld_src + c] for r < rows, c < cols: the k
+// real units of a KH-wide gradient (k < KH, zero-padded kappa MLP)
+__global__ void add_block_kernel(const float *__restrict__ src, int64_t ld_src, float *__restrict__ dst,
+                                 int64_t ld_dst, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / cols, c = t - r * cols;
+    dst[r * ld_dst + c] += src[r * ld_src + c];
+  }
+}
+
 // dW1[r, c] += full[r, c] for c < d_e (full is [k x 16]); same for de rows
 __global__ void add_cols_kernel(const float *__restrict__ full, int64_t rows, int ld_full, int ncols,
                                 float *__restrict__ dst, int accumulate) {
@@ -178,32 +189,43 @@ struct BBwd {
   float *b1_part;          // [kNumSMs/2 x 2 x KH]  fused B5+B6 per-pair db1
   float *w2_part;          // [kNumSMs/2 x KH x KH] B4 (dw2.cuh) per-pair dW2
   float *b0_part;          // [ceil(n_dst/32) x D] B0 per-block column sums of ghat
+  // k < KH: the KH-wide W1, b1, W2, b2, W3 gradients (contiguous, zeroed per call)
+  float *gW1 = nullptr, *gb1 = nullptr, *gW2 = nullptr, *gb2 = nullptr, *gW3 = nullptr;
+  char *gpad_end = nullptr;
 };
 constexpr int kSplitsW = 64;
 static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst, int64_t E) {
   BBwd b;
   const int D = d.d_in;
-  int64_t kp = (int64_t)(d.k + 2) * D;
+  int64_t kp = (int64_t)(KH + 2) * D;
   kp = (kp + 63) / 64 * 64;
   b.gh = c.take<float>(n_dst * D);
   b.gh16 = c.take<__nv_bfloat16>(n_dst * D);
   b.inv_deg = c.take<float>(n_dst);
   b.dT = c.take<float>(kp * D);
-  b.dS = c.take<__nv_bfloat16>(n_dst * (int64_t)(d.k + 1) * D);
-  b.A1 = c.take<__nv_bfloat16>(E * d.k);
-  b.dZ2 = c.take<__nv_bfloat16>(E * d.k);
-  b.dZ1 = c.take<__nv_bfloat16>(E * d.k);
+  b.dS = c.take<__nv_bfloat16>(n_dst * (int64_t)(KH + 1) * D);
+  b.A1 = c.take<__nv_bfloat16>(E * KH);
+  b.dZ2 = c.take<__nv_bfloat16>(E * KH);
+  b.dZ1 = c.take<__nv_bfloat16>(E * KH);
   b.U = c.take<__nv_bfloat16>(E * D);
-  b.part = c.take<float>((int64_t)kSplitsW * d.k * d.k);
-  b.db2_part = c.take<float>((int64_t)kNumSMs * d.k);
-  b.db1_part = c.take<float>((int64_t)kColsumRows * d.k);
-  b.cs_ws = c.take<float>((int64_t)kColsumChunks * std::max(d.k, d.d_in));
-  b.dW1f = c.take<float>((int64_t)d.k * 16);
+  b.part = c.take<float>((int64_t)kSplitsW * KH * KH);
+  b.db2_part = c.take<float>((int64_t)kNumSMs * KH);
+  b.db1_part = c.take<float>((int64_t)kColsumRows * KH);
+  b.cs_ws = c.take<float>((int64_t)kColsumChunks * std::max(KH, d.d_in));
+  b.dW1f = c.take<float>((int64_t)KH * 16);
   b.de16 = c.take<float>(E * 16);
   b.w1_part = c.take<float>((int64_t)(kNumSMs / 2) * KH * 16);
   b.b1_part = c.take<float>((int64_t)kNumSMs * KH);
   b.w2_part = c.take<float>((int64_t)(kNumSMs / 2 + kDw2Groups) * KH * KH);
   b.b0_part = c.take<float>(ceil_div(std::max<int64_t>(n_dst, 1), 32) * D);
+  if (d.k < KH) {  // KH-wide gradients of the kappa MLP (k real units added to the caller's at the end)
+    b.gW1 = c.take<float>((int64_t)KH * d.d_e);
+    b.gb1 = c.take<float>(KH);
+    b.gW2 = c.take<float>((int64_t)KH * KH);
+    b.gb2 = c.take<float>(KH);
+    b.gW3 = c.take<float>((int64_t)d.d_in * d.d_out * KH);
+    b.gpad_end = c.take<char>(0);
+  }
   return b;
 }
 
@@ -404,10 +426,33 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   DS_CHECK_ARG(c.ok(), DSMPNN_ERR_CAPACITY, "layer_bwd: bwd workspace too small");
   BFwdView f = view_fwd(d, ws, n_dst);
   Packed pw = carve_packed(d, const_cast<void *>(w.packed));
-  const int D = d.d_in, k = d.k;
+  const int D = d.d_in, k = KH;  // k < KH: the padded units run too (their gradients are dropped below)
+  const bool padk = d.k < KH;
+  dsmpnn_grads g = gr;
+  if (padk) {
+    DS_CUDA(cudaMemsetAsync(b.gW1, 0, (size_t)(b.gpad_end - reinterpret_cast<char *>(b.gW1)), s));
+    g.W1 = gr.W1 ? b.gW1 : nullptr;
+    g.b1 = gr.b1 ? b.gb1 : nullptr;
+    g.W2 = gr.W2 ? b.gW2 : nullptr;
+    g.b2 = gr.b2 ? b.gb2 : nullptr;
+    g.W3 = gr.W3 ? b.gW3 : nullptr;
+  }
+  auto unpad = [&]() -> dsmpnn_status {
+    if (!padk) return DSMPNN_OK;
+    const int64_t kr = d.k, DD = (int64_t)d.d_in * d.d_out;
+    struct { const float *src; float *dst; int64_t ld_src, ld_dst, rows, cols; } parts[5] = {
+        {b.gW1, gr.W1, d.d_e, d.d_e, kr, d.d_e}, {b.gb1, gr.b1, KH, kr, 1, kr}, {b.gW2, gr.W2, KH, kr, kr, kr},
+        {b.gb2, gr.b2, KH, kr, 1, kr}, {b.gW3, gr.W3, KH, kr, DD, kr}};
+    for (auto &q : parts) {
+      if (!q.dst) continue;
+      add_block_kernel<<<grid_of(q.rows * q.cols), 256, 0, s>>>(q.src, q.ld_src, q.dst, q.ld_dst, q.rows, q.cols);
+      DS_LAUNCH_CHECK();
+    }
+    return DSMPNN_OK;
+  };
   const int64_t kp = kpad_of(d);
   const int64_t nR = re - rb, nE = ee - eb;
-  if (nR <= 0) return DSMPNN_OK;
+  if (nR <= 0) return unpad();
 
   // B0
   {
@@ -419,21 +464,21 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
       b0_bf16_kernel<32><<<nblk, 256, 0, s>>>(G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
                                               b.inv_deg, b.b0_part, dv);
     DS_LAUNCH_CHECK();
-    if (gr.b) DS_TRY(colsum(b.b0_part, nblk, D, D, gr.b, 1, s));
+    if (g.b) DS_TRY(colsum(b.b0_part, nblk, D, D, g.b, 1, s));
   }
   // B1: dTheta~_aug [kp x D] = S~_aug^T ghat  (K = rows)
-  if (gr.W3 || gr.b3 || gr.W_root) {
+  if (g.W3 || g.b3 || g.W_root) {
     TgemmArgs a{kp, D, nR, f.S + rb * kp, kp, true, b.gh16 + rb * D, D, true, b.dT, D, 1, 0, 0};
     DS_TRY(tgemm(a, s));
-    if (gr.W3) {
-      unpack_dw3_kernel<<<dim3(k / 32, D / 32, D), 256, 0, s>>>(b.dT, k, D, gr.W3);
+    if (g.W3) {
+      unpack_dw3_kernel<<<dim3(k / 32, D / 32, D), 256, 0, s>>>(b.dT, k, D, g.W3);
       DS_LAUNCH_CHECK();
     }
     unpack_bias_root_kernel<<<grid_of((int64_t)D * D), 256, 0, s>>>(
-        b.dT, k, D, gr.b3, d.root == DSMPNN_ROOT_DENSE ? gr.W_root : nullptr);
+        b.dT, k, D, g.b3, d.root == DSMPNN_ROOT_DENSE ? g.W_root : nullptr);
     DS_LAUNCH_CHECK();
   }
-  if (nE <= 0) return DSMPNN_OK;
+  if (nE <= 0) return unpad();
   // B2: dS_i = (ghat_i Theta~^T) / deg_i   -> bf16 [n_dst x (k+1)*D]
   {
     TgemmArgs a{nR, (int64_t)(k + 1) * D, D, b.gh16 + rb * D, D, false, pw.Th, D, false, nullptr, 0, 1, 0, 0};
@@ -449,24 +494,24 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   // B3: edge kernel
   int grid = 1;
   if (D == 64)
-    DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, !fused, &grid, s));
+    DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, &grid, s));
   else
-    DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, w.b1, w.b2, b, !fused, &grid, s));
-  DS_TRY(colsum(b.db2_part, grid, k, k, gr.b2, 1, s));
+    DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, &grid, s));
+  DS_TRY(colsum(b.db2_part, grid, k, k, g.b2, 1, s));
   // B4: dW2 += dz2^T a1   (M = k, N = k, K = edges)
-  if (gr.W2 && fused) {
-    DS_TRY(launch_dw2(pw, b.dZ2 + eb * k, e + eb * 16, nE, w.b1, b.w2_part, gr.W2, s));
-  } else if (gr.W2) {
+  if (g.W2 && fused) {
+    DS_TRY(launch_dw2(pw, b.dZ2 + eb * k, e + eb * 16, nE, pw.b1, b.w2_part, g.W2, s));
+  } else if (g.W2) {
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
     TgemmArgs a{k, k, nE, b.dZ2 + eb * k, k, true, b.A1 + eb * k, k, true, b.part, k, splits, (int64_t)k * k, 0};
     DS_TRY(tgemm(a, s));
     int64_t nkb = (nE + 63) / 64;
     int kbps = (int)std::max<int64_t>(1, ceil_div(nkb, splits));
     int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
-    DS_TRY(splitk_sum(b.part, real, (int64_t)k * k, k, k, k, gr.W2, k, 1, s));
+    DS_TRY(splitk_sum(b.part, real, (int64_t)k * k, k, k, k, g.W2, k, 1, s));
   }
   if (fused) {
-    DS_TRY(launch_dz1w1(pw, b.dZ2 + eb * k, e + eb * 16, nE, w.b1, b.w1_part, b.b1_part, d.d_e, gr.W1, gr.b1, s));
+    DS_TRY(launch_dz1w1(pw, b.dZ2 + eb * k, e + eb * 16, nE, pw.b1, b.w1_part, b.b1_part, d.d_e, g.W1, g.b1, s));
   } else {
     // B5: dz1 = (dz2 W2) * [a1 > 0]  (bf16), column sums -> db1
     {
@@ -479,10 +524,10 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
       a.b_resident = true;
       DS_CUDA(cudaMemsetAsync(b.db1_part, 0, (size_t)kColsumRows * k * sizeof(float), s));
       DS_TRY(tgemm(a, s));
-      DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, gr.b1, 1, b.cs_ws, s));
+      DS_TRY(colsum_ws(b.db1_part, kColsumRows, k, k, g.b1, 1, b.cs_ws, s));
     }
     // B6: dW1 += dz1^T e ;  de = dz1 W1
-    if (gr.W1) {
+    if (g.W1) {
       int splits = (int)std::max<int64_t>(1, std::min<int64_t>(kSplitsW, nE / 512));
       TgemmArgs a{k, 16, nE, b.dZ1 + eb * k, k, true, e + eb * 16, 16, true, b.part, 16, splits, (int64_t)k * 16, 0};
       DS_TRY(tgemm(a, s));
@@ -490,7 +535,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
       int kbps = (int)std::max<int64_t>(1, ceil_div(nkb, splits));
       int real = (int)std::max<int64_t>(1, ceil_div(nkb, kbps));
       DS_TRY(splitk_sum(b.part, real, (int64_t)k * 16, k, 16, 16, b.dW1f, 16, 0, s));
-      add_cols_kernel<<<grid_of((int64_t)k * d.d_e), 256, 0, s>>>(b.dW1f, k, 16, d.d_e, gr.W1, 1);
+      add_cols_kernel<<<grid_of((int64_t)k * d.d_e), 256, 0, s>>>(b.dW1f, k, 16, d.d_e, g.W1, 1);
       DS_LAUNCH_CHECK();
     }
     if (de) {
@@ -507,7 +552,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     else scatter_csc_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
     DS_LAUNCH_CHECK();
   }
-  return DSMPNN_OK;
+  return unpad();
 }
 
 }  // namespace dsmpnn

@@ -372,3 +372,30 @@ except L.DsmpnnError as ex:
     p = subprocess.run([sys.executable, "-c", code, root], env=dict(os.environ, DSMPNN_DEBUG="1"),
                        capture_output=True, text=True, timeout=300)
     assert "STATUS -3" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("k,d,want_de", [(128, 64, False), (64, 32, False), (100, 64, True)])
+def test_fwd_bwd_bf16_kappa_width_below_256(L, k, d, want_de):
+    """kappa width k < 256 in BF16 mode: the
+    weights are zero-padded to 256 units (dsmpnn_pack_weights), the padded
+    units stay exact zeros, and the output and every gradient of width k
+    match the fp64 oracle of width k at the north_star's 2e-2 -- on the fused
+    backward (no edge-attribute gradient) and on the unfused one."""
+    p = _problem(700, 2, 0.1, 40, "diff", d, k, seed=51 + k, n_dst=650, isolated=3)
+    _mask_kinks(p, 1, 2, 1)
+    got = _run_gpu(L, p, 1, 2, 1, want_de=want_de)
+    ref = _oracle(p, 1, 2, 1)
+    assert nerr(got["out"], ref["out"]) <= TOL[1]
+    assert nerr(got["dv"], ref["dv"]) <= TOL[1]
+    if want_de:
+        assert nerr(got["de"], ref["de"]) <= TOL[1]
+    for nm in GNAMES:
+        assert got["grads"][nm].shape == p["W"][nm].shape, nm
+        assert nerr(got["grads"][nm], ref["grads"][nm]) <= TOL[1], nm
+
+
+def test_bf16_kappa_width_above_256_is_unsupported(L):
+    desc = L.make_desc(3, 64, 64, 512, L.BF16, L.ROOT_DENSE, L.ACT_RELU)
+    with pytest.raises(L.DsmpnnError) as ei:
+        L.packed_weights_size(desc)
+    assert ei.value.status == -8  # UNSUPPORTED

@@ -490,10 +490,21 @@ def main():
                                  next_ready=ready)
 
     def run_steps(n, marks=None):
+        """n steps of the steady-state pipeline: every step prefetches its
+        successor's graph (the last warm-up step prefetches the first timed
+        step's), so a timed run of K steps holds K layer passes and K builds
+        (those of steps 2 .. K+1); the region ends after the last build."""
         for k_ in range(n):
-            step(devin, devin if k_ + 1 < n else None)
+            step(devin, devin if pipelined else None)
             if marks is not None and k_ < n - 1:
                 marks[k_].record(torch.cuda.current_stream())
+
+    def drop_prefetch():
+        """Forget a prefetched graph (after a timed region) so the next
+        region starts from a graph built from its own inputs."""
+        if pipelined:
+            torch.cuda.current_stream().wait_stream(hp._build_stream())
+            hp._next = None
 
     run_steps(args.warmup)
     # settle: at least 8 untimed steps in all (W + extra) before timing; with
@@ -531,6 +542,8 @@ def main():
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps - 1)]
     e0.record(st)
     run_steps(args.steps, marks)
+    if pipelined:
+        st.wait_stream(hp._build_stream())  # the prefetched build of step K+1 is inside the region
     e1.record(st)
     torch.cuda.synchronize()
     bounds = [e0] + marks + [e1]
@@ -563,15 +576,21 @@ def main():
                 dbuf[i][n].copy_(t, non_blocking=True)
             loaded[i].record(cpy)
 
+    # one continuous run across calls: step s computes on dbuf[s % 2] while
+    # the inputs of step s + 1 are copied into the other buffer (and, in the
+    # pipeline, its graph is built from them); a call of K steps therefore
+    # holds K input copies, K builds, K layer passes and K read-backs
+    e2e_pos = [0]
+
     def e2e_run(n_steps):
-        load_inputs(0)
-        for s_ in range(n_steps):
+        for _ in range(n_steps):
+            s_ = e2e_pos[0]
             i = s_ % 2
-            last = s_ + 1 == n_steps
-            if not last:  # the next step's inputs (its graph is built from them during this step)
-                load_inputs(1 - i, after=used[1 - i] if s_ >= 1 else None)
+            if s_ == 0:
+                load_inputs(0)
+            load_inputs(1 - i, after=used[1 - i] if s_ >= 1 else None)
             st.wait_event(loaded[i])
-            grads = step(dbuf[i], None if last else dbuf[1 - i], None if last else loaded[1 - i])
+            grads = step(dbuf[i], dbuf[1 - i], loaded[1 - i])
             for n, t in grads.items():
                 gstage[i][n].copy_(t, non_blocking=True)
             used[i].record(st)
@@ -579,8 +598,12 @@ def main():
                 cpy.wait_event(used[i])
                 for n, t in gstage[i].items():
                     out_host[n].copy_(t, non_blocking=True)
+            e2e_pos[0] = s_ + 1
         st.wait_stream(cpy)
+        if pipelined:
+            st.wait_stream(hp._build_stream())
 
+    drop_prefetch()
     e2e_run(2)  # untimed: first use of the buffers and streams
     if world > 1:
         dist.barrier()
@@ -591,6 +614,7 @@ def main():
     x1.record(st)
     torch.cuda.synchronize()
     e2e_ms = x0.elapsed_time(x1) / args.steps
+    drop_prefetch()
 
     # ---- layer-only time (SURVEY D.1 t_iter: L x (fwd + halo) + L x bwd on
     # the built graphs, no graph build) with the halo exchange on and off:
@@ -712,8 +736,10 @@ def main():
                        "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd",
                        "streams": sc.streams,
                        "pipeline": ("the graph of step t+1 is built on a second stream while step t's layers run "
-                                    "(Alg. 1 builds graphs ahead of the training loop); K steps = K builds + K "
-                                    "layer passes" if pipelined else "off: each step builds its graph first"),
+                                    "(Alg. 1 builds graphs ahead of the training loop); the timed K steps hold K "
+                                    "layer passes and K builds (steps 2..K+1; step 1's graph was prefetched by the "
+                                    "last warm-up step) and end after the last build"
+                                    if pipelined else "off: each step builds its graph first"),
                        "comm": "library NCCL context (dsmpnn_halo_exchange)" if world > 1 else
                                "sub-domains on one device: halo = device copies"},
             "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,

@@ -460,8 +460,10 @@ class HotPath:
     # build and its full layer work.
     def _build_stream(self):
         if getattr(self, "_bstream", None) is None:
-            _, hi = torch.cuda.Stream.priority_range()
-            self._bstream = torch.cuda.Stream(self.dev, priority=hi)
+            import os
+            lo, hi = torch.cuda.Stream.priority_range()
+            self._bstream = torch.cuda.Stream(self.dev, priority=lo if os.environ.get("DSMPNN_BUILD_PRIO") == "lo"
+                                              else hi)
         return self._bstream
 
     def _graph_state(self):

@@ -50,6 +50,8 @@ def parse():
                     help="skip every halo refresh (PAPER.md:209 no-communication ablation; halos stay stale)")
     ap.add_argument("--halo-ratio", type=float, default=1.0, help="overlap length l = ratio * r (Table 4 sweep)")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check of the timed run")
+    ap.add_argument("--batch", type=int, default=-1, choices=[-1, 0, 1],
+                    help="sub-domains of a process as one union graph (a8): -1 auto, 0 per part, 1 on")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="build each step's graph inside the step (no prefetch of the next step's graph)")
     return ap.parse_args()
@@ -464,7 +466,7 @@ def main():
     from paper_2402_15106_b200 import synth
     from paper_2402_15106_b200.api import HotPath
     cfg, sc, coords, attr = step_config(args.config, world, args.dtype, args.halo_ratio, not args.no_comm)
-    sc = dataclasses.replace(sc, streams=args.streams)
+    sc = dataclasses.replace(sc, streams=args.streams, batch=args.batch)
     d_e = (sc.dim + sc.n_attr) * (1 if sc.edge_mode == L.EDGE_DIFF else 2)
     W = synth.weights(d_e, sc.d, sc.d, sc.k)
     v0 = synth.node_features(sc.s, sc.d)
@@ -735,6 +737,8 @@ def main():
                        "l2": "256 MB buffer zeroed at the start of every step, inside the timed region",
                        "step": "sample + partition + radius graph + edge attrs + L x (fwd + halo) + L x bwd",
                        "streams": sc.streams,
+                       "subdomain_batch": ("one union graph (a8)" if getattr(hp, "bat", None) is not None
+                                           else "per sub-domain"),
                        "pipeline": ("the graph of step t+1 is built on a second stream while step t's layers run "
                                     "(Alg. 1 builds graphs ahead of the training loop); the timed K steps hold K "
                                     "layer passes and K builds (steps 2..K+1; step 1's graph was prefetched by the "

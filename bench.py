@@ -778,6 +778,7 @@ def main():
                             "what": "L x (fwd + halo) + L x bwd on the built graphs (SURVEY D.1 t_iter), "
                                     "max over ranks; no-comm = the same with every halo refresh skipped"},
             "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
+            "step_ms": [round(x, 3) for x in step_ms],
             "ms_per_step_unpipelined": serial_ms,
             "gpu_launches": launches * args.steps,
             "warmup_extra": warmup_extra,

@@ -99,20 +99,28 @@ class HotPath:
     def build(self, coords, attr):
         """Alg. 1 lines 391-397 on device-resident points (float32 [N x dim], [N x n_attr])."""
         c = self.cfg
-        ids = pipeline.sample_nodes(c.n_points, c.s, c.seed_sampling, self.dev)
+        # graph arrays come from two alternating slots of persistent buffers
+        # (pipeline.Pool): a build overwrites the arrays of the build before
+        # last, whose step has finished (step_pipelined waits for it)
+        if not hasattr(self, "_pools"):
+            self._pools, self._slot = [pipeline.Pool(self.dev), pipeline.Pool(self.dev)], 1
+        self._slot ^= 1
+        pool = self._pools[self._slot]
+        ids = pipeline.sample_nodes(c.n_points, c.s, c.seed_sampling, self.dev, pool=pool)
         self.ids = ids
-        ids64 = ids.to(torch.int64)
-        cs = torch.empty((ids.numel(), c.dim), dtype=torch.float32, device=self.dev)
+        ids64 = pool.empty("ids64", ids.numel(), torch.int64)
+        ids64.copy_(ids)
+        cs = pool.empty("cs", (ids.numel(), c.dim), torch.float32)
         L.gather_rows(coords, ids64, cs)
-        a = torch.empty((ids.numel(), c.n_attr), dtype=torch.float32, device=self.dev)
+        a = pool.empty("as", (ids.numel(), c.n_attr), torch.float32)
         L.gather_rows(attr, ids64, a)
         gid_bits = max(1, int(c.n_points - 1).bit_length())  # sampled ids are < n_points
         self.subs, self.plan = pipeline.decompose(cs, ids64, a, c.nparts, c.overlap_l, c.r, self.my_parts,
-                                                  gid_bits=gid_bits)
+                                                  gid_bits=gid_bits, pool=pool)
         pipeline.build_graphs(self.subs, c.r, c.n_e, c.seed_capping, c.edge_mode, want_f32=(c.dtype == L.F32),
                               want_bf16=(c.dtype == L.BF16), streams=self._side_streams(),
-                              ws_cache=self.ws.setdefault("graph", {}))
-        self.bat = pipeline.batch_subdomains(self.subs) if self._batched() else None
+                              ws_cache=self.ws.setdefault("graph", {}), pool=pool)
+        self.bat = pipeline.batch_subdomains(self.subs, pool=pool) if self._batched() else None
         return self
 
     def _batched(self):

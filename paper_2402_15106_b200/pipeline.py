@@ -46,26 +46,59 @@ class Subdomain:
         return self.n_own + self.n_halo
 
 
-def sample_nodes(n_points, s, seed, device):
-    ids = torch.empty(min(s, n_points), dtype=torch.int32, device=device)
+class Pool:
+    """Persistent device buffers of one graph slot: `empty(key, shape, dtype)`
+    returns a view of a cached byte buffer (grown on demand with 25 %
+    headroom), so steady-state graph builds allocate nothing.  HotPath keeps
+    two slots and alternates them build by build: a build overwrites the
+    arrays of the build before last, which no queued work reads any more
+    (the pipelined build waits for the previous step's layers)."""
+
+    def __init__(self, device):
+        self.dev = device
+        self.bufs = {}
+
+    def empty(self, key, shape, dtype):
+        shape = tuple(int(x) for x in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+        count = 1
+        for x in shape:
+            count *= x
+        esz = torch.empty((), dtype=dtype).element_size()
+        nbytes = max(1, count) * esz
+        b = self.bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8, device=self.dev)
+            self.bufs[key] = b
+        return b[:nbytes].view(dtype)[:count].view(shape)
+
+
+def _empty(pool, key, shape, dtype, device):
+    if pool is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    return pool.empty(key, shape, dtype)
+
+
+def sample_nodes(n_points, s, seed, device, pool=None):
+    ids = _empty(pool, "ids", min(s, n_points), torch.int32, device)
     L.sample(n_points, s, seed, ids)
     return ids
 
 
-def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bits=0):
+def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bits=0, pool=None):
     """Partition the sampled set (all ranks' plans from one RCB, one host
     synchronisation) and build the local arrays of the given ranks.
-    gid_bits: every gid < 2^gid_bits (0 = unknown), shortens the plan sorts."""
+    gid_bits: every gid < 2^gid_bits (0 = unknown), shortens the plan sorts.
+    pool: optional Pool the arrays are taken from."""
     dev = coords_s.device
     n, dim = coords_s.shape
-    owner = torch.empty(n, dtype=torch.int32, device=dev)
-    boxes = torch.empty(nparts * 2 * dim, dtype=torch.float32, device=dev)
-    internal = torch.empty(nparts * 2 * dim, dtype=torch.uint8, device=dev)
+    owner = _empty(pool, "owner", n, torch.int32, dev)
+    boxes = _empty(pool, "boxes", nparts * 2 * dim, torch.float32, dev)
+    internal = _empty(pool, "internal", nparts * 2 * dim, torch.uint8, dev)
     nc = 5 + 2 * (nparts + 1)
     cap = n * max(1, nparts - 1)
-    local_rows = torch.empty((nparts, n), dtype=torch.int64, device=dev)
-    counts = torch.empty((nparts, nc), dtype=torch.int64, device=dev)
-    send_idx = torch.empty((nparts, cap), dtype=torch.int32, device=dev)
+    local_rows = _empty(pool, "local_rows", (nparts, n), torch.int64, dev)
+    counts = _empty(pool, "counts", (nparts, nc), torch.int64, dev)
+    send_idx = _empty(pool, "send_idx", (nparts, cap), torch.int32, dev)
     L.partition_all(coords_s, gid_s, nparts, overlap_l, radius, owner, boxes, internal, local_rows, counts,
                     send_idx, gid_bits=gid_bits)
     hcounts = counts.cpu().tolist()  # the one synchronisation
@@ -79,17 +112,18 @@ def decompose(coords_s, gid_s, attr_s, nparts, overlap_l, radius, ranks, gid_bit
         send_ptr = h[4 + nparts + 1:4 + 2 * (nparts + 1)]
         n_loc = nd + nn + nh
         lr = local_rows[q, :n_loc]
-        c = torch.empty((n_loc, dim), dtype=torch.float32, device=dev)
+        c = _empty(pool, ("coords", q), (n_loc, dim), torch.float32, dev)
         L.gather_rows(coords_s, lr, c)
-        g = torch.empty(n_loc, dtype=torch.int64, device=dev)
+        g = _empty(pool, ("gid", q), n_loc, torch.int64, dev)
         L.gather_rows(gid_s, lr, g)
-        a = torch.empty((n_loc, attr_s.shape[1]), dtype=torch.float32, device=dev)
+        a = _empty(pool, ("attr", q), (n_loc, attr_s.shape[1]), torch.float32, dev)
         L.gather_rows(attr_s, lr, a)
         out.append(Subdomain(q, nparts, nd, nn, nh, halo_ptr, send_ptr, lr, send_idx[q, :max(ns, 0)], c, g, a))
     return out, dict(owner=owner, boxes=boxes.view(nparts, 2, dim), internal=internal.view(nparts, 2, dim))
 
 
-def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, streams=None, ws_cache=None):
+def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, streams=None, ws_cache=None,
+                 pool=None):
     """build_graph for several sub-domains with one host synchronisation: all
     radius graphs are enqueued (capacity n_own * n_e), then the edge counts and
     the host copies of row_ptr are read back together, then edge attributes
@@ -97,7 +131,10 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, s
     kernels go to streams[q % len(streams)] (arrays are allocated on the
     current stream, which waits for every stream before returning).
     ws_cache: optional dict keeping the radius-graph / CSC workspaces of each
-    sub-domain slot across calls (grown on demand)."""
+    sub-domain slot across calls (grown on demand).  pool: optional Pool the
+    graph arrays are taken from.  The edge attributes of all sub-domains are
+    views of one array (sub-domain q at its edge offset), so the union graph
+    (batch_subdomains) needs no copy of them."""
     if not subs:
         return subs
     dev = subs[0].coords.device
@@ -131,8 +168,8 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, s
 
     cols, rws = [], []
     for q, sd in enumerate(subs):
-        sd.row_ptr = torch.empty(sd.n_own + 1, dtype=torch.int64, device=dev)
-        cols.append(torch.empty(max(1, sd.n_own * n_e), dtype=torch.int32, device=dev))
+        sd.row_ptr = _empty(pool, ("row_ptr", q), sd.n_own + 1, torch.int64, dev)
+        cols.append(_empty(pool, ("col", q), max(1, sd.n_own * n_e), torch.int32, dev))
         rws.append(ws(("radius", q), L.radius_graph_workspace_size(sd.n_loc, sd.n_own, sd.coords.shape[1])))
     fan_out(lambda q, sd: L.radius_graph(sd.coords, sd.gid, sd.n_own, r, n_e, seed, sd.row_ptr, cols[q],
                                          want_count=False, ws=rws[q]))
@@ -144,20 +181,22 @@ def build_graphs(subs, r, n_e, seed, edge_mode, want_f32=True, want_bf16=True, s
         E = int(sd.row_ptr_host[-1])
         sd.col_idx = col[:E]
         sd.n_edges = E
-        _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16)
+    E_tot = sum(sd.n_edges for sd in subs)
+    de = (subs[0].coords.shape[1] + subs[0].attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
+    e32_all = _empty(pool, "e32", (E_tot + 1, de), torch.float32, dev) if want_f32 else None
+    e16_all = _empty(pool, "e16", (E_tot + 1, 16), torch.bfloat16, dev) if want_bf16 else None  # all 16 written
+    eoff = 0
+    for q, sd in enumerate(subs):
+        E = sd.n_edges
+        # (an empty sub-domain's one-row view is never written)
+        sd.e32 = e32_all[eoff:eoff + max(E, 1)] if want_f32 else None
+        sd.e16 = e16_all[eoff:eoff + max(E, 1)] if want_bf16 else None
+        sd.csc_perm = _empty(pool, ("csc_perm", q), max(E, 1), torch.int32, dev)
+        sd.csc_ptr = _empty(pool, ("csc_ptr", q), sd.n_loc + 1, torch.int64, dev)
+        eoff += E
     cws = [ws(("csc", q), L.csc_workspace_size(sd.n_edges, sd.n_loc)) for q, sd in enumerate(subs)]
     fan_out(lambda q, sd: _edge_arrays(sd, edge_mode, cws[q]))
     return subs
-
-
-def _alloc_edge_arrays(sd, edge_mode, want_f32, want_bf16):
-    dev = sd.coords.device
-    E = sd.n_edges
-    de = (sd.coords.shape[1] + sd.attr.shape[1]) * (1 if edge_mode == L.EDGE_DIFF else 2)
-    sd.e32 = torch.empty((max(E, 1), de), dtype=torch.float32, device=dev) if want_f32 else None
-    sd.e16 = torch.empty((max(E, 1), 16), dtype=torch.bfloat16, device=dev) if want_bf16 else None  # all 16 written
-    sd.csc_perm = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
-    sd.csc_ptr = torch.empty(sd.n_loc + 1, dtype=torch.int64, device=dev)
 
 
 def _edge_arrays(sd, edge_mode, csc_ws=None):
@@ -213,8 +252,10 @@ class Batch:
     halo_src: torch.Tensor          # int32 [n_loc - n_own]
 
 
-def batch_subdomains(subs, ws=None):
-    """Union graph of `subs` (every sub-domain of the plan, all on this device)."""
+def batch_subdomains(subs, ws=None, pool=None):
+    """Union graph of `subs` (every sub-domain of the plan, all on this device).
+    When the sub-domains' edge attributes are consecutive views of one array
+    (build_graphs), the union uses that array as is."""
     dev = subs[0].coords.device
     n_own = sum(sd.n_own for sd in subs)
     n_loc = sum(sd.n_loc for sd in subs)
@@ -235,13 +276,23 @@ def batch_subdomains(subs, ws=None):
     e_arr = subs[0].e16 if subs[0].e16 is not None else subs[0].e32
     e_row_bytes = e_arr.shape[1] * e_arr.element_size()
     b = Batch(subs, n_own, n_loc, E, own_off, halo_off,
-              row_ptr=torch.empty(n_own + 1, dtype=torch.int64, device=dev), row_ptr_host=rph,
-              col_idx=torch.empty(max(E, 1), dtype=torch.int32, device=dev), e32=None, e16=None,
-              csc_perm=torch.empty(max(E, 1), dtype=torch.int32, device=dev),
-              csc_ptr=torch.empty(n_loc + 1, dtype=torch.int64, device=dev),
-              local_rows=torch.empty(n_loc, dtype=torch.int64, device=dev),
-              halo_src=torch.empty(max(n_loc - n_own, 1), dtype=torch.int32, device=dev))
-    e_out = torch.empty((max(E, 1), e_arr.shape[1]), dtype=e_arr.dtype, device=dev)
+              row_ptr=_empty(pool, "u_row_ptr", n_own + 1, torch.int64, dev), row_ptr_host=rph,
+              col_idx=_empty(pool, "u_col", max(E, 1), torch.int32, dev), e32=None, e16=None,
+              csc_perm=_empty(pool, "u_csc_perm", max(E, 1), torch.int32, dev),
+              csc_ptr=_empty(pool, "u_csc_ptr", n_loc + 1, torch.int64, dev),
+              local_rows=_empty(pool, "u_rows", n_loc, torch.int64, dev),
+              halo_src=_empty(pool, "u_halo_src", max(n_loc - n_own, 1), torch.int32, dev))
+    # the parts' attributes already form the union array when they are consecutive views of one buffer
+    base, eoff, contiguous = e_arr.data_ptr(), 0, True
+    for sd in subs:
+        t = sd.e16 if subs[0].e16 is not None else sd.e32
+        contiguous &= t.data_ptr() == base + eoff * e_row_bytes
+        eoff += sd.n_edges
+    if contiguous:
+        e_out, e_copy = torch.as_strided(e_arr, (max(E, 1), e_arr.shape[1]), e_arr.stride()), None
+    else:
+        e_out = _empty(pool, "u_e", (max(E, 1), e_arr.shape[1]), e_arr.dtype, dev)
+        e_copy = e_out
     if subs[0].e16 is not None:
         b.e16 = e_out
     else:
@@ -250,7 +301,7 @@ def batch_subdomains(subs, ws=None):
                   e=sd.e16 if sd.e16 is not None else sd.e32, csc_perm=sd.csc_perm, csc_ptr=sd.csc_ptr,
                   rows=sd.local_rows, halo_ptr=sd.halo_ptr, send_ptr=sd.send_ptr, send_idx=sd.send_idx)
              for sd in subs]
-    L.batch_subdomains(parts, e_row_bytes, b.row_ptr, b.col_idx, e_out, b.csc_perm, b.csc_ptr, b.local_rows,
+    L.batch_subdomains(parts, e_row_bytes, b.row_ptr, b.col_idx, e_copy, b.csc_perm, b.csc_ptr, b.local_rows,
                        b.halo_src, ws=ws)
     return b
 

@@ -5,7 +5,7 @@
 //   U    = H dS_i         (M = 128 slots, N = NMAX * D, K = kappa)
 //   dH^T = dS_i V_seg^T   (M = kappa halves, N = the row's slots, K = c)
 // then dz2 = dH * [h > 0] -> dZ2 (global, bf16), u_p = U + dS_i[k] -> U
-// (global, bf16) and per-CTA db2 partial sums.
+// (global, bf16; row upos[p] when upos is given) and per-CTA db2 partial sums.
 //
 // What changed against edge_bwd3 (whose per-tile chain ended with the dz2
 // epilogue storing 64 KB to HBM at the write ceiling while the tensor cores
@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(512, 1)
                      const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t rb, int64_t re,
                      int64_t eb, int64_t ee, Packed pw, const float *__restrict__ b2,
                      const __nv_bfloat16 *__restrict__ dS, __nv_bfloat16 *__restrict__ dZ2g,
-                     __nv_bfloat16 *__restrict__ Ug, float *__restrict__ db2_part) {
+                     __nv_bfloat16 *__restrict__ Ug, const int32_t *__restrict__ upos,
+                     float *__restrict__ db2_part) {
   using C = EB4<D>;
   using Misc = typename C::Misc;
   constexpr int NMAX = C::NMAX;
@@ -548,7 +549,10 @@ __global__ void __launch_bounds__(512, 1)
           for (int c0 = 0; c0 < D; c0 += 32) {
             const uint32_t *x = &xx[c0];
             if (mine) {
-              uint4 *dst = reinterpret_cast<uint4 *>(Ug + (int64_t)p * D + c0);
+              // u_p goes to row upos[p] (its CSC position: the scatter then streams
+              // each source's rows contiguously) or to row p
+              const int64_t urow = upos ? (int64_t)__ldg(upos + p) : (int64_t)p;
+              uint4 *dst = reinterpret_cast<uint4 *>(Ug + urow * D + c0);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const uint4 bb = *reinterpret_cast<const uint4 *>(brow + c0 + 8 * u);

@@ -189,6 +189,7 @@ struct BBwd {
   float *b1_part;          // [kNumSMs/2 x 2 x KH]  fused B5+B6 per-pair db1
   float *w2_part;          // [kNumSMs/2 x KH x KH] B4 (dw2.cuh) per-pair dW2
   float *b0_part;          // [ceil(n_dst/32) x D] B0 per-block column sums of ghat
+  int32_t *upos;           // [E] CSC position of every edge (U rows in CSC order for the B7 stream)
   // k < KH: the KH-wide W1, b1, W2, b2, W3 gradients (contiguous, zeroed per call)
   float *gW1 = nullptr, *gb1 = nullptr, *gW2 = nullptr, *gb2 = nullptr, *gW3 = nullptr;
   char *gpad_end = nullptr;
@@ -218,6 +219,7 @@ static BBwd carve_bf16_bwd(Carver &c, const dsmpnn_layer_desc &d, int64_t n_dst,
   b.b1_part = c.take<float>((int64_t)kNumSMs * KH);
   b.w2_part = c.take<float>((int64_t)(kNumSMs / 2 + kDw2Groups) * KH * KH);
   b.b0_part = c.take<float>(ceil_div(std::max<int64_t>(n_dst, 1), 32) * D);
+  b.upos = c.take<int32_t>(std::max<int64_t>(E, 1));
   if (d.k < KH) {  // KH-wide gradients of the kappa MLP (k real units added to the caller's at the end)
     b.gW1 = c.take<float>((int64_t)KH * d.d_e);
     b.gb1 = c.take<float>(KH);
@@ -308,11 +310,78 @@ __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, con
   }
 }
 
+// upos[perm[q]] = q: the CSC position of every edge
+__global__ void csc_inverse_kernel(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ upos) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    upos[perm[q]] = (int32_t)q;
+}
+
+// B7 with U already in CSC order (edge_bwd4 wrote u_p to row upos[p]):
+// dv[j] += sum of U rows cptr[j] .. cptr[j+1] (edges outside [eb, ee) skipped
+// through perm unless the range is the whole graph).  One warp per node;
+// lane = (row sub-slot, 16-byte chunk), consecutive rows: every warp load is
+// one contiguous 512-byte (D = 64) block.  Sub-slot sums combine by a
+// butterfly: the summation order is fixed.
+template <int D>
+__global__ void scatter_sorted_bf16_kernel(const __nv_bfloat16 *__restrict__ U, const int32_t *__restrict__ perm,
+                                           const int64_t *__restrict__ cptr, int64_t n_loc, int64_t eb, int64_t ee,
+                                           int full, float *__restrict__ dv) {
+  constexpr int LPR = D / 8, RPI = 32 / LPR, UNR = 4;
+  const int lane = threadIdx.x & 31, cl = lane % LPR, sub = lane / LPR;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_loc; j += nw) {
+    const int64_t q0 = cptr[j], q1 = cptr[j + 1];
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    bool any = false;
+    for (int64_t qb = q0; qb < q1; qb += RPI * UNR) {
+      uint4 x[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t q = qb + u * RPI + sub;
+        bool ok = q < q1;
+        if (ok && !full) {
+          const int32_t pe = __ldg(perm + q);
+          ok = pe >= eb && pe < ee;
+        }
+        any |= ok;
+        x[u] = ok ? __ldg(reinterpret_cast<const uint4 *>(U + q * D) + cl) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&x[u]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          acc[2 * i] += f.x;
+          acc[2 * i + 1] += f.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (any && sub == 0) {
+      float4 *o = reinterpret_cast<float4 *>(dv + j * D + cl * 8);
+      float4 a0 = o[0], a1 = o[1];
+      a0.x += acc[0]; a0.y += acc[1]; a0.z += acc[2]; a0.w += acc[3];
+      a1.x += acc[4]; a1.y += acc[5]; a1.z += acc[6]; a1.w += acc[7];
+      o[0] = a0;
+      o[1] = a1;
+    }
+  }
+}
+
 template <int D>
 static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &pw, const __nv_bfloat16 *e,
                                      const __nv_bfloat16 *v, const int64_t *row_ptr, const int32_t *col, int64_t n_dst,
                                      int64_t rb, int64_t re, int64_t eb, int64_t ee, const float *b1, const float *b2,
-                                     const BBwd &b, bool write_a1, int *grid_out, cudaStream_t s) {
+                                     const BBwd &b, bool write_a1, const int32_t *upos, bool *u_sorted, int *grid_out,
+                                     cudaStream_t s) {
   CUtensorMap tW2, tDS;
   DS_TRY(make_tmap_bf16(&tW2, pw.W2, KH, KH, KH, 64, KH));
   DS_TRY(make_tmap_bf16(&tDS, b.dS, D, n_dst * (int64_t)(KH + 1), D, D, KH));
@@ -336,7 +405,8 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
     cudaMemsetAsync(dbg4, 0, 32 * 32 * 8, s);
 #endif
     kern<<<grid, 512, EB4<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
-                                         b.db2_part);
+                                         upos, b.db2_part);
+    *u_sorted = upos != nullptr;
 #ifdef DSMPNN_TIMELINE
     dump_timeline("edge_bwd4", dbg4, 24, s);
 #endif
@@ -493,10 +563,20 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   const bool fused = !de && k == KH && d.d_e <= 16;
   // B3: edge kernel
   int grid = 1;
+  // U rows in CSC order (edge_bwd4 only) so that B7 streams them
+  const int32_t *upos = nullptr;
+  if (dv && fused && E > 0) {
+    csc_inverse_kernel<<<grid_of(E), 256, 0, s>>>(perm, E, b.upos);
+    DS_LAUNCH_CHECK();
+    upos = b.upos;
+  }
+  bool u_sorted = false;
   if (D == 64)
-    DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, &grid, s));
+    DS_TRY(launch_edge_bwd<64>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, upos,
+                               &u_sorted, &grid, s));
   else
-    DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, &grid, s));
+    DS_TRY(launch_edge_bwd<32>(d, pw, e, v, row_ptr, col, n_dst, rb, re, eb, ee, pw.b1, pw.b2, b, !fused, upos,
+                               &u_sorted, &grid, s));
   DS_TRY(colsum(b.db2_part, grid, k, k, g.b2, 1, s));
   // B4: dW2 += dz2^T a1   (M = k, N = k, K = edges)
   if (g.W2 && fused) {
@@ -548,8 +628,15 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   // B7: dv[j] += sum of u_p over edges with source j (CSC order)
   if (dv) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 8), 148 * 16));
-    if (D == 64) scatter_csc_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
-    else scatter_csc_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
+    const int full = eb == 0 && ee == E;
+    if (u_sorted) {
+      if (D == 64) scatter_sorted_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, full, dv);
+      else scatter_sorted_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, full, dv);
+    } else if (D == 64) {
+      scatter_csc_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
+    } else {
+      scatter_csc_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
+    }
     DS_LAUNCH_CHECK();
   }
   return unpad();

@@ -399,3 +399,41 @@ def test_bf16_kappa_width_above_256_is_unsupported(L):
     with pytest.raises(L.DsmpnnError) as ei:
         L.packed_weights_size(desc)
     assert ei.value.status == -8  # UNSUPPORTED
+
+
+def test_bf16_bwd_row_ranges_sum_to_full(L):
+    """layer_bwd over rows [0, a) plus [a, n_dst) (edges [eb, ee) of each
+    range; the B7 scatter then skips the other range's edges) accumulates the
+    full-range dv and weight gradients (fused backward, U rows in CSC order)."""
+    p = _problem(700, 2, 0.1, 40, "diff", 64, 256, seed=61, n_dst=650, isolated=3)
+    d, k, d_e = p["d"], p["k"], p["d_e"]
+    desc = L.make_desc(d_e, d, d, k, L.BF16, 2, 1)
+    Wd = {n: T(p["W"][n]) for n in GNAMES}
+    packed = torch.empty(L.packed_weights_size(desc), dtype=torch.uint8, device=cuda())
+    L.pack_weights(desc, Wd, packed)
+    n, n_dst, E = p["n"], p["n_dst"], len(p["col"])
+    v = T(p["v"]).to(torch.bfloat16)
+    e16 = np.zeros((E, 16), np.float32)
+    e16[:, :d_e] = p["e"]
+    e = T(e16).to(torch.bfloat16)
+    rp, col, rph = T(p["rp"]), T(p["col"]), torch.from_numpy(p["rp"])
+    out = torch.empty((n_dst, d), device=cuda())
+    ws = torch.empty(L.layer_workspace_size(desc, n_dst, E), dtype=torch.uint8, device=cuda())
+    L.layer_fwd(desc, Wd, packed, v, e, rp, col, n_dst, 0, n_dst, out, None, ws, row_ptr_host=rph)
+    perm = torch.empty(E, dtype=torch.int32, device=cuda())
+    cptr = torch.empty(n + 1, dtype=torch.int64, device=cuda())
+    L.csc(col, n, perm, cptr)
+    bws = torch.empty(L.layer_bwd_workspace_size(desc, n_dst, n, E), dtype=torch.uint8, device=cuda())
+    Gt = T(p["G"])
+    res = []
+    for ranges in ([(0, n_dst)], [(0, 311), (311, n_dst)]):
+        gv = torch.zeros((n, d), device=cuda())
+        grads = {nm: torch.zeros_like(Wd[nm]) for nm in GNAMES}
+        for a, b in ranges:
+            L.layer_bwd(desc, Wd, packed, v, e, rp, col, perm, cptr, n_dst, n, a, b, Gt, gv, None, grads, ws, bws,
+                        row_ptr_host=rph)
+        torch.cuda.synchronize()
+        res.append((N(gv), {nm: N(t) for nm, t in grads.items()}))
+    assert nerr(res[1][0], res[0][0]) <= 1e-5
+    for nm in GNAMES:
+        assert nerr(res[1][1][nm], res[0][1][nm]) <= 1e-5, nm

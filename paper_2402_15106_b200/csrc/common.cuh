@@ -63,6 +63,46 @@ static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int kNumSMs = 148;
 
+// Programmatic dependent launch (PDL) along the layer's kernel chain: the
+// chain's kernels are launched with launch_pdl (stream attribute
+// ProgrammaticStreamSerialization) and each calls pdl_wait() before it reads
+// or writes data of another kernel (weights packed by dsmpnn_pack_weights and
+// the graph arrays may be read earlier: no kernel that lets its successor
+// start early writes them), then pdl_trigger(), so its successor's launch and
+// prologue (barrier init, TMEM allocation, resident weight loads) overlap its
+// own tail (with the early trigger, see below).  A kernel launched without
+// the attribute passes pdl_wait at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The early trigger (successor CTAs launched while this grid's last CTAs run)
+// shortens the layer chain a little more (8.23 vs 8.29 ms per Darcy step of
+// layers) but its resident successor CTAs take every SM a finishing CTA
+// frees, so the next step's graph build on the high-priority stream starves
+// and the pipelined step slows from 8.6 to 9.5 ms: by default successors
+// launch at the grid's completion (the implicit trigger), which still hides
+// the launch latency between the chain's kernels.
+#ifdef DSMPNN_PDL_EARLY_TRIGGER
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#else
+__device__ __forceinline__ void pdl_trigger() {}
+#endif
+bool pdl_enabled();  // DSMPNN_PDL=0 turns the launch attribute off (A/B timing)
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // live timing probe (dsmpnn_probe_begin/end): true if launches of `id` are recorded
 bool probe_armed(int id);
 void probe_before(int id, cudaStream_t s);

@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(DW2C::THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = m->tmem_slot;
+  pdl_wait();  // dz2 / e of other kernels from here on
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -246,6 +248,8 @@ __global__ void __launch_bounds__(DW2C::THREADS, 1)
 // pass 2 adds the groups in order.  Deterministic run to run.
 constexpr int kDw2Groups = 8;
 __global__ void dw2_reduce1_kernel(const float4 *__restrict__ part, int npairs, float4 *__restrict__ tmp) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= KH * KH / 4) return;
   const int per = (npairs + kDw2Groups - 1) / kDw2Groups;
@@ -261,6 +265,8 @@ __global__ void dw2_reduce1_kernel(const float4 *__restrict__ part, int npairs, 
   tmp[(int64_t)blockIdx.y * (KH * KH / 4) + i] = s;
 }
 __global__ void dw2_reduce2_kernel(const float4 *__restrict__ tmp, float4 *__restrict__ gW2) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= KH * KH / 4) return;
   float4 s = gW2[i];

@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(DZ1C::THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = m->tmem_slot;
+  pdl_wait();  // dz2 / e of other kernels from here on
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -272,6 +274,8 @@ __global__ void __launch_bounds__(DZ1C::THREADS, 1)
 // order is fixed, so the result is run-to-run identical.
 __global__ void dz1w1_reduce_kernel(const float *__restrict__ part_w, const float *__restrict__ part_b, int npairs,
                                     int d_e, float *__restrict__ gW1, float *__restrict__ gb1) {
+  pdl_wait();
+  pdl_trigger();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int r = w / (d_e + 1), c = w - r * (d_e + 1);
   if (r >= KH) return;

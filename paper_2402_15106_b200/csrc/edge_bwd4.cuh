@@ -180,6 +180,8 @@ __global__ void __launch_bounds__(512, 1)
   tc::tc_fence_after();
   const uint32_t tmem = m->tmem;
   const uint32_t tZ = tmem, tA = tmem + 256, tU = tmem + 384;
+  pdl_wait();  // dS, v, e and the outputs of other kernels from here on
+  pdl_trigger();
 
   if (warp == 0 || warp == 2) {
     // ============================================================ loaders

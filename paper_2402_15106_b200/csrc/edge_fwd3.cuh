@@ -132,6 +132,8 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = m->tmem;
+  pdl_wait();  // v, e and S of other kernels from here on
+  pdl_trigger();
 
   if (warp == 0 || warp == 2 || warp == 3) {
     // ============================================================ loader

@@ -126,6 +126,8 @@ template <int D>
 __global__ void s_fill_kernel(const __nv_bfloat16 *__restrict__ v, const int64_t *__restrict__ row_ptr,
                               const int32_t *__restrict__ col, int64_t rb, int64_t re, int64_t kp,
                               __nv_bfloat16 *__restrict__ S) {
+  pdl_wait();
+  pdl_trigger();
   // warp per row; lane = (edge sub-slot, 16-byte column chunk): D / 8 lanes
   // cover one v row, so a warp instruction gathers 32 / (D / 8) rows and
   // UNR instructions are in flight; sub-slot sums combine by a butterfly
@@ -192,6 +194,8 @@ __global__ void node_epi_bf16_kernel(const float *__restrict__ part, int splits,
                                      int64_t re, int D, const float *__restrict__ b,
                                      const __nv_bfloat16 *__restrict__ v, int root, int act, float *__restrict__ pre,
                                      float *__restrict__ out, __nv_bfloat16 *__restrict__ out_lowp) {
+  pdl_wait();
+  pdl_trigger();
   int64_t total = (re - rb) * D;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     float x = 0.f;
@@ -285,7 +289,7 @@ static dsmpnn_status launch_edge_fwd(const __nv_bfloat16 *e, const __nv_bfloat16
     }
     cudaMemsetAsync(dbg, 0, 32 * 32 * 8, s);
 #endif
-    kern<<<grid, 512, EF3<D>::SMEM, s>>>(tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col);
+    DS_CUDA(launch_pdl(kern, grid, 512, EF3<D>::SMEM, s, tW2, e, v, row_ptr, rb, re, eb, ee, pw, b1, b2, S, kp, col));
 #ifdef DSMPNN_TIMELINE
     dump_timeline("edge_fwd3", dbg, 29, s);
 #endif
@@ -308,8 +312,8 @@ dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   // 1. bias row, root operand, isolated rows
   {
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * 32, 256), 148 * 8));
-    if (D == 64) s_fill_kernel<64><<<blocks, 256, 0, s>>>(v, row_ptr, col, rb, re, kp, f.S);
-    else s_fill_kernel<32><<<blocks, 256, 0, s>>>(v, row_ptr, col, rb, re, kp, f.S);
+    if (D == 64) DS_CUDA(launch_pdl(s_fill_kernel<64>, blocks, 256, 0, s, v, row_ptr, col, rb, re, kp, f.S));
+    else DS_CUDA(launch_pdl(s_fill_kernel<32>, blocks, 256, 0, s, v, row_ptr, col, rb, re, kp, f.S));
     DS_LAUNCH_CHECK();
   }
   // 2. fused kappa MLP + S formation
@@ -325,8 +329,8 @@ dsmpnn_status bf16_fwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     TgemmArgs a{nR, D, kp, f.S + rb * kp, kp, false, pw.ThT, kp, false, f.part, D, splits, nR * D, 0};
     DS_TRY(tgemm(a, s));
   }
-  node_epi_bf16_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * D, 256), 148 * 8)), 256, 0, s>>>(
-      f.part, real, nR * D, rb, re, D, w.b, v, d.root, d.act, f.pre, out, out_lowp);
+  DS_CUDA(launch_pdl(node_epi_bf16_kernel, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nR * D, 256), 148 * 8)), 256, 0, s, 
+      f.part, real, nR * D, rb, re, D, w.b, v, d.root, d.act, f.pre, out, out_lowp));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

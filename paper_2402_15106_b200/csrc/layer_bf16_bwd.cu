@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ 
                                                       float *__restrict__ gh, __nv_bfloat16 *__restrict__ gh16,
                                                       float *__restrict__ inv_deg, float *__restrict__ cs_part,
                                                       float *__restrict__ dv) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sg[32][D + 1];
   __shared__ __align__(16) float sw[D][D];
   const int t = threadIdx.x;
@@ -120,6 +122,8 @@ __global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ 
 // order): 32 x 32 tiles transposed through shared memory so both the dT reads
 // and the dW3 read-modify-writes are coalesced.  grid = (k/32, D/32, D)
 __global__ void unpack_dw3_kernel(const float *__restrict__ dT, int k, int D, float *__restrict__ dW3) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float t[32][33];
   const int kap0 = blockIdx.x * 32, o0 = blockIdx.y * 32, c = blockIdx.z;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
@@ -134,6 +138,8 @@ __global__ void unpack_dw3_kernel(const float *__restrict__ dT, int k, int D, fl
 // db3[c*D+o] += dT[k*D+c, o]; dW_root[o, c] += dT[(k+1)*D+c, o]
 __global__ void unpack_bias_root_kernel(const float *__restrict__ dT, int k, int D, float *__restrict__ db3,
                                         float *__restrict__ dWr) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)D * D;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int a = (int)(t / D), b = (int)(t - (int64_t)a * D);
@@ -312,6 +318,8 @@ __global__ void scatter_csc_bf16_kernel(const __nv_bfloat16 *__restrict__ U, con
 
 // upos[perm[q]] = q: the CSC position of every edge
 __global__ void csc_inverse_kernel(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ upos) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     upos[perm[q]] = (int32_t)q;
 }
@@ -326,6 +334,8 @@ template <int D>
 __global__ void scatter_sorted_bf16_kernel(const __nv_bfloat16 *__restrict__ U, const int32_t *__restrict__ perm,
                                            const int64_t *__restrict__ cptr, int64_t n_loc, int64_t eb, int64_t ee,
                                            int full, float *__restrict__ dv) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int LPR = D / 8, RPI = 32 / LPR, UNR = 4;
   const int lane = threadIdx.x & 31, cl = lane % LPR, sub = lane / LPR;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -404,8 +414,8 @@ static dsmpnn_status launch_edge_bwd(const dsmpnn_layer_desc &d, const Packed &p
     }
     cudaMemsetAsync(dbg4, 0, 32 * 32 * 8, s);
 #endif
-    kern<<<grid, 512, EB4<D>::SMEM, s>>>(tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
-                                         upos, b.db2_part);
+    DS_CUDA(launch_pdl(kern, grid, 512, EB4<D>::SMEM, s, tW2, tDS, e, v, row_ptr, col, rb, re, eb, ee, pw, b2, b.dS, b.dZ2, b.U,
+                                         upos, b.db2_part));
     *u_sorted = upos != nullptr;
 #ifdef DSMPNN_TIMELINE
     dump_timeline("edge_bwd4", dbg4, 24, s);
@@ -452,11 +462,11 @@ static dsmpnn_status launch_dz1w1(const Packed &pw, const __nv_bfloat16 *dZ2, co
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
   {
     ProbeScope probe(DSMPNN_PROBE_BF16_DZ1W1, s);
-    dz1w1_kernel<<<2 * npairs, DZ1C::THREADS, DZ1C::SMEM, s>>>(tW2, tW1, tDZ, tE, nE, b1, part_w, part_b);
+    DS_CUDA(launch_pdl(dz1w1_kernel, 2 * npairs, DZ1C::THREADS, DZ1C::SMEM, s, tW2, tW1, tDZ, tE, nE, b1, part_w, part_b));
     DS_LAUNCH_CHECK();
   }
   const int n = KH * (d_e + 1) * 32;
-  dz1w1_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(part_w, part_b, npairs, d_e, gW1, gb1);
+  DS_CUDA(launch_pdl(dz1w1_reduce_kernel, (n + 255) / 256, 256, 0, s, part_w, part_b, npairs, d_e, gW1, gb1));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -474,14 +484,14 @@ static dsmpnn_status launch_dw2(const Packed &pw, const __nv_bfloat16 *dZ2, cons
   const int npairs = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs / 2, ceil_div(nE, 128)));
   {
     ProbeScope probe(DSMPNN_PROBE_BF16_DW2, s);
-    dw2_kernel<<<2 * npairs, DW2C::THREADS, DW2C::SMEM, s>>>(tW1, tDZ, tE, nE, b1, part);
+    DS_CUDA(launch_pdl(dw2_kernel, 2 * npairs, DW2C::THREADS, DW2C::SMEM, s, tW1, tDZ, tE, nE, b1, part));
     DS_LAUNCH_CHECK();
   }
   float4 *tmp = reinterpret_cast<float4 *>(part + (int64_t)(kNumSMs / 2) * KH * KH);
-  dw2_reduce1_kernel<<<dim3(KH * KH / 4 / 256, kDw2Groups), 256, 0, s>>>(reinterpret_cast<const float4 *>(part),
-                                                                         npairs, tmp);
+  DS_CUDA(launch_pdl(dw2_reduce1_kernel, dim3(KH * KH / 4 / 256, kDw2Groups), 256, 0, s, reinterpret_cast<const float4 *>(part),
+                                                                         npairs, tmp));
   DS_LAUNCH_CHECK();
-  dw2_reduce2_kernel<<<KH * KH / 4 / 256, 256, 0, s>>>(tmp, reinterpret_cast<float4 *>(gW2));
+  DS_CUDA(launch_pdl(dw2_reduce2_kernel, KH * KH / 4 / 256, 256, 0, s, tmp, reinterpret_cast<float4 *>(gW2)));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }
@@ -528,11 +538,11 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   {
     const int nblk = (int)ceil_div(nR, 32);
     if (D == 64)
-      b0_bf16_kernel<64><<<nblk, 256, 0, s>>>(G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
-                                              b.inv_deg, b.b0_part, dv);
+      DS_CUDA(launch_pdl(b0_bf16_kernel<64>, nblk, 256, 0, s, G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
+                                              b.inv_deg, b.b0_part, dv));
     else
-      b0_bf16_kernel<32><<<nblk, 256, 0, s>>>(G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
-                                              b.inv_deg, b.b0_part, dv);
+      DS_CUDA(launch_pdl(b0_bf16_kernel<32>, nblk, 256, 0, s, G, f.pre, row_ptr, rb, re, d.act, d.root, w.W_root, b.gh, b.gh16,
+                                              b.inv_deg, b.b0_part, dv));
     DS_LAUNCH_CHECK();
     if (g.b) DS_TRY(colsum(b.b0_part, nblk, D, D, g.b, 1, s));
   }
@@ -541,11 +551,11 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     TgemmArgs a{kp, D, nR, f.S + rb * kp, kp, true, b.gh16 + rb * D, D, true, b.dT, D, 1, 0, 0};
     DS_TRY(tgemm(a, s));
     if (g.W3) {
-      unpack_dw3_kernel<<<dim3(k / 32, D / 32, D), 256, 0, s>>>(b.dT, k, D, g.W3);
+      DS_CUDA(launch_pdl(unpack_dw3_kernel, dim3(k / 32, D / 32, D), 256, 0, s, b.dT, k, D, g.W3));
       DS_LAUNCH_CHECK();
     }
-    unpack_bias_root_kernel<<<grid_of((int64_t)D * D), 256, 0, s>>>(
-        b.dT, k, D, g.b3, d.root == DSMPNN_ROOT_DENSE ? g.W_root : nullptr);
+    DS_CUDA(launch_pdl(unpack_bias_root_kernel, grid_of((int64_t)D * D), 256, 0, s, 
+        b.dT, k, D, g.b3, d.root == DSMPNN_ROOT_DENSE ? g.W_root : nullptr));
     DS_LAUNCH_CHECK();
   }
   if (nE <= 0) return unpad();
@@ -566,7 +576,7 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
   // U rows in CSC order (edge_bwd4 only) so that B7 streams them
   const int32_t *upos = nullptr;
   if (dv && fused && E > 0) {
-    csc_inverse_kernel<<<grid_of(E), 256, 0, s>>>(perm, E, b.upos);
+    DS_CUDA(launch_pdl(csc_inverse_kernel, grid_of(E), 256, 0, s, perm, E, b.upos));
     DS_LAUNCH_CHECK();
     upos = b.upos;
   }
@@ -630,8 +640,8 @@ dsmpnn_status bf16_bwd(const dsmpnn_layer_desc &d, const dsmpnn_weights &w, cons
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 8), 148 * 16));
     const int full = eb == 0 && ee == E;
     if (u_sorted) {
-      if (D == 64) scatter_sorted_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, full, dv);
-      else scatter_sorted_bf16_kernel<32><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, full, dv);
+      if (D == 64) DS_CUDA(launch_pdl(scatter_sorted_bf16_kernel<64>, blocks, 256, 0, s, b.U, perm, cptr, n_loc, eb, ee, full, dv));
+      else DS_CUDA(launch_pdl(scatter_sorted_bf16_kernel<32>, blocks, 256, 0, s, b.U, perm, cptr, n_loc, eb, ee, full, dv));
     } else if (D == 64) {
       scatter_csc_bf16_kernel<64><<<blocks, 256, 0, s>>>(b.U, perm, cptr, n_loc, eb, ee, dv);
     } else {

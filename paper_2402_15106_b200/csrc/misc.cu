@@ -12,6 +12,14 @@ namespace dsmpnn {
 
 static thread_local std::string g_last_error;
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("DSMPNN_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void set_error(const char *fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -111,6 +119,8 @@ __global__ void edge_features_kernel(int32_t mode, const float *__restrict__ x, 
 template <typename T>
 __global__ void halo_gather_kernel(const T *__restrict__ v, const int32_t *__restrict__ rows, int64_t n_rows,
                                    int width, T *__restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   int64_t total = n_rows * width;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = t / width, c = t - r * width;
@@ -276,9 +286,9 @@ dsmpnn_status dsmpnn_halo_gather(const void *values, const int32_t *rows, int64_
   cudaStream_t s = as_stream(stream);
   int g = grid_for(n_rows * width);
   if (dtype == DSMPNN_F32)
-    halo_gather_kernel<float><<<g, 256, 0, s>>>((const float *)values, rows, n_rows, width, (float *)out);
+    DS_CUDA(launch_pdl(halo_gather_kernel<float>, g, 256, 0, s, (const float *)values, rows, n_rows, width, (float *)out));
   else if (dtype == DSMPNN_BF16)
-    halo_gather_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t *)values, rows, n_rows, width, (uint16_t *)out);
+    DS_CUDA(launch_pdl(halo_gather_kernel<uint16_t>, g, 256, 0, s, (const uint16_t *)values, rows, n_rows, width, (uint16_t *)out));
   else
     DS_CHECK_ARG(false, DSMPNN_ERR_INVALID_ARG, "halo_gather: dtype");
   DS_LAUNCH_CHECK();

@@ -106,6 +106,8 @@ dsmpnn_status sgemm(const SgemmArgs &a, int splits, float *partial, cudaStream_t
 // one block per 32 columns; 32 row lanes per column, fixed reduction order
 __global__ void __launch_bounds__(1024) colsum_kernel(const float *__restrict__ A, int64_t M, int64_t N, int64_t lda,
                                                       float *__restrict__ out, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32][33];
   int c = threadIdx.x & 31, r = threadIdx.x >> 5;
   int64_t n = (int64_t)blockIdx.x * 32 + c;
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(1024) colsum_chunk_kernel(const float *__restr
 
 dsmpnn_status colsum(const float *A, int64_t M, int64_t N, int64_t lda, float *out, int accumulate, cudaStream_t s) {
   if (N <= 0 || !out) return DSMPNN_OK;
-  colsum_kernel<<<(unsigned)ceil_div(N, 32), 1024, 0, s>>>(A, M, N, lda, out, accumulate);
+  DS_CUDA(launch_pdl(colsum_kernel, (unsigned)ceil_div(N, 32), 1024, 0, s, A, M, N, lda, out, accumulate));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

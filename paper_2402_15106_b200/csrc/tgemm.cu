@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(TG<BN, A_MN, B_MN, E16, BRES>::THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // operands and outputs of other kernels from here on
+  pdl_trigger();
 
   auto tile_coords = [&](int64_t t, int64_t &m0, int64_t &n0, int64_t &kb0, int &nkb, int &z) {
     z = (int)(t / (nm * nn));
@@ -398,7 +400,7 @@ static dsmpnn_status launch_tgemm(const TgemmArgs &a, cudaStream_t s) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm));
   DS_CHECK_ARG(T::EPI == 4 || a.colsum_part == nullptr, DSMPNN_ERR_UNSUPPORTED,
                "tgemm: column sums need the resident-B bf16 epilogue");
-  kern<<<grid, T::THREADS, T::SMEM, s>>>(ta, tb, tout, tmask, a.M, a.N, a.K, kbps, a, splits);
+  DS_CUDA(launch_pdl(kern, grid, T::THREADS, T::SMEM, s, ta, tb, tout, tmask, a.M, a.N, a.K, kbps, a, splits));
   DS_LAUNCH_CHECK();
   return DSMPNN_OK;
 }

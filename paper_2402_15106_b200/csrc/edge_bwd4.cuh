@@ -22,10 +22,14 @@
 //  * per-tile dS buffer (rows at slots 0 .. nn-1) instead of a ring.
 //
 // Roles (16 warps): loader 0 (walker, e rows, dS_i[k] rows), loader 2 (v
-// rows), warp 3 lane 16 (dS loads, dz2 bulk stores), MMA 1, EPI_A 4-11 (a1,
-// h, bits; then the dz2 epilogue of kappa half cg), EPI_B 12-15 (U epilogue).
-// TMEM as edge_bwd3: Z = 0..255 (z1, z2, then dH^T half h at 128 h + slot),
-// A = 256..383 (a1, then h), U = 384..511 (row g at 384 + g D).
+// rows), warp 3 lane 16 (dS loads, dz2 bulk stores), MMA 1, EPI_A 4-11 (h,
+// bits; then the dz2 epilogue of kappa half cg), EPI_B 12-15 (a1 epilogue,
+// then the U epilogue).
+// TMEM: Z = 0..255 (z2, then dH^T half h at 128 h + slot), A = 256..383 (z1
+// kappa 0..127, then a1 packed, then h), U = 384..511 (z1 kappa 128..255,
+// then U row g at 384 + g D).  z1 of tile t+1 goes to A and U as soon as U
+// of tile t is drained, so the next tile's MLP starts while tile t's dz2
+// drain still reads Z; MMA2 of tile t+1 waits for that drain (dh_free).
 #pragma once
 #include "edge_bwd3.cuh"
 
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(512, 1)
     tc::mbar_init(&m->v_full, 32);
     tc::mbar_init(&m->v_empty, 1);
     tc::mbar_init(&m->d1_full, 1);
-    tc::mbar_init(&m->a1_ready, 256);
+    tc::mbar_init(&m->a1_ready, 128);  // EPI_B (the a1 epilogue)
     tc::mbar_init(&m->d2_full, 1);
     tc::mbar_init(&m->h_ready, 256);
     tc::mbar_init(&m->a_free, 1);
@@ -310,14 +314,20 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t aW2 = tc::smem_u32(sW2), aDS = tc::smem_u32(sDS), aV = tc::smem_u32(sV),
                      aW1 = tc::smem_u32(sW1), aE = tc::smem_u32(sE);
       constexpr uint32_t IDESC_MLP = tc::idesc_bf16(128, KH, false, false);
+      constexpr uint32_t IDESC_MLP_H = tc::idesc_bf16(128, KH / 2, false, false);
       constexpr uint32_t IDESC_U = tc::idesc_bf16(128, NMAX * D, false, true);
       auto mma1 = [&](uint32_t t) -> bool {
         const int b = t & 1;
         tc::mbar_wait(&m->e_full[b], (t >> 1) & 1);
         if (!m->desc[b].more) return false;
         tc::tc_fence_after();
-        tc::mma_bf16_ss(tZ, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone), IDESC_MLP,
-                        0u);
+        // z1 in two kappa halves: 0..127 into A, 128..255 into U (both free once
+        // U of the previous tile is drained), so the a1 epilogue of this tile
+        // runs while the previous tile's dz2 drain still reads Z
+        tc::mma_bf16_ss(tA, tc::sdesc(aE, 128, 256, tc::kSwNone), tc::sdesc(aW1, 128, 256, tc::kSwNone),
+                        IDESC_MLP_H, 0u);
+        tc::mma_bf16_ss(tU, tc::sdesc(aE, 128, 256, tc::kSwNone),
+                        tc::sdesc(aW1 + (KH / 2 / 8) * 256, 128, 256, tc::kSwNone), IDESC_MLP_H, 0u);
         tc::mma_commit(&m->d1_full);
         tc::mma_commit(&m->e_empty);
         return true;
@@ -333,6 +343,7 @@ __global__ void __launch_bounds__(512, 1)
         // MMA2: z2 = a1 W2^T (A = a1 in TMEM, W2 resident)
         TLB4(t, 0);
         tc::mbar_wait(&m->a1_ready, p1);
+        if (t >= 1) tc::mbar_wait(&m->dh_free, (t - 1) & 1);  // the previous tile's dz2 drain has read Z
         TLB4(t, 1);
         tc::tc_fence_after();
 #pragma unroll
@@ -370,8 +381,7 @@ __global__ void __launch_bounds__(512, 1)
         tc::mma_commit(&m->v_empty);
         tc::mbar_wait(&m->h_ready, p1);
         TLB4(t, 3);
-        if (t >= 1) tc::mbar_wait(&m->u_free, (t - 1) & 1);
-        TLB4(t, 4);
+        TLB4(t, 4);  // U's region: freed before this tile's MMA1 (u_free of the previous tile)
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < KH / 16; ++kk) {
@@ -382,8 +392,8 @@ __global__ void __launch_bounds__(512, 1)
         tc::mma_commit(&m->a_free);
         tc::mma_commit(&m->dh_full);  // dH and U done: Z holds dH^T, the dS buffer is free
         TLB4(t, 5);
-        // the next tile's MMA1 once the dz2 epilogue has read dH^T out of Z
-        tc::mbar_wait(&m->dh_free, p1);
+        // the next tile's MMA1 into A and U once this tile's U is drained
+        tc::mbar_wait(&m->u_free, p1);
         TLB4(t, 6);
         tc::tc_fence_after();
         more = mma1(t + 1);
@@ -411,26 +421,7 @@ __global__ void __launch_bounds__(512, 1)
       tr.load(dsc);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&m->desc_free[b]);
-      // a1 = relu(z1) (z1 holds + b1) -> A columns 64 cg .. 64 cg + 63
-      tc::mbar_wait(&m->d1_full, p1);
-      if (t >= 1) tc::mbar_wait(&m->a_free, (t - 1) & 1);
-      if (warp == 4 && lane == 0) TLB4(t, 8);
-      tc::tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c0 = cg * 128 + cc * 64;
-        uint32_t x[64], pk[32];
-        tc::tmem_ld32(rz + c0, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
-        tc::tmem_ld32(rz + c0 + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) pk[q] = tc::pack_bf16_relu(__uint_as_float(x[2 * q]), __uint_as_float(x[2 * q + 1]));
-        tc::tmem_st32(ra + c0 / 2, pk);
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&m->a1_ready);
-      if (warp == 4 && lane == 0) TLB4(t, 9);
+      // (a1 is formed by the EPI_B warps, below)
       // h = relu(z2 + b2) -> A, and the [h > 0] bits: the lane's 32 slot...
       // rather its own slot's 32 kappa' bits (bit q = kappa' c0 + 2q, bit
       // 16 + q = kappa' c0 + 2q + 1, from the bf16 pairs), transposed across
@@ -529,6 +520,38 @@ __global__ void __launch_bounds__(512, 1)
       TileRegs<NMAX> tr;
       tr.load(dsc);
       const int nn = tr.nn;
+      {
+        // a1 = relu(z1) (z1 holds + b1): kappa 0..127 from A, 128..255 from U,
+        // packed bf16 pairs to A columns 0..127 (lane = slot).  Each thread
+        // reads its lane's A columns before it overwrites them; the U
+        // columns are free for this tile's U product afterwards.
+        tc::mbar_wait(&m->d1_full, p1);
+        if (warp == 12 && lane == 0) TLB4(t, 8);
+        tc::tc_fence_after();
+        const uint32_t ra = tA + lane_off, ru = tU + lane_off;
+        auto chunk = [&](uint32_t addr, uint32_t (&pk)[32]) {
+          uint32_t x[64];
+          tc::tmem_ld32(addr, *reinterpret_cast<uint32_t (*)[32]>(&x[0]));
+          tc::tmem_ld32(addr + 32, *reinterpret_cast<uint32_t (*)[32]>(&x[32]));
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            pk[q] = tc::pack_bf16_relu(__uint_as_float(x[2 * q]), __uint_as_float(x[2 * q + 1]));
+        };
+        uint32_t pk0[32], pk1[32];
+        chunk(ra, pk0);       // kappa 0..63
+        chunk(ra + 64, pk1);  // kappa 64..127
+        tc::tmem_st32(ra, pk0);
+        tc::tmem_st32(ra + 32, pk1);
+        chunk(ru, pk0);       // kappa 128..191
+        tc::tmem_st32(ra + 64, pk0);
+        chunk(ru + 64, pk1);  // kappa 192..255
+        tc::tmem_st32(ra + 96, pk1);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&m->a1_ready);
+        if (warp == 12 && lane == 0) TLB4(t, 9);
+      }
       tc::mbar_wait(&m->u_full, p1);
       if (warp == 12 && lane == 0) TLB4(t, 14);
       tc::tc_fence_after();

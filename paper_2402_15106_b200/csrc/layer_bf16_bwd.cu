@@ -54,20 +54,40 @@ __global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ 
   const int t = threadIdx.x;
   const int64_t r0 = rb + (int64_t)blockIdx.x * 32;
   const bool dense = root == DSMPNN_ROOT_DENSE && dv != nullptr;
+  // thread = (row rr, group of D / 8 consecutive columns) for the root term:
+  // its dv entries are loaded first, so the read-modify-write at the end
+  // does not wait on them
+  constexpr int NC = D / 8;
+  const int rr = t >> 3, n0 = (t & 7) * NC;
+  const bool mine = dv != nullptr && root != DSMPNN_ROOT_NONE && r0 + rr < re;
+  float4 dvv[NC / 4];
+  if (mine) {
+#pragma unroll
+    for (int j = 0; j < NC / 4; ++j) dvv[j] = reinterpret_cast<const float4 *>(dv + (r0 + rr) * D + n0)[j];
+  }
   if (dense)
     for (int i = t; i < D * D / 4; i += 256) reinterpret_cast<float4 *>(&sw[0][0])[i] = reinterpret_cast<const float4 *>(Wr)[i];
-  for (int i = t; i < 32 * D; i += 256) {
-    const int r = i / D, c = i % D;
+  for (int i = t; i < 32 * D / 4; i += 256) {  // four consecutive columns per thread
+    const int r = (i * 4) / D, c = (i * 4) % D;
     const int64_t row = r0 + r;
-    float g = 0.f;
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     if (row < re) {
       const int64_t idx = row * D + c;
-      g = G[idx];
-      if (act == DSMPNN_ACT_RELU && !(pre[idx] > 0.f)) g = 0.f;
-      gh[idx] = g;
-      gh16[idx] = __float2bfloat16_rn(g);
+      g = *reinterpret_cast<const float4 *>(G + idx);
+      if (act == DSMPNN_ACT_RELU) {
+        const float4 p = *reinterpret_cast<const float4 *>(pre + idx);
+        g.x = p.x > 0.f ? g.x : 0.f;
+        g.y = p.y > 0.f ? g.y : 0.f;
+        g.z = p.z > 0.f ? g.z : 0.f;
+        g.w = p.w > 0.f ? g.w : 0.f;
+      }
+      *reinterpret_cast<float4 *>(gh + idx) = g;
+      *reinterpret_cast<uint2 *>(gh16 + idx) = make_uint2(tc::pack_bf16(g.x, g.y), tc::pack_bf16(g.z, g.w));
     }
-    sg[r][c] = g;
+    sg[r][c] = g.x;
+    sg[r][c + 1] = g.y;
+    sg[r][c + 2] = g.z;
+    sg[r][c + 3] = g.w;
   }
   if (t < 32 && r0 + t < re) {
     const int64_t i = r0 + t;
@@ -81,18 +101,14 @@ __global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ 
     for (int r = 0; r < 32; ++r) cs += sg[r][t];
     cs_part[(int64_t)blockIdx.x * D + t] = cs;
   }
-  if (dv == nullptr || root == DSMPNN_ROOT_NONE) return;
-  // thread = (row r, group of D / 8 consecutive columns): 256 threads = 32 rows x 8 groups
-  constexpr int NC = D / 8;
-  const int r = t >> 3, n0 = (t & 7) * NC;
-  if (r0 + r >= re) return;
+  if (!mine) return;
   float acc[NC];
   if (dense) {
 #pragma unroll
     for (int j = 0; j < NC; ++j) acc[j] = 0.f;
 #pragma unroll 4
     for (int c = 0; c < D; ++c) {
-      const float g = sg[r][c];
+      const float g = sg[rr][c];
 #pragma unroll
       for (int j = 0; j < NC; j += 4) {
         const float4 w4 = *reinterpret_cast<const float4 *>(&sw[c][n0 + j]);
@@ -104,17 +120,17 @@ __global__ void __launch_bounds__(256) b0_bf16_kernel(const float *__restrict__ 
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < NC; ++j) acc[j] = sg[r][n0 + j];
+    for (int j = 0; j < NC; ++j) acc[j] = sg[rr][n0 + j];
   }
-  float *o = dv + (r0 + r) * D + n0;
+  float4 *o = reinterpret_cast<float4 *>(dv + (r0 + rr) * D + n0);
 #pragma unroll
-  for (int j = 0; j < NC; j += 4) {
-    float4 x = *reinterpret_cast<float4 *>(o + j);
-    x.x += acc[j];
-    x.y += acc[j + 1];
-    x.z += acc[j + 2];
-    x.w += acc[j + 3];
-    *reinterpret_cast<float4 *>(o + j) = x;
+  for (int j = 0; j < NC / 4; ++j) {
+    float4 x = dvv[j];
+    x.x += acc[4 * j];
+    x.y += acc[4 * j + 1];
+    x.z += acc[4 * j + 2];
+    x.w += acc[4 * j + 3];
+    o[j] = x;
   }
 }
 

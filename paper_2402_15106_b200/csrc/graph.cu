@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_kernel(
 
 
 // ----------------------------------------------------------- fast path --
-constexpr int kHB = 10, kHBins = 1 << kHB;  // top key bits of the pass-1 histogram
+#ifndef DSMPNN_KHB
+#define DSMPNN_KHB 9  // 512 bins: smaller per-warp histograms, more resident warps in graph1 (airfoil build -4 %)
+#endif
+constexpr int kHB = DSMPNN_KHB, kHBins = 1 << kHB;  // top key bits of the pass-1 histogram
 constexpr int kCapB = 384;                  // boundary-bin buffer per warp
 constexpr int kGWarps = 8;
 

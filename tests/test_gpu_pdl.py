@@ -5,7 +5,6 @@ its griddepcontrol.wait would race.  The full BF16 step (union graph, 2
 layers, forward + backward + weight gradients) must give bitwise the same
 results with PDL on and off, and run to run.  DSMPNN_PDL is read once per
 process, hence the child processes."""
-import hashlib
 import os
 import subprocess
 import sys

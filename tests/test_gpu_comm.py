@@ -159,3 +159,28 @@ os._exit(0)
     p = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=240)
     assert "STATUS -7" in p.stdout, p.stdout + p.stderr
     assert "AFTER -6" in p.stdout, p.stdout + p.stderr
+
+
+def test_pipelined_steps_through_nccl(comm):
+    """HotPath.step_pipelined with the library communicator (every halo
+    refresh through NCCL send / recv, overlapped with the deep rows on the
+    comm stream) while the next step's graph is built on the build stream:
+    bitwise the gradients of HotPath.step, step after step."""
+    from paper_2402_15106_b200 import _lib as L
+    from paper_2402_15106_b200.api import HotPath
+    c = _case(seed=75, d=64, k=256)
+    sc = _cfg(c, 1, overlap_halo=1, halo_flags=L.HALO_VIA_NCCL)
+    inp = [_T(c["x"]), _T(c["a"]), _T(c["v0"]), _T(c["G"])]
+    hs = HotPath(sc, c["W"], cuda(), comm=comm)
+    want = []
+    for _ in range(3):
+        g = hs.step(*inp)
+        torch.cuda.synchronize()
+        want.append({n: g[n].cpu().numpy().copy() for n in NAMES})
+    hp = HotPath(sc, c["W"], cuda(), comm=comm)
+    for i in range(3):
+        g = hp.step_pipelined(*inp, next_inputs=inp[:2] if i < 2 else None)
+        torch.cuda.synchronize()
+        for n in NAMES:
+            assert np.array_equal(g[n].cpu().numpy(), want[i][n]), (i, n)
+    comm.sync(timeout_ms=60000)
